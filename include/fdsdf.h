@@ -1,0 +1,203 @@
+/*
+ * fdsdf.h -- C ABI of the B200-native finite-difference curvature step for neural SDFs
+ * (arXiv 2511.08980, "A Finite Difference Approximation of Second Order Regularization
+ * of Neural-SDFs").
+ *
+ * Citation keys: P:Lx = PAPER.md line x (section / equation named beside it);
+ * S:Lx = SPEC.md line x; SURVEY = /root/repo/SURVEY.md.
+ *
+ * What the library computes (§3):
+ *   f        : the SDF MLP (SIREN or softplus), evaluated at a centre x0;
+ *   g        : grad_x f(x0) (n = g/|g|);
+ *   (u, v)   : a uniformly random orthonormal completion of n;
+ *   f_uu, f_vv, f_uv : the central-difference stencils of P:L83-91 (§3.1) over the 9
+ *              points x0, x0 +- h u, x0 +- h v, x0 +- h u +- h v;
+ *   D_FD     : f_uu f_vv - f_uv^2 (§3.3);
+ *   K_FD     : D_FD / |g|^p, p = 4 (§3.2), with |g| replaced by 1 on near-surface
+ *              (surface-role) rows under FDSDF_DENOM_PAPER (§3.4);
+ *   loss     : Eq. (1): w_dm L_DM + l_dnm L_DNM + l_eik L_eik + l_fd L_fd,
+ *              forms of the first three from S:L278 / S:L296 / S:L287;
+ *   grad     : d loss / d params, frames and the degenerate mask held fixed.
+ *
+ * Conventions (all entry points):
+ *   - d_* pointers are DEVICE memory owned by the caller; h_* pointers are host memory.
+ *   - fdsdf_eval / fdsdf_step / fdsdf_allreduce are asynchronous: work is enqueued on the
+ *     caller's stream (cudaStream_t passed as void*; NULL = legacy default stream).  Their
+ *     status covers host-side validation and launch errors only.  Device-detected
+ *     conditions are latched in sticky per-context flags (fdsdf_get_device_flags).
+ *   - No allocation happens after fdsdf_create; n > max_centers -> FDSDF_E_INVALID.
+ *   - Parameters are read-only during a call.  One context per host thread / stream.
+ *   - Determinism: same inputs, same device count -> bitwise identical outputs (fixed
+ *     reduction orders; frames are a pure function of (seed, global index)).
+ *   - Errors: invalid argument -> FDSDF_E_INVALID (nothing enqueued); n == 0, or an empty
+ *     role with a positive weight -> FDSDF_E_EMPTY; CUDA launch failure -> FDSDF_E_CUDA;
+ *     NCCL failure -> FDSDF_E_NCCL.  fdsdf_last_error() returns a message for the last
+ *     failure on that context.
+ *
+ * Flat parameter layout: layer-major; for each linear layer l:
+ *   W_l row-major [out_l][in_l], then b_l[out_l];  in_l = width[l] (+3 if l == skip_at,
+ *   whose input is cat(a, x)/sqrt(2)); out_l = width[l+1].  Hidden layers apply
+ *   sin(omega_l * (W a + b)) (SINE; omega_0 = omega0_first, omega_l = omega0_hidden) or
+ *   softplus_beta(W a + b) = log(1 + exp(beta z))/beta (SOFTPLUS, exact, no threshold);
+ *   the last layer is linear.
+ */
+#ifndef FDSDF_H
+#define FDSDF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDSDF_MAX_LINEAR 16   /* at most 16 linear layers                          */
+#define FDSDF_MAX_WIDTH 512   /* hidden widths 1..512 (skip fan-in width+3 <= 512)  */
+
+typedef enum {
+  FDSDF_OK = 0,
+  FDSDF_E_INVALID = 1,     /* bad argument; nothing was enqueued                     */
+  FDSDF_E_EMPTY = 2,       /* n == 0, or an empty role set whose weight is > 0       */
+  FDSDF_E_CUDA = 3,        /* CUDA runtime / launch failure                          */
+  FDSDF_E_NCCL = 4,        /* NCCL missing or failed                                 */
+  FDSDF_E_NOMEM = 5,       /* workspace allocation failed in fdsdf_create            */
+  FDSDF_E_UNSUPPORTED = 6  /* e.g. no sm_100 device, or comm not initialised         */
+} fdsdf_status;
+
+enum { FDSDF_ACT_SOFTPLUS = 0, FDSDF_ACT_SINE = 1 };
+
+/* MLP description.  width[0] = 3, width[n_linear] = 1. */
+typedef struct {
+  int32_t n_linear;                        /* number of linear layers, 2..16              */
+  int32_t width[FDSDF_MAX_LINEAR + 1];     /* width[0..n_linear]                          */
+  int32_t act;                             /* FDSDF_ACT_*                                 */
+  float beta;                              /* softplus beta > 0 (P:L153 setups: 100)      */
+  float omega0_first;                      /* SIREN omega of layer 0 (> 0), 30            */
+  float omega0_hidden;                     /* SIREN omega of later hidden layers (> 0)    */
+  int32_t skip_at;                         /* -1, or layer in [1, n_linear-2] whose input */
+                                           /* is cat(a, x)/sqrt(2)                         */
+} fdsdf_mlp_spec;
+
+enum { FDSDF_FRAME_RANDOM = 0, FDSDF_FRAME_GIVEN = 1 };
+enum { FDSDF_DENOM_PAPER = 0, FDSDF_DENOM_ONE = 1, FDSDF_DENOM_GRAD = 2 };
+
+/* Stencil / frame configuration. */
+typedef struct {
+  float h;                    /* FD step, finite and > 0                           */
+  uint64_t frame_seed;        /* RANDOM frames: theta = 2 pi U, U from SplitMix64 over      */
+                              /* (frame_seed, global index)               */
+  int64_t index_offset;       /* global index of row 0 (data-parallel shards)               */
+  int32_t frame_mode;         /* FDSDF_FRAME_RANDOM or FDSDF_FRAME_GIVEN                    */
+  const float* d_frames_in;   /* GIVEN: [n][6] = (u, v) per row, device; else NULL          */
+  float eps_grad;             /* degenerate mask m = [|g| >= eps_grad], 1e-6       */
+  int32_t denom;              /* FDSDF_DENOM_*: den of K_FD                                  */
+  int32_t denom_pow;          /* p in |g|^p (P:L112 prints 4)                               */
+  int64_t n_surface;          /* rows [0, n_surface) are surface-role                       */
+} fdsdf_stencil;
+
+/* Optional per-row outputs of fdsdf_eval; every pointer may be NULL ("do not write"). */
+typedef struct {
+  float* d_f;        /* [n]     f(x0)                                                      */
+  float* d_grad;     /* [n][3]  grad f(x0)                                                 */
+  float* d_hess;     /* [n][3]  (f_uu, f_uv, f_vv)                             */
+  float* d_K;        /* [n]     K_FD (0 on masked rows)                                    */
+  float* d_D;        /* [n]     D_FD                                                       */
+  float* d_frames;   /* [n][6]  (u, v) used (0 on masked rows)                             */
+  uint8_t* d_mask;   /* [n]     1 = |g| >= eps_grad                                        */
+} fdsdf_eval_out;
+
+enum { FDSDF_LOSS_NCR = 0, FDSDF_LOSS_NSH = 1 };   /* Q = K_FD or D_FD */
+enum { FDSDF_FD_ABS = 0, FDSDF_FD_SQUARE = 1 };    /* L_fd = mean m|Q| or mean m Q^2     */
+
+/* Loss configuration (Eq. (1)).  Denominators are the GLOBAL counts so that a
+ * plain SUM over data-parallel ranks gives the global loss and gradient. */
+typedef struct {
+  int32_t kind;                 /* FDSDF_LOSS_*                                           */
+  int32_t fd_form;              /* FDSDF_FD_*                                             */
+  float w_dm;                   /* weight of L_DM = mean_surface |f|            (>= 0)    */
+  float lambda_dnm;             /* weight of L_DNM = mean_uniform exp(-alpha|f|) (>= 0)   */
+  float alpha_dnm;              /* alpha > 0 (100)                                */
+  float lambda_eik;             /* weight of L_eik = mean_all (|g| - 1)^2       (>= 0)    */
+  float lambda_fd;              /* weight of L_fd                               (>= 0)    */
+  int64_t n_surface_global;     /* N_s                                                    */
+  int64_t n_uniform_global;     /* N_u                                                    */
+  int64_t n_global;             /* N                                                      */
+} fdsdf_loss;
+
+enum {
+  FDSDF_STEP_ACCUMULATE = 1u,   /* d_grad += instead of =                                  */
+  FDSDF_STEP_ALLREDUCE = 2u     /* NCCL SUM of d_grad and d_loss after the step (same      */
+                                /* stream); requires fdsdf_comm_init                       */
+};
+
+enum {                          /* sticky device flags                                     */
+  FDSDF_FLAG_NONFINITE_INPUT = 1u,  /* a centre coordinate was not finite          */
+  FDSDF_FLAG_NONFINITE_LOSS = 2u,   /* the loss was not finite                     */
+  FDSDF_FLAG_ALL_FD_SKIPPED = 4u    /* every centre was masked: L_fd = 0           */
+};
+
+typedef struct fdsdf_ctx fdsdf_ctx;
+
+/* Build a context for `spec` on CUDA `device` with workspace for up to `max_centers` rows
+ * per call.  flags: 0, or FDSDF_CREATE_EVAL_ONLY (no step workspace).
+ * Errors: invalid spec (width out of range, < 2 layers, beta/omega <= 0, skip_at out of
+ * range) -> FDSDF_E_INVALID; no sm_100 device -> FDSDF_E_UNSUPPORTED;
+ * allocation failure -> FDSDF_E_NOMEM.  *out is NULL on failure. */
+enum { FDSDF_CREATE_EVAL_ONLY = 1u };
+fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_centers,
+                          uint32_t flags, fdsdf_ctx** out);
+
+/* Validate a spec without touching any GPU (host only). */
+fdsdf_status fdsdf_validate_spec(const fdsdf_mlp_spec* spec);
+
+/* Free the context and its workspace (the caller's buffers are untouched).  NULL is a no-op. */
+void fdsdf_destroy(fdsdf_ctx* ctx);
+
+/* Number of parameters P of a spec, and the flat offset of W_layer (is_bias = 0) or
+ * b_layer (is_bias = 1); -1 on an invalid spec / layer.  Host only. */
+int64_t fdsdf_spec_num_params(const fdsdf_mlp_spec* spec);
+int64_t fdsdf_spec_param_offset(const fdsdf_mlp_spec* spec, int layer, int is_bias);
+int64_t fdsdf_num_params(const fdsdf_ctx* ctx);
+
+/* Forward only: f, grad f, the FD tangent Hessian entries, D_FD, K_FD, frames and mask for
+ * n centres d_x [n][3] (fp32, device) with params d_params [P] (fp32, device).
+ * Errors: ctx/d_params/d_x NULL, n > max_centers, h <= 0 or non-finite, eps_grad < 0,
+ * denom/frame_mode out of range, GIVEN without d_frames_in -> FDSDF_E_INVALID;
+ * n == 0 -> FDSDF_E_EMPTY. */
+fdsdf_status fdsdf_eval(fdsdf_ctx* ctx, const float* d_params, const float* d_x, int64_t n,
+                        const fdsdf_stencil* st, const fdsdf_eval_out* out, void* stream);
+
+/* One training step: the loss of Eq. (1) and its gradient with respect to every parameter.
+ * d_grad [P] fp32 (overwritten, or accumulated with FDSDF_STEP_ACCUMULATE);
+ * d_loss [8] fp64 = (L_DM, L_DNM, L_eik, L_fd, total, n_degenerate, 0, 0), each term
+ * already divided by its global count (so it is SUM-reducible across ranks).
+ * Errors: as fdsdf_eval, plus ctx created EVAL_ONLY, d_grad/d_loss NULL, negative or
+ * non-finite weights, alpha <= 0, global counts smaller than the local ones ->
+ * FDSDF_E_INVALID; an empty role with positive weight -> FDSDF_E_EMPTY;
+ * ALLREDUCE without fdsdf_comm_init -> FDSDF_E_UNSUPPORTED. */
+fdsdf_status fdsdf_step(fdsdf_ctx* ctx, const float* d_params, const float* d_x, int64_t n,
+                        const fdsdf_stencil* st, const fdsdf_loss* ls, float* d_grad,
+                        double* d_loss, uint32_t flags, void* stream);
+
+/* Data-parallel plumbing: rank 0 calls fdsdf_comm_unique_id, the caller
+ * broadcasts the 128 bytes (e.g. through its torch process group), every rank calls
+ * fdsdf_comm_init.  NCCL is loaded at run time (libnccl.so.2); missing -> FDSDF_E_NCCL.
+ * fdsdf_allreduce: in-place SUM of count fp32 elements on the stream. */
+fdsdf_status fdsdf_comm_unique_id(uint8_t id[128]);
+fdsdf_status fdsdf_comm_init(fdsdf_ctx* ctx, const uint8_t id[128], int rank, int world);
+fdsdf_status fdsdf_allreduce(fdsdf_ctx* ctx, float* d_buf, int64_t count, void* stream);
+
+/* Diagnostics (synchronous). */
+const char* fdsdf_status_string(fdsdf_status s);
+const char* fdsdf_last_error(const fdsdf_ctx* ctx);
+/* Returns and clears the sticky device flags (synchronises the context's device). */
+fdsdf_status fdsdf_get_device_flags(fdsdf_ctx* ctx, uint32_t* out);
+/* Number of kernel launches enqueued by the last eval/step call on this context. */
+int32_t fdsdf_last_launch_count(const fdsdf_ctx* ctx);
+/* Library version string. */
+const char* fdsdf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDSDF_H */

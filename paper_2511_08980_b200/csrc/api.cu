@@ -1,0 +1,525 @@
+// api.cu -- the C ABI (include/fdsdf.h): validation, workspace, launch sequencing, NCCL.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/fdsdf.h"
+#include "kernels.cuh"
+
+
+using namespace fdsdf;
+
+namespace {
+
+struct NcclApi {
+  void* lib = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, const void*, int) = nullptr;  // id passed by value: see wrapper
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*groupStart)() = nullptr;
+  int (*groupEnd)() = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+};
+
+NcclApi g_nccl;
+
+bool nccl_load(std::string* err) {
+  if (g_nccl.lib) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    if (err) *err = std::string("cannot load libnccl.so.2: ") + dlerror();
+    return false;
+  }
+  g_nccl.getUniqueId = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
+  g_nccl.commInitRank = (int (*)(void**, int, const void*, int))dlsym(h, "ncclCommInitRank");
+  g_nccl.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
+  g_nccl.groupStart = (int (*)())dlsym(h, "ncclGroupStart");
+  g_nccl.groupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+  g_nccl.commDestroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+  g_nccl.getErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.groupStart || !g_nccl.groupEnd) {
+    if (err) *err = "libnccl.so.2 lacks required symbols";
+    return false;
+  }
+  g_nccl.lib = h;
+  return true;
+}
+
+struct NcclId {
+  char internal[128];
+};
+
+// ncclCommInitRank takes ncclUniqueId by value (a 128-byte struct): call through a typed pointer
+typedef int (*CommInitRankFn)(void**, int, NcclId, int);
+
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0;
+
+}  // namespace
+
+struct fdsdf_ctx {
+  int device = 0;
+  fdsdf_mlp_spec spec{};
+  Net net{};          // pointers filled per call
+  int L = 0, mpad = 0, nh = 0, ngemm = 0;
+  int64_t P = 0;
+  int64_t offW[FDSDF_MAX_LINEAR]{}, offb[FDSDF_MAX_LINEAR]{};
+  int64_t max_centers = 0;
+  bool eval_only = false;
+  int nsm = 0, fgrid = 0, bgrid = 0, ftile = 0, btile = 0, nsplit = 1;
+  int64_t nacc = 0;
+  // workspace
+  float* wt = nullptr;
+  float* wb = nullptr;
+  float* zf = nullptr;       // step workspace
+  float* zscr = nullptr;     // eval scratch (per CTA)
+  float* seed = nullptr;
+  double* lossp = nullptr;
+  float* del = nullptr;
+  float* actv = nullptr;
+  float* bacc = nullptr;
+  float* part = nullptr;
+  unsigned* dflags = nullptr;
+  void* comm = nullptr;
+  int rank = 0, world = 1;
+  int launches = 0;
+  std::string err;
+};
+
+static fdsdf_status fail(fdsdf_ctx* c, fdsdf_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+static fdsdf_status cuda_fail(fdsdf_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, FDSDF_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+static int layer_fan_in(const fdsdf_mlp_spec* s, int l) { return s->width[l] + (l == s->skip_at ? 3 : 0); }
+
+extern "C" {
+
+const char* fdsdf_version(void) { return "fdsdf 0.1 (sm_100a, pair-symmetric difference form, fp32 FFMA)"; }
+
+const char* fdsdf_status_string(fdsdf_status s) {
+  switch (s) {
+    case FDSDF_OK: return "ok";
+    case FDSDF_E_INVALID: return "invalid argument";
+    case FDSDF_E_EMPTY: return "empty input";
+    case FDSDF_E_CUDA: return "CUDA error";
+    case FDSDF_E_NCCL: return "NCCL error";
+    case FDSDF_E_NOMEM: return "out of device memory";
+    case FDSDF_E_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+fdsdf_status fdsdf_validate_spec(const fdsdf_mlp_spec* s) {
+  if (!s) return FDSDF_E_INVALID;
+  const int L = s->n_linear;
+  if (L < 2 || L > FDSDF_MAX_LINEAR) return FDSDF_E_INVALID;
+  if (s->width[0] != 3 || s->width[L] != 1) return FDSDF_E_INVALID;
+  for (int l = 1; l < L; ++l)
+    if (s->width[l] < 1 || s->width[l] > FDSDF_MAX_WIDTH) return FDSDF_E_INVALID;
+  if (s->act != FDSDF_ACT_SINE && s->act != FDSDF_ACT_SOFTPLUS) return FDSDF_E_INVALID;
+  if (s->act == FDSDF_ACT_SOFTPLUS && !(s->beta > 0.f && std::isfinite(s->beta))) return FDSDF_E_INVALID;
+  if (s->act == FDSDF_ACT_SINE && !(s->omega0_first > 0.f && s->omega0_hidden > 0.f &&
+                                    std::isfinite(s->omega0_first) && std::isfinite(s->omega0_hidden)))
+    return FDSDF_E_INVALID;
+  if (s->skip_at != -1) {
+    if (s->skip_at < 1 || s->skip_at > L - 2) return FDSDF_E_INVALID;
+    if (s->width[s->skip_at] + 3 > FDSDF_MAX_WIDTH) return FDSDF_E_INVALID;
+  }
+  return FDSDF_OK;
+}
+
+int64_t fdsdf_spec_num_params(const fdsdf_mlp_spec* s) {
+  if (fdsdf_validate_spec(s) != FDSDF_OK) return -1;
+  int64_t P = 0;
+  for (int l = 0; l < s->n_linear; ++l) P += (int64_t)s->width[l + 1] * layer_fan_in(s, l) + s->width[l + 1];
+  return P;
+}
+
+int64_t fdsdf_spec_param_offset(const fdsdf_mlp_spec* s, int layer, int is_bias) {
+  if (fdsdf_validate_spec(s) != FDSDF_OK || layer < 0 || layer >= s->n_linear) return -1;
+  int64_t off = 0;
+  for (int l = 0; l < layer; ++l) off += (int64_t)s->width[l + 1] * layer_fan_in(s, l) + s->width[l + 1];
+  if (is_bias) off += (int64_t)s->width[layer + 1] * layer_fan_in(s, layer);
+  return off;
+}
+
+int64_t fdsdf_num_params(const fdsdf_ctx* c) { return c ? c->P : -1; }
+const char* fdsdf_last_error(const fdsdf_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int32_t fdsdf_last_launch_count(const fdsdf_ctx* c) { return c ? c->launches : 0; }
+
+void fdsdf_destroy(fdsdf_ctx* c) {
+  if (!c) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  void* bufs[] = {c->wt, c->wb, c->zf, c->zscr, c->seed, c->lossp, c->del, c->actv, c->bacc, c->part, c->dflags};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  cudaSetDevice(prev);
+  delete c;
+}
+
+fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_centers, uint32_t flags,
+                          fdsdf_ctx** out) {
+  if (!out) return FDSDF_E_INVALID;
+  *out = nullptr;
+  if (fdsdf_validate_spec(spec) != FDSDF_OK) return FDSDF_E_INVALID;
+  if (max_centers < 1) return FDSDF_E_INVALID;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return FDSDF_E_UNSUPPORTED;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return FDSDF_E_UNSUPPORTED;
+  if (prop.major != 10) return FDSDF_E_UNSUPPORTED;  // built for sm_100a only
+
+  fdsdf_ctx* c = new fdsdf_ctx();
+  c->device = device;
+  c->spec = *spec;
+  c->L = spec->n_linear;
+  c->nh = c->L - 1;
+  c->ngemm = c->L - 2;
+  int wmax = 1;
+  for (int l = 1; l < c->L; ++l) wmax = std::max(wmax, spec->width[l]);
+  if (spec->skip_at >= 0) wmax = std::max(wmax, spec->width[spec->skip_at] + 3);
+  c->mpad = wmax <= 64 ? 64 : (wmax <= 128 ? 128 : (wmax <= 256 ? 256 : 512));
+  c->P = fdsdf_spec_num_params(spec);
+  for (int l = 0; l < c->L; ++l) {
+    c->offW[l] = fdsdf_spec_param_offset(spec, l, 0);
+    c->offb[l] = fdsdf_spec_param_offset(spec, l, 1);
+  }
+  c->max_centers = max_centers;
+  c->eval_only = (flags & FDSDF_CREATE_EVAL_ONLY) != 0;
+  c->nsm = prop.multiProcessorCount;
+  c->ftile = fwd_tile_centres(c->mpad);
+  c->btile = bwd_tile_centres(c->mpad);
+
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  // occupancy-derived persistent grids
+  c->fgrid = c->nsm * 2;
+  c->bgrid = c->nsm * 2;
+  {
+    const size_t fs = fwd_smem_bytes(c->mpad), bs = bwd_smem_bytes(c->mpad);
+    const size_t per_sm = (size_t)prop.sharedMemPerMultiprocessor;
+    const int fo = (int)std::max<size_t>(1, std::min<size_t>(2, per_sm / (fs + 1024)));
+    const int bo = (int)std::max<size_t>(1, std::min<size_t>(2, per_sm / (bs + 1024)));
+    c->fgrid = c->nsm * fo;
+    c->bgrid = c->nsm * bo;
+  }
+  const int mp = c->mpad;
+  const int64_t ftile_cap = (max_centers + c->ftile - 1) / c->ftile;
+  const int64_t btile_cap = (max_centers + c->btile - 1) / c->btile;
+  c->fgrid = (int)std::min<int64_t>(c->fgrid, ftile_cap);
+  c->bgrid = (int)std::min<int64_t>(c->bgrid, btile_cap);
+  c->nacc = bacc_size(c->L, mp);
+  const int nb = (mp >= 128 ? mp / 128 : 1);
+  c->nsplit = std::max(1, (int)std::min<int64_t>((4 * c->nsm + c->ngemm * nb * nb - 1) / std::max(1, c->ngemm * nb * nb),
+                                                  (max_centers * NCOLB + 255) / 256));
+  auto alloc = [&](void** p, size_t bytes) -> bool {
+    if (bytes == 0) return true;
+    return cudaMalloc(p, bytes) == cudaSuccess;
+  };
+  bool ok = true;
+  const size_t gemm_w = (size_t)std::max(0, c->ngemm) * mp * mp * sizeof(float);
+  ok = ok && alloc((void**)&c->wt, gemm_w);
+  ok = ok && alloc((void**)&c->wb, gemm_w);
+  ok = ok && alloc((void**)&c->zscr, (size_t)c->fgrid * c->ftile * c->nh * mp * sizeof(float));
+  ok = ok && alloc((void**)&c->lossp, (size_t)c->fgrid * NLOSS * sizeof(double));
+  ok = ok && alloc((void**)&c->dflags, sizeof(unsigned));
+  if (ok && !c->eval_only) {
+    ok = ok && alloc((void**)&c->zf, (size_t)max_centers * c->nh * NCOLF * mp * sizeof(float));
+    ok = ok && alloc((void**)&c->seed, (size_t)max_centers * NSEED * sizeof(float));
+    ok = ok && alloc((void**)&c->del, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
+    ok = ok && alloc((void**)&c->actv, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
+    ok = ok && alloc((void**)&c->bacc, (size_t)c->bgrid * c->nacc * sizeof(float));
+    ok = ok && alloc((void**)&c->part, (size_t)std::max(0, c->ngemm) * c->nsplit * mp * mp * sizeof(float));
+  }
+  if (ok) ok = cudaMemset(c->dflags, 0, sizeof(unsigned)) == cudaSuccess;
+  cudaSetDevice(prev);
+  if (!ok) {
+    cudaGetLastError();
+    fdsdf_destroy(c);
+    return FDSDF_E_NOMEM;
+  }
+  *out = c;
+  return FDSDF_OK;
+}
+
+}  // extern "C"
+
+static void fill_net(fdsdf_ctx* c, const float* d_params) {
+  Net& n = c->net;
+  n.L = c->L;
+  n.skip = c->spec.skip_at;
+  n.act = c->spec.act == FDSDF_ACT_SINE ? ACT_SINE : ACT_SOFTPLUS;
+  n.mpad = c->mpad;
+  n.beta = c->spec.act == FDSDF_ACT_SOFTPLUS ? c->spec.beta : 1.0f;
+  for (int l = 0; l <= c->L; ++l) n.width[l] = c->spec.width[l];
+  for (int l = 0; l < c->L; ++l) {
+    n.omega[l] = (c->spec.act == FDSDF_ACT_SINE && l < c->L - 1)
+                     ? (l == 0 ? c->spec.omega0_first : c->spec.omega0_hidden)
+                     : 1.0f;
+    n.W[l] = d_params + c->offW[l];
+    n.b[l] = d_params + c->offb[l];
+    n.Wt[l] = (l >= 1 && l <= c->L - 2) ? c->wt + (size_t)(l - 1) * c->mpad * c->mpad : nullptr;
+    n.Wb[l] = (l >= 1 && l <= c->L - 2) ? c->wb + (size_t)(l - 1) * c->mpad * c->mpad : nullptr;
+  }
+}
+
+static fdsdf_status check_common(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n,
+                                 const fdsdf_stencil* st) {
+  if (!c) return FDSDF_E_INVALID;
+  if (!d_params || !d_x || !st) return fail(c, FDSDF_E_INVALID, "null pointer argument");
+  if (n < 0 || n > c->max_centers) return fail(c, FDSDF_E_INVALID, "n out of range [0, max_centers]");
+  if (n == 0) return fail(c, FDSDF_E_EMPTY, "n == 0");
+  if (!(st->h > 0.f) || !std::isfinite(st->h)) return fail(c, FDSDF_E_INVALID, "h must be finite and > 0");
+  if (!(st->eps_grad >= 0.f) || !std::isfinite(st->eps_grad)) return fail(c, FDSDF_E_INVALID, "eps_grad must be >= 0");
+  if (st->denom < 0 || st->denom > 2) return fail(c, FDSDF_E_INVALID, "denom out of range");
+  if (st->denom_pow < 0 || st->denom_pow > 16) return fail(c, FDSDF_E_INVALID, "denom_pow out of range");
+  if (st->frame_mode != FDSDF_FRAME_RANDOM && st->frame_mode != FDSDF_FRAME_GIVEN)
+    return fail(c, FDSDF_E_INVALID, "frame_mode out of range");
+  if (st->frame_mode == FDSDF_FRAME_GIVEN && !st->d_frames_in)
+    return fail(c, FDSDF_E_INVALID, "GIVEN frames without d_frames_in");
+  if (st->n_surface < 0 || st->n_surface > n) return fail(c, FDSDF_E_INVALID, "n_surface out of range [0, n]");
+  if (st->index_offset < 0) return fail(c, FDSDF_E_INVALID, "index_offset < 0");
+  return FDSDF_OK;
+}
+
+static void fill_fwd(fdsdf_ctx* c, FwdArgs& a, const float* d_x, int64_t n, const fdsdf_stencil* st) {
+  a.net = c->net;
+  a.x = d_x;
+  a.n = n;
+  a.n_surface = st->n_surface;
+  a.index_offset = st->index_offset;
+  a.frame_seed = st->frame_seed;
+  a.frame_given = st->frame_mode == FDSDF_FRAME_GIVEN;
+  a.frames_in = st->d_frames_in;
+  a.h = st->h;
+  a.dflags = c->dflags;
+  a.lossp = c->lossp;
+  a.ntiles = (n + c->ftile - 1) / c->ftile;
+  a.ls.denom = st->denom;
+  a.ls.denom_pow = st->denom_pow;
+  a.ls.eps_grad = st->eps_grad;
+}
+
+extern "C" {
+
+fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
+                        const fdsdf_eval_out* out, void* stream) {
+  fdsdf_status s = check_common(c, d_params, d_x, n, st);
+  if (s != FDSDF_OK) return s;
+  cudaStream_t strm = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != c->device) cudaSetDevice(c->device);
+  fill_net(c, d_params);
+  c->launches = 0;
+  cudaError_t e = launch_pack(c->net, c->wt, c->wb, strm);
+  if (c->ngemm > 0) c->launches++;
+  if (e != cudaSuccess) {
+    if (prev != c->device) cudaSetDevice(prev);
+    return cuda_fail(c, e, "pack");
+  }
+  FwdArgs a{};
+  fill_fwd(c, a, d_x, n, st);
+  a.ls.kind = 0;
+  a.step = 0;
+  a.zf = c->zscr;
+  if (out) {
+    a.out_f = out->d_f;
+    a.out_g = out->d_grad;
+    a.out_hess = out->d_hess;
+    a.out_K = out->d_K;
+    a.out_D = out->d_D;
+    a.out_frames = out->d_frames;
+    a.out_mask = out->d_mask;
+  }
+  const int grid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
+  e = launch_fwd(a, grid, strm);
+  c->launches++;
+  if (prev != c->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(c, e, "fwd_kernel");
+  return FDSDF_OK;
+}
+
+fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
+                        const fdsdf_loss* ls, float* d_grad, double* d_loss, uint32_t flags, void* stream) {
+  fdsdf_status s = check_common(c, d_params, d_x, n, st);
+  if (s != FDSDF_OK) return s;
+  if (c->eval_only) return fail(c, FDSDF_E_INVALID, "context created EVAL_ONLY");
+  if (!ls || !d_grad || !d_loss) return fail(c, FDSDF_E_INVALID, "null pointer argument");
+  if (ls->kind != FDSDF_LOSS_NCR && ls->kind != FDSDF_LOSS_NSH) return fail(c, FDSDF_E_INVALID, "loss kind");
+  if (ls->fd_form != FDSDF_FD_ABS && ls->fd_form != FDSDF_FD_SQUARE) return fail(c, FDSDF_E_INVALID, "fd_form");
+  const float ws[] = {ls->w_dm, ls->lambda_dnm, ls->lambda_eik, ls->lambda_fd};
+  for (float w : ws)
+    if (!(w >= 0.f) || !std::isfinite(w)) return fail(c, FDSDF_E_INVALID, "loss weights must be finite and >= 0");
+  if (!(ls->alpha_dnm > 0.f) || !std::isfinite(ls->alpha_dnm)) return fail(c, FDSDF_E_INVALID, "alpha must be > 0");
+  const int64_t nsl = st->n_surface, nul = n - st->n_surface;
+  if (ls->n_surface_global < nsl || ls->n_uniform_global < nul || ls->n_global < n ||
+      ls->n_global != ls->n_surface_global + ls->n_uniform_global)
+    return fail(c, FDSDF_E_INVALID, "global counts inconsistent with the local rows");
+  if (ls->w_dm > 0.f && ls->n_surface_global == 0) return fail(c, FDSDF_E_EMPTY, "no surface rows but w_dm > 0");
+  if (ls->lambda_dnm > 0.f && ls->n_uniform_global == 0)
+    return fail(c, FDSDF_E_EMPTY, "no uniform rows but lambda_dnm > 0");
+  if ((flags & FDSDF_STEP_ALLREDUCE) && !c->comm)
+    return fail(c, FDSDF_E_UNSUPPORTED, "ALLREDUCE requested before fdsdf_comm_init");
+
+  cudaStream_t strm = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != c->device) cudaSetDevice(c->device);
+  auto done = [&](fdsdf_status r) {
+    if (prev != c->device) cudaSetDevice(prev);
+    return r;
+  };
+  fill_net(c, d_params);
+  c->launches = 0;
+  cudaError_t e = launch_pack(c->net, c->wt, c->wb, strm);
+  if (c->ngemm > 0) c->launches++;
+  if (e != cudaSuccess) return done(cuda_fail(c, e, "pack"));
+
+  FwdArgs a{};
+  fill_fwd(c, a, d_x, n, st);
+  a.ls.kind = ls->kind;
+  a.ls.fd_form = ls->fd_form;
+  a.ls.w_dm = ls->w_dm;
+  a.ls.lambda_dnm = ls->lambda_dnm;
+  a.ls.alpha = ls->alpha_dnm;
+  a.ls.lambda_eik = ls->lambda_eik;
+  a.ls.lambda_fd = ls->lambda_fd;
+  a.ls.inv_ns = ls->n_surface_global > 0 ? 1.0 / (double)ls->n_surface_global : 0.0;
+  a.ls.inv_nu = ls->n_uniform_global > 0 ? 1.0 / (double)ls->n_uniform_global : 0.0;
+  a.ls.inv_n = 1.0 / (double)ls->n_global;
+  a.step = 1;
+  a.zf = c->zf;
+  a.seed = c->seed;
+  const int fgrid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
+  e = launch_fwd(a, fgrid, strm);
+  c->launches++;
+  if (e != cudaSuccess) return done(cuda_fail(c, e, "fwd_kernel"));
+
+  BwdArgs b{};
+  b.net = c->net;
+  b.x = d_x;
+  b.zf = c->zf;
+  b.seed = c->seed;
+  b.n = n;
+  b.h = st->h;
+  b.del = c->del;
+  b.actv = c->actv;
+  b.bacc = c->bacc;
+  b.nacc = c->nacc;
+  b.ntiles = (n + c->btile - 1) / c->btile;
+  const int bgrid = (int)std::min<int64_t>(c->bgrid, b.ntiles);
+  e = launch_bwd(b, bgrid, strm);
+  c->launches++;
+  if (e != cudaSuccess) return done(cuda_fail(c, e, "bwd_kernel"));
+
+  WgradArgs w{};
+  w.del = c->del;
+  w.actv = c->actv;
+  w.part = c->part;
+  w.rows = n * NCOLB;
+  w.stride_layer = n * NCOLB * c->mpad;
+  w.mpad = c->mpad;
+  w.nsplit = c->nsplit;
+  w.first_layer = 1;
+  e = launch_wgrad(w, c->ngemm, strm);
+  if (c->ngemm > 0) c->launches++;
+  if (e != cudaSuccess) return done(cuda_fail(c, e, "wgrad_kernel"));
+
+  FinArgs f{};
+  f.net = c->net;
+  f.part = c->part;
+  f.nsplit = c->nsplit;
+  f.bacc = c->bacc;
+  f.nacc = c->nacc;
+  f.nbcta = bgrid;
+  f.lossp = c->lossp;
+  f.nfcta = fgrid;
+  f.ls = a.ls;
+  f.grad = d_grad;
+  f.loss = d_loss;
+  f.accumulate = (flags & FDSDF_STEP_ACCUMULATE) ? 1 : 0;
+  f.dflags = c->dflags;
+  f.n_local = n;
+  f.P = c->P;
+  e = launch_finalize(f, strm);
+  c->launches++;
+  if (e != cudaSuccess) return done(cuda_fail(c, e, "finalize_kernel"));
+
+  if (flags & FDSDF_STEP_ALLREDUCE) {
+    g_nccl.groupStart();
+    int r1 = g_nccl.allReduce(d_grad, d_grad, (size_t)c->P, kNcclFloat32, kNcclSum, c->comm, strm);
+    int r2 = g_nccl.allReduce(d_loss, d_loss, 8, kNcclFloat64, kNcclSum, c->comm, strm);
+    int r3 = g_nccl.groupEnd();
+    if (r1 || r2 || r3) return done(fail(c, FDSDF_E_NCCL, "ncclAllReduce failed"));
+  }
+  return done(FDSDF_OK);
+}
+
+fdsdf_status fdsdf_comm_unique_id(uint8_t id[128]) {
+  if (!id) return FDSDF_E_INVALID;
+  std::string err;
+  if (!nccl_load(&err)) return FDSDF_E_NCCL;
+  NcclId u;
+  if (g_nccl.getUniqueId(&u) != 0) return FDSDF_E_NCCL;
+  memcpy(id, u.internal, 128);
+  return FDSDF_OK;
+}
+
+fdsdf_status fdsdf_comm_init(fdsdf_ctx* c, const uint8_t id[128], int rank, int world) {
+  if (!c || !id || world < 1 || rank < 0 || rank >= world) return FDSDF_E_INVALID;
+  std::string err;
+  if (!nccl_load(&err)) return fail(c, FDSDF_E_NCCL, err);
+  NcclId u;
+  memcpy(u.internal, id, 128);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  void* comm = nullptr;
+  int r = ((CommInitRankFn)g_nccl.commInitRank)(&comm, world, u, rank);
+  cudaSetDevice(prev);
+  if (r != 0) return fail(c, FDSDF_E_NCCL, "ncclCommInitRank failed");
+  if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  c->comm = comm;
+  c->rank = rank;
+  c->world = world;
+  return FDSDF_OK;
+}
+
+fdsdf_status fdsdf_allreduce(fdsdf_ctx* c, float* d_buf, int64_t count, void* stream) {
+  if (!c || !d_buf || count < 0) return FDSDF_E_INVALID;
+  if (!c->comm) return fail(c, FDSDF_E_UNSUPPORTED, "comm not initialised");
+  int r = g_nccl.allReduce(d_buf, d_buf, (size_t)count, kNcclFloat32, kNcclSum, c->comm, (cudaStream_t)stream);
+  return r == 0 ? FDSDF_OK : fail(c, FDSDF_E_NCCL, "ncclAllReduce failed");
+}
+
+fdsdf_status fdsdf_get_device_flags(fdsdf_ctx* c, uint32_t* out) {
+  if (!c || !out) return FDSDF_E_INVALID;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  unsigned v = 0;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(&v, c->dflags, sizeof(unsigned), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(c->dflags, 0, sizeof(unsigned));
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(c, e, "get_device_flags");
+  *out = v;
+  return FDSDF_OK;
+}
+
+}  // extern "C"

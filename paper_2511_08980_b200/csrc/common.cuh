@@ -1,0 +1,102 @@
+// common.cuh -- device helpers for the fdsdf sm_100a kernels.
+//
+//  * mbarrier / cp.async.bulk (TMA bulk-copy engine) PTX wrappers used to stream layer
+//    weights into shared memory (BASELINE north_star (a));
+//  * accurate fp32 elementary functions for the cancellation-free activation identities
+//    (DESIGN.md §4): range-reduced sincos (Cody-Waite, 3-part pi/2 with FMA) and the
+//    logistic / expm1 / log1p helpers of the softplus identities.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fdsdf {
+
+// ----------------------------------------------------------------------------- PTX: mbarrier + bulk copy
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D bulk copy global -> shared through the TMA engine, completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// named barrier over the compute warps only (the producer warp never joins)
+__device__ __forceinline__ void bar_compute(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// ----------------------------------------------------------------------------- accurate fp32 math
+
+// sin and cos of x, |x| up to ~1e5, error ~1-2 ulp (relative for small |x|).
+// Cody-Waite reduction by pi/2 with FMA, minimax polynomials on [-pi/4, pi/4].
+__device__ __forceinline__ void sincos_acc(float x, float* s, float* c) {
+  const float k = rintf(x * 0.636619772367581343f);
+  float r = fmaf(-k, 1.5707963705062866f, x);
+  r = fmaf(-k, -4.371138828673793e-08f, r);
+  r = fmaf(-k, -1.7763568394002505e-15f, r);
+  const int q = static_cast<int>(k);
+  const float z = r * r;
+  float ps = fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f);
+  ps = fmaf(ps * z, r, r);
+  float pc = fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f);
+  pc = fmaf(pc * z, z, fmaf(-0.5f, z, 1.0f));
+  float sv = (q & 1) ? pc : ps;
+  float cv = (q & 1) ? ps : pc;
+  if (q & 2) sv = -sv;
+  if ((q + 1) & 2) cv = -cv;
+  *s = sv;
+  *c = cv;
+}
+
+// logistic s(t) = 1/(1+exp(-t)), accurate, saturating without NaN
+__device__ __forceinline__ float logistic_acc(float t) { return 1.0f / (1.0f + expf(-t)); }
+
+// exact softplus log(1+exp(t)) without threshold
+__device__ __forceinline__ float softplus_acc(float t) { return fmaxf(t, 0.0f) + log1pf(expf(-fabsf(t))); }
+
+}  // namespace fdsdf

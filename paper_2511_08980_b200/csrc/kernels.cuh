@@ -1,0 +1,125 @@
+// kernels.cuh -- kernel argument blocks and launch entry points shared by the C-ABI layer.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fdsdf {
+
+enum { ACT_SOFTPLUS = 0, ACT_SINE = 1 };
+
+constexpr int MAXL = 16;
+constexpr int NCW = 8;             // compute warps per CTA
+constexpr int NCT = NCW * 32;      // compute threads
+constexpr int NTH = NCT;           // thread 0 also issues the TMA weight slabs
+constexpr int NCOLF = 12;          // stored forward columns per centre: c, t0..2, (A,S) x 4
+constexpr int NCOLB = 10;          // backward columns: c, t_r, (A,S) x 4
+constexpr int NSEED = 16;          // per-centre: fbar, Sbar_u, Sbar_v, Sbar_p, Sbar_q, r(3), u(3), v(3), pad
+constexpr int NLOSS = 6;           // dm, dnm, eik, fd, n_degenerate, n_nonfinite
+
+struct Net {
+  int L;                 // linear layers
+  int skip;              // -1 or skip layer
+  int act;               // ACT_*
+  int mpad;              // padded hidden width (64/128/256/512)
+  float beta;
+  int width[MAXL + 1];
+  float omega[MAXL];     // per linear layer: omega for sine hidden layers, 1 otherwise
+  const float* W[MAXL];  // into the caller's flat params
+  const float* b[MAXL];
+  const float* Wt[MAXL]; // packed forward weights (GEMM layers): [mpad k][mpad m]
+  const float* Wb[MAXL]; // packed backward weights (GEMM layers): [mpad m][mpad k]
+};
+
+struct LossCfg {
+  int kind, fd_form, denom, denom_pow;
+  float w_dm, lambda_dnm, alpha, lambda_eik, lambda_fd, eps_grad;
+  double inv_ns, inv_nu, inv_n;  // 1 / global counts (0 if the count is 0)
+};
+
+struct FwdArgs {
+  Net net;
+  LossCfg ls;
+  const float* x;        // [n][3]
+  int64_t n;
+  int64_t n_surface;
+  int64_t index_offset;
+  uint64_t frame_seed;
+  int frame_given;
+  const float* frames_in;  // [n][6]
+  float h;
+  int step;              // 1: store the backward workspace and seeds
+  // outputs (nullable)
+  float* out_f;
+  float* out_g;
+  float* out_hess;
+  float* out_K;
+  float* out_D;
+  float* out_frames;
+  uint8_t* out_mask;
+  // workspace
+  float* zf;             // step: [n][nh][12][mpad]; eval: per-CTA scratch
+  float* seed;           // [n][8]
+  double* lossp;         // [gridDim.x][NLOSS]
+  unsigned* dflags;      // sticky device flags
+  int64_t ntiles;
+};
+
+struct BwdArgs {
+  Net net;
+  const float* x;
+  const float* zf;       // [n][nh][12][mpad]
+  const float* seed;     // [n][8]
+  int64_t n;
+  float h;
+  float* del;            // [nh][n*10][mpad]  (layers 1..L-2 used)
+  float* actv;           // [nh][n*10][mpad]  (layers 0..L-3 used: input of layer l+1)
+  float* bacc;           // [gridDim.x][nacc] per-CTA accumulators
+  int64_t nacc;
+  int64_t ntiles;
+};
+
+struct WgradArgs {
+  const float* del;
+  const float* actv;
+  float* part;           // [nglayers][nsplit][mpad][mpad]
+  int64_t rows;          // n*10
+  int64_t stride_layer;  // floats per layer in del / actv
+  int mpad;
+  int nsplit;
+  int first_layer;       // GEMM layers first_layer .. first_layer + gridDim.z - 1
+};
+
+struct FinArgs {
+  Net net;
+  const float* part;     // wgrad partials
+  int nsplit;
+  const float* bacc;
+  int64_t nacc;
+  int nbcta;
+  const double* lossp;
+  int nfcta;
+  LossCfg ls;
+  float* grad;
+  double* loss;
+  int accumulate;
+  unsigned* dflags;
+  int64_t n_local;
+  int64_t P;
+};
+
+// per-CTA accumulator layout of the backward kernel (floats):
+//   db hidden layers [L-1][mpad] | dW_last [mpad] | db_last [1] | dW_0 [mpad][3]
+inline int64_t bacc_size(int L, int mpad) { return (int64_t)(L - 1) * mpad + mpad + 1 + (int64_t)mpad * 3; }
+
+// launchers (kernels.cu); return cudaError_t of the launch
+cudaError_t launch_pack(const Net& net, float* wt_base, float* wb_base, cudaStream_t st);
+cudaError_t launch_fwd(const FwdArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_bwd(const BwdArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_wgrad(const WgradArgs& a, int nglayers, cudaStream_t st);
+cudaError_t launch_finalize(const FinArgs& a, cudaStream_t st);
+int fwd_tile_centres(int mpad);   // centres per forward tile
+int bwd_tile_centres(int mpad);   // centres per backward tile
+size_t fwd_smem_bytes(int mpad);
+size_t bwd_smem_bytes(int mpad);
+
+}  // namespace fdsdf

@@ -1,0 +1,307 @@
+"""Thin ctypes binding of libfdsdf.so (include/fdsdf.h).
+
+Argument marshalling only: every step of the FD curvature path runs in the CUDA kernels of
+csrc/.  torch is used for device memory and streams.  There is no CPU fallback: a missing
+library or a non-sm_100 device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfdsdf.so")
+
+MAX_LINEAR = 16
+ACT = {"softplus": 0, "sine": 1}
+FRAME_RANDOM, FRAME_GIVEN = 0, 1
+DENOM = {"paper": 0, "one": 1, "grad": 2}
+KIND = {"ncr": 0, "nsh": 1}
+FD_FORM = {"abs": 0, "square": 1}
+STEP_ACCUMULATE, STEP_ALLREDUCE = 1, 2
+CREATE_EVAL_ONLY = 1
+FLAG_NONFINITE_INPUT, FLAG_NONFINITE_LOSS, FLAG_ALL_FD_SKIPPED = 1, 2, 4
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_EMPTY", 3: "E_CUDA", 4: "E_NCCL", 5: "E_NOMEM",
+          6: "E_UNSUPPORTED"}
+
+
+class FdsdfError(RuntimeError):
+    def __init__(self, status, msg=""):
+        self.status = status
+        self.code = STATUS.get(status, str(status))
+        super().__init__(f"fdsdf {self.code}: {msg}")
+
+
+class MlpSpec(C.Structure):
+    _fields_ = [("n_linear", C.c_int32), ("width", C.c_int32 * (MAX_LINEAR + 1)), ("act", C.c_int32),
+                ("beta", C.c_float), ("omega0_first", C.c_float), ("omega0_hidden", C.c_float),
+                ("skip_at", C.c_int32)]
+
+
+class Stencil(C.Structure):
+    _fields_ = [("h", C.c_float), ("frame_seed", C.c_uint64), ("index_offset", C.c_int64),
+                ("frame_mode", C.c_int32), ("d_frames_in", C.c_void_p), ("eps_grad", C.c_float),
+                ("denom", C.c_int32), ("denom_pow", C.c_int32), ("n_surface", C.c_int64)]
+
+
+class EvalOut(C.Structure):
+    _fields_ = [("d_f", C.c_void_p), ("d_grad", C.c_void_p), ("d_hess", C.c_void_p), ("d_K", C.c_void_p),
+                ("d_D", C.c_void_p), ("d_frames", C.c_void_p), ("d_mask", C.c_void_p)]
+
+
+class Loss(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("fd_form", C.c_int32), ("w_dm", C.c_float), ("lambda_dnm", C.c_float),
+                ("alpha_dnm", C.c_float), ("lambda_eik", C.c_float), ("lambda_fd", C.c_float),
+                ("n_surface_global", C.c_int64), ("n_uniform_global", C.c_int64), ("n_global", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfdsdf.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FdsdfError(6, f"{LIB_PATH} not built (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, u32 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32
+        L.fdsdf_create.argtypes = [C.POINTER(MlpSpec), C.c_int, i64, u32, C.POINTER(vp)]
+        L.fdsdf_create.restype = C.c_int
+        L.fdsdf_validate_spec.argtypes = [C.POINTER(MlpSpec)]
+        L.fdsdf_validate_spec.restype = C.c_int
+        L.fdsdf_destroy.argtypes = [vp]
+        L.fdsdf_destroy.restype = None
+        L.fdsdf_spec_num_params.argtypes = [C.POINTER(MlpSpec)]
+        L.fdsdf_spec_num_params.restype = i64
+        L.fdsdf_spec_param_offset.argtypes = [C.POINTER(MlpSpec), C.c_int, C.c_int]
+        L.fdsdf_spec_param_offset.restype = i64
+        L.fdsdf_num_params.argtypes = [vp]
+        L.fdsdf_num_params.restype = i64
+        L.fdsdf_eval.argtypes = [vp, vp, vp, i64, C.POINTER(Stencil), C.POINTER(EvalOut), vp]
+        L.fdsdf_eval.restype = C.c_int
+        L.fdsdf_step.argtypes = [vp, vp, vp, i64, C.POINTER(Stencil), C.POINTER(Loss), vp, vp, u32, vp]
+        L.fdsdf_step.restype = C.c_int
+        L.fdsdf_comm_unique_id.argtypes = [C.c_char_p]
+        L.fdsdf_comm_unique_id.restype = C.c_int
+        L.fdsdf_comm_init.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
+        L.fdsdf_comm_init.restype = C.c_int
+        L.fdsdf_allreduce.argtypes = [vp, vp, i64, vp]
+        L.fdsdf_allreduce.restype = C.c_int
+        L.fdsdf_status_string.argtypes = [C.c_int]
+        L.fdsdf_status_string.restype = C.c_char_p
+        L.fdsdf_last_error.argtypes = [vp]
+        L.fdsdf_last_error.restype = C.c_char_p
+        L.fdsdf_get_device_flags.argtypes = [vp, C.POINTER(u32)]
+        L.fdsdf_get_device_flags.restype = C.c_int
+        L.fdsdf_last_launch_count.argtypes = [vp]
+        L.fdsdf_last_launch_count.restype = i32
+        L.fdsdf_version.argtypes = []
+        L.fdsdf_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def make_spec(spec: dict) -> MlpSpec:
+    """C spec from the plain-dict spec used by the harness."""
+    w = list(spec["widths"])
+    s = MlpSpec()
+    s.n_linear = len(w) - 1
+    if len(w) > MAX_LINEAR + 1:
+        raise FdsdfError(1, "too many layers")
+    for i, v in enumerate(w):
+        s.width[i] = int(v)
+    s.act = ACT[spec["act"]]
+    s.beta = float(spec.get("beta", 100.0))
+    s.omega0_first = float(spec.get("omega0_first", 30.0))
+    s.omega0_hidden = float(spec.get("omega0_hidden", 30.0))
+    s.skip_at = int(spec.get("skip_at", -1))
+    return s
+
+
+def _check(status, ctx=None):
+    if status != 0:
+        msg = lib().fdsdf_last_error(ctx).decode() if ctx else ""
+        raise FdsdfError(status, msg)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+# ----------------------------------------------------------------------------- same-name thin wrappers
+
+def fdsdf_validate_spec(spec: dict) -> int:
+    s = make_spec(spec)
+    return lib().fdsdf_validate_spec(C.byref(s))
+
+
+def fdsdf_spec_num_params(spec: dict) -> int:
+    s = make_spec(spec)
+    return lib().fdsdf_spec_num_params(C.byref(s))
+
+
+def fdsdf_create(spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False):
+    s = make_spec(spec)
+    h = C.c_void_p()
+    _check(lib().fdsdf_create(C.byref(s), int(device), int(max_centers),
+                              CREATE_EVAL_ONLY if eval_only else 0, C.byref(h)))
+    return h
+
+
+def fdsdf_destroy(ctx):
+    lib().fdsdf_destroy(ctx)
+
+
+def make_stencil(h, n_surface, frame_seed=0, index_offset=0, frames=None, eps_grad=1e-6, denom="paper",
+                 denom_pow=4):
+    st = Stencil()
+    st.h = float(h)
+    st.frame_seed = int(frame_seed) & ((1 << 64) - 1)
+    st.index_offset = int(index_offset)
+    st.frame_mode = FRAME_GIVEN if frames is not None else FRAME_RANDOM
+    st.d_frames_in = None if frames is None else frames.data_ptr()
+    st.eps_grad = float(eps_grad)
+    st.denom = DENOM[denom] if isinstance(denom, str) else int(denom)
+    st.denom_pow = int(denom_pow)
+    st.n_surface = int(n_surface)
+    return st
+
+
+def make_loss(cfg: dict, counts):
+    ls = Loss()
+    ls.kind = KIND[cfg["kind"]]
+    ls.fd_form = FD_FORM[cfg.get("fd_form", "abs")]
+    ls.w_dm = float(cfg["w_dm"])
+    ls.lambda_dnm = float(cfg["lambda_dnm"])
+    ls.alpha_dnm = float(cfg.get("alpha_dnm", 100.0))
+    ls.lambda_eik = float(cfg["lambda_eik"])
+    ls.lambda_fd = float(cfg["lambda_fd"])
+    ls.n_surface_global, ls.n_uniform_global, ls.n_global = (int(c) for c in counts)
+    return ls
+
+
+def fdsdf_eval(ctx, params, x, n, stencil: Stencil, out: EvalOut, stream=None):
+    _check(lib().fdsdf_eval(ctx, _ptr(params), _ptr(x), int(n), C.byref(stencil), C.byref(out),
+                            _stream(stream)), ctx)
+
+
+def fdsdf_step(ctx, params, x, n, stencil: Stencil, loss: Loss, grad, loss_out, flags=0, stream=None):
+    _check(lib().fdsdf_step(ctx, _ptr(params), _ptr(x), int(n), C.byref(stencil), C.byref(loss),
+                            _ptr(grad), _ptr(loss_out), int(flags), _stream(stream)), ctx)
+
+
+def fdsdf_comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().fdsdf_comm_unique_id(buf))
+    return buf.raw
+
+
+def fdsdf_comm_init(ctx, uid: bytes, rank: int, world: int):
+    _check(lib().fdsdf_comm_init(ctx, uid, int(rank), int(world)), ctx)
+
+
+def fdsdf_allreduce(ctx, buf, count=None, stream=None):
+    _check(lib().fdsdf_allreduce(ctx, _ptr(buf), int(buf.numel() if count is None else count),
+                                 _stream(stream)), ctx)
+
+
+def fdsdf_get_device_flags(ctx) -> int:
+    v = C.c_uint32()
+    _check(lib().fdsdf_get_device_flags(ctx, C.byref(v)), ctx)
+    return int(v.value)
+
+
+def fdsdf_last_launch_count(ctx) -> int:
+    return int(lib().fdsdf_last_launch_count(ctx))
+
+# ----------------------------------------------------------------------------- convenience object
+
+
+class FDSDF:
+    """A context bound to one device: eval() / step() on torch CUDA tensors."""
+
+    def __init__(self, spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False):
+        import torch
+        self.spec = spec
+        self.device = torch.device("cuda", device)
+        self.ctx = fdsdf_create(spec, device, max_centers, eval_only)
+        self.P = int(lib().fdsdf_num_params(self.ctx))
+        self.max_centers = int(max_centers)
+
+    def close(self):
+        if self.ctx is not None:
+            fdsdf_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _dev(self, a, dtype):
+        import torch
+        if isinstance(a, np.ndarray):
+            a = torch.from_numpy(np.ascontiguousarray(a))
+        return a.to(device=self.device, dtype=dtype).contiguous()
+
+    def eval(self, params, x, n_surface, h, frame_seed=0, index_offset=0, frames=None, eps_grad=1e-6,
+             denom="paper", denom_pow=4, stream=None, outputs=None):
+        """Returns a dict of device tensors: f, g, hess (f_uu, f_uv, f_vv), K, D, frames, mask."""
+        import torch
+        params = self._dev(params, torch.float32)
+        x = self._dev(x, torch.float32).reshape(-1, 3)
+        n = x.shape[0]
+        fr = None if frames is None else self._dev(frames, torch.float32).reshape(n, 6)
+        st = make_stencil(h, n_surface, frame_seed, index_offset, fr, eps_grad, denom, denom_pow)
+        dev = self.device
+        o = outputs or dict(
+            f=torch.empty(n, device=dev), g=torch.empty(n, 3, device=dev), hess=torch.empty(n, 3, device=dev),
+            K=torch.empty(n, device=dev), D=torch.empty(n, device=dev), frames=torch.empty(n, 6, device=dev),
+            mask=torch.empty(n, dtype=torch.uint8, device=dev))
+        out = EvalOut(*(_ptr(o.get(k)) for k in ("f", "g", "hess", "K", "D", "frames", "mask")))
+        fdsdf_eval(self.ctx, params, x, n, st, out, stream)
+        return o
+
+    def step(self, params, x, n_surface, h, loss_cfg, counts=None, frame_seed=0, index_offset=0, frames=None,
+             eps_grad=1e-6, grad=None, loss=None, accumulate=False, allreduce=False, stream=None):
+        """Returns (grad [P] fp32, loss [8] fp64) device tensors."""
+        import torch
+        params = self._dev(params, torch.float32)
+        x = self._dev(x, torch.float32).reshape(-1, 3)
+        n = x.shape[0]
+        if counts is None:
+            counts = (n_surface, n - n_surface, n)
+        fr = None if frames is None else self._dev(frames, torch.float32).reshape(n, 6)
+        st = make_stencil(h, n_surface, frame_seed, index_offset, fr, eps_grad, loss_cfg.get("denom", "paper"),
+                          loss_cfg.get("denom_pow", 4))
+        ls = make_loss(loss_cfg, counts)
+        if grad is None:
+            grad = torch.zeros(self.P, device=self.device, dtype=torch.float32)
+        if loss is None:
+            loss = torch.zeros(8, device=self.device, dtype=torch.float64)
+        flags = (STEP_ACCUMULATE if accumulate else 0) | (STEP_ALLREDUCE if allreduce else 0)
+        fdsdf_step(self.ctx, params, x, n, st, ls, grad, loss, flags, stream)
+        return grad, loss
+
+    def comm_init(self, uid: bytes, rank: int, world: int):
+        fdsdf_comm_init(self.ctx, uid, rank, world)
+
+    def device_flags(self) -> int:
+        return fdsdf_get_device_flags(self.ctx)
+
+    def launch_count(self) -> int:
+        return fdsdf_last_launch_count(self.ctx)
+
+
+def version() -> str:
+    return lib().fdsdf_version().decode()

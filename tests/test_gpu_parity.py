@@ -1,0 +1,181 @@
+"""GPU (CUDA, sm_100a) vs fp64 oracle parity, through the C ABI (libfdsdf.so).
+
+Inputs: the seeded BASELINE.json configs (harness.make_config), at sizes the oracle finishes
+in seconds but that span several tiles and a ragged tail.  Frames: the primary per-entry gate
+uses the GPU's exported frames in the oracle (GIVEN mode, SURVEY §8c "two frame modes");
+the self-framed mode is checked separately.  Tolerances: tests/gpu_util.py.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from harness import make_config, plane_mlp, loss_cfg, num_params  # noqa: E402
+from oracle import oracle_step, oracle_eval  # noqa: E402
+from gpu_util import (compare_eval, gpu_eval, per_tensor_grad_errors, LOSS_RTOL,  # noqa: E402
+                      GRAD_RTOL)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_08980_b200._build import build
+    build()
+
+
+def _model(spec, n, eval_only=False):
+    from paper_2511_08980_b200 import FDSDF
+    return FDSDF(spec, 0, max_centers=n, eval_only=eval_only)
+
+
+# (name, n_surface, n_uniform, h): several tiles + a ragged tail
+EVAL_CASES = [("c1", 1024, 1024, None), ("c1", 37, 29, None), ("c2", 300, 213, 1e-2),
+              ("c2", 256, 256, None), ("c3", 70, 61, None), ("c4", 100, 157, 1e-2)]
+
+
+@pytest.mark.parametrize("name,ns,nu,h", EVAL_CASES)
+def test_eval_parity_given_frames(name, ns, nu, h):
+    c = make_config(name, ns, nu, h=h)
+    m = _model(c["spec"], len(c["x"]), eval_only=True)
+    g = gpu_eval(m, c)
+    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
+                    frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    err = compare_eval(g, o)
+    print(name, ns, nu, {k: float(v) for k, v in err.items()})
+    for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K"):
+        assert err[k] <= 1.0, (k, err)
+    assert err["mask"] == 0
+
+
+@pytest.mark.parametrize("name,ns,nu", [("c1", 1024, 1024), ("c2", 200, 200)])
+def test_eval_parity_self_framed(name, ns, nu):
+    """End-to-end: the GPU draws its own frame from its fp32 gradient; the oracle from its
+    fp64 gradient with the same counter-based SplitMix64 angle."""
+    c = make_config(name, ns, nu, h=1e-2)
+    m = _model(c["spec"], len(c["x"]), eval_only=True)
+    g = gpu_eval(m, c)
+    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frame_seed=c["frame_seed"])
+    fr = np.concatenate([o["u"], o["v"]], 1)
+    assert np.max(np.abs(g["frames"] - fr)) < 1e-3
+    err = compare_eval(g, o)
+    print(name, {k: float(v) for k, v in err.items()})
+    for k in ("f", "g", "fuu", "fuv", "fvv"):
+        assert err[k] <= 1.0, (k, err)
+
+
+STEP_CASES = [
+    ("c1", 1024, 1024, loss_cfg("ncr", "paper", w_dm=0, lambda_dnm=0, lambda_eik=0, lambda_fd=1)),  # C1a
+    ("c1", 1024, 1024, loss_cfg("ncr", "paper", w_dm=1, lambda_dnm=100, lambda_eik=50, lambda_fd=1)),  # C1b
+    ("c1", 1024, 1024, loss_cfg("nsh", "paper", w_dm=0, lambda_dnm=0, lambda_eik=0, lambda_fd=1)),  # C1c
+    ("c1", 1024, 1024, loss_cfg("ncr", "one", w_dm=0, lambda_dnm=0, lambda_eik=0, lambda_fd=1,
+                                fd_form="square")),  # C1d
+    ("c1", 53, 40, loss_cfg("ncr", "grad", w_dm=1, lambda_dnm=100, lambda_eik=50, lambda_fd=1)),
+    ("c2", 256, 256, None),
+    ("c3", 64, 64, None),
+    ("c4", 128, 128, None),
+]
+
+
+@pytest.mark.parametrize("case", range(len(STEP_CASES)))
+def test_step_parity(case):
+    name, ns, nu, ls = STEP_CASES[case]
+    c = make_config(name, ns, nu)
+    if ls is not None:
+        c["loss"] = ls
+    n = len(c["x"])
+    m = _model(c["spec"], n)
+    ev = gpu_eval(m, c, denom=c["loss"]["denom"])
+    grad, loss = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])
+    grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
+    o = oracle_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"],
+                    frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
+    lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
+    gerr = per_tensor_grad_errors(c["spec"], grad, o["grad"])
+    print(name, ns, nu, "loss", loss[:6], "ref", o["loss"][:6], "lerr", lerr, "gerr", gerr)
+    for i in range(5):
+        if o["loss"][i] != 0:
+            assert lerr[i] <= LOSS_RTOL, (i, lerr)
+        else:
+            assert abs(loss[i]) <= 1e-12
+    assert loss[5] == o["loss"][5]
+    assert np.all(gerr <= GRAD_RTOL), gerr
+
+
+def test_step_deterministic_and_accumulate():
+    c = make_config("c2", 300, 300)
+    m = _model(c["spec"], 600)
+    g1, l1 = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=7)
+    g1, l1 = g1.clone(), l1.clone()
+    g2, l2 = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=7)
+    assert torch.equal(g1, g2) and torch.equal(l1, l2)
+    g3, _ = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=7, grad=g2.clone(),
+                   accumulate=True)
+    assert torch.allclose(g3, 2 * g1, rtol=1e-6, atol=0)
+    assert m.launch_count() >= 4
+
+
+def test_shard_sum_equals_full_step():
+    """Data-parallel identity on one GPU: steps on two shards with global counts and global
+    index offsets sum (grad and loss) to the full step."""
+    c = make_config("c1", 512, 512)
+    x, ns = c["x"], c["n_surface"]
+    N = len(x)
+    m = _model(c["spec"], N)
+    gf, lf = m.step(c["params"], x, ns, c["h"], c["loss"], frame_seed=9)
+    gf, lf = gf.cpu().numpy(), lf.cpu().numpy()
+    # shard r: rows [r*N/2, (r+1)*N/2) -- shard 0 is all surface, shard 1 all uniform
+    counts = (ns, N - ns, N)
+    g0, l0 = m.step(c["params"], x[:512], 512, c["h"], c["loss"], counts=counts, frame_seed=9, index_offset=0)
+    g0, l0 = g0.cpu().numpy(), l0.cpu().numpy()
+    g1, l1 = m.step(c["params"], x[512:], 0, c["h"], c["loss"], counts=counts, frame_seed=9, index_offset=512)
+    g1, l1 = g1.cpu().numpy(), l1.cpu().numpy()
+    assert np.allclose(l0 + l1, lf, rtol=1e-6, atol=1e-12)
+    assert np.linalg.norm(g0 + g1 - gf) <= 1e-5 * np.linalg.norm(gf)
+
+
+def test_plane_mlp_zero_curvature():
+    spec, params = plane_mlp([0.48, -0.6, 0.64], 0.1, beta=100.0, hidden_layers=3)
+    x = np.random.default_rng(0).uniform(-1, 1, (300, 3)).astype(np.float32)
+    m = _model(spec, 300, eval_only=True)
+    o = m.eval(params, x, 150, 1e-2, frame_seed=1)
+    for k in ("hess", "K", "D"):
+        assert torch.max(torch.abs(o[k])).item() < 1e-3
+    n = np.array([0.48, -0.6, 0.64], np.float32)
+    assert np.max(np.abs(o["g"].cpu().numpy() - n)) < 1e-5
+
+
+def test_errors_and_flags():
+    from paper_2511_08980_b200 import FdsdfError
+    c = make_config("c1", 16, 16)
+    m = _model(c["spec"], 32)
+    with pytest.raises(FdsdfError) as e:
+        m.eval(c["params"], c["x"][:0], 0, 1e-2)
+    assert e.value.code == "E_EMPTY"
+    with pytest.raises(FdsdfError) as e:
+        m.eval(c["params"], c["x"], 16, 0.0)
+    assert e.value.code == "E_INVALID"
+    with pytest.raises(FdsdfError) as e:
+        m.eval(c["params"], np.zeros((33, 3), np.float32), 16, 1e-2)
+    assert e.value.code == "E_INVALID"
+    with pytest.raises(FdsdfError) as e:
+        m.step(c["params"], c["x"], 0, 1e-2, c["loss"] | {"w_dm": 1.0}, counts=(0, 32, 32))
+    assert e.value.code == "E_EMPTY"
+    x = c["x"].copy()
+    x[3, 1] = np.nan
+    m.eval(c["params"], x, 16, 1e-2)
+    assert m.device_flags() & 1
+    assert m.device_flags() == 0  # cleared
+
+
+@pytest.mark.parametrize("n", [1, 2, 33])
+def test_tiny_batches(n):
+    c = make_config("c2", max(1, n // 2), n - max(1, n // 2))
+    m = _model(c["spec"], n)
+    g = gpu_eval(m, c)
+    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
+                    frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    err = compare_eval(g, o)
+    assert max(err[k] for k in ("f", "g", "fuu", "fuv", "fvv")) <= 1.0, err
