@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the FD curvature-regularised neural-SDF training step
+(arXiv 2511.08980) on B200, through the C ABI of libfdsdf.so.
+
+One "step" = one fdsdf_step over one batch: centre forward + grad f, random tangent frame,
+the 9-point stencil of PAPER.md L83-91 (§3.1), K_FD / D_FD (L112, L121), Eq. (1) (L134-141),
+the backward to every weight, and (N > 1) the NCCL allreduce of the weight gradient.
+
+Workload (BASELINE.json configs[1], "C2"): SIREN 3->256x4->1 (omega0 = 30), 20k surface
+points on a seeded CSG shape + 20k uniform points in [-1.1, 1.1]^3, h = 5e-3, FD Gaussian
+curvature (PAPER denominators) + eikonal + Dirichlet.  N > 1: weak scaling, every rank owns a
+fresh C2-sized shard (rank-seeded), global index offsets and global loss denominators, and
+the step ends with the gradient allreduce.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c5]
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "FD-regularized SDF train steps/s & stencil points/s; % of pipe/HBM roofline"
+UNIT = "stencil points/s"
+FP32_LANES_PER_SM = 128          # FP32 FFMA lanes per SM (4 SMSPs x 32), B200_PROFILING.md
+NOMINAL_SMS = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("c2", "c5"), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def p_mm(spec):
+    from harness import layer_shapes
+    sh = layer_shapes(spec)
+    return sum(o * i for o, i in sh), sum(o * i for o, i in sh[1:-1])
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock and throttle reasons DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) arm
+
+
+def oracle_rate(cfg, budget_s=10.0, max_reps=3):
+    """Time the fp64 oracle (as it stands) on the workload: full step(s) over all centres,
+    repeated until ~budget_s.  Returns (stencil points/s, seconds per step, cores, sample)."""
+    import torch
+    from oracle import oracle_step
+    x = cfg["x"]
+    n = len(x)
+    reps, t_tot = 0, 0.0
+    while reps < max_reps and (reps == 0 or t_tot < budget_s):
+        t0 = time.perf_counter()
+        oracle_step(cfg["spec"], cfg["params"], x, cfg["n_surface"], cfg["h"], cfg["loss"],
+                    frame_seed=cfg["frame_seed"], index_offset=cfg["index_offset"],
+                    counts=cfg["counts"], need_grad=True)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+    per = t_tot / reps
+    return 9.0 * n / per, per, torch.get_num_threads(), f"{reps} full step(s) of {n} centres (all of the rank-0 shard)"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = workload(args.config, 0, 1)
+    t_steps = []
+    from oracle import oracle_step
+    import torch
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle_step(cfg["spec"], cfg["params"], cfg["x"], cfg["n_surface"], cfg["h"], cfg["loss"],
+                    frame_seed=cfg["frame_seed"], counts=cfg["counts"], need_grad=True)
+        if i >= args.warmup:
+            t_steps.append(time.perf_counter() - t0)
+    per = sum(t_steps) / len(t_steps)
+    n = len(cfg["x"])
+    v = 9.0 * n / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "steps_per_s": 1.0 / per,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg["config_json"],
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
+                         "sample": f"each step = one full oracle step over all {n} centres of the rank-0 shard"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- workload
+
+
+def workload(name, rank, world):
+    from harness import make_config, frame_seed
+    c = make_config("c2" if name == "c2" else "c5", rank=rank)
+    n = len(c["x"])
+    ns = c["n_surface"]
+    c["index_offset"] = rank * n
+    c["counts"] = (ns * world, (n - ns) * world, n * world)
+    c["frame_seed"] = frame_seed(4, 0)
+    P_mm, P_gemm = p_mm(c["spec"])
+    c["config_json"] = {
+        "workload": ("C2: SIREN 3->256x4->1 (omega0=30, SIREN init), 20k CSG surface + 20k uniform "
+                     "centres per GPU, h=5e-3, FD-NCR (paper denominators) + eikonal(50) + Dirichlet(1)")
+        if name == "c2" else
+        ("C5: SIREN 3->256x4->1, 100k CSG surface + 100k uniform centres per GPU, h=5e-3, FD-NCR + eik + DM"),
+        "centres_per_gpu": n, "global_centres": n * world, "stencil_points_per_centre": 9,
+        "params": int(len(c["params"])), "P_mm": P_mm, "h": c["h"],
+        "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every timed step",
+    }
+    return c
+
+
+# ----------------------------------------------------------------------------- our arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2511_08980_b200 import FDSDF
+    from paper_2511_08980_b200 import fdsdf as F
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = workload(args.config, rank, world)
+    n = len(cfg["x"])
+    spec = cfg["spec"]
+    model = FDSDF(spec, local, max_centers=n)
+    P = model.P
+    if world > 1:
+        uid = F.fdsdf_comm_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0)
+        model.comm_init(bytes(t.cpu().tolist()), rank, world)
+
+    params = torch.from_numpy(cfg["params"]).to(dev)
+    x = torch.from_numpy(cfg["x"]).to(dev)
+    grad = torch.zeros(P, device=dev, dtype=torch.float32)
+    loss = torch.zeros(8, device=dev, dtype=torch.float64)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    lc = cfg["loss"]
+    ls = F.make_loss(lc, cfg["counts"])
+    flags = F.STEP_ALLREDUCE if world > 1 else 0
+
+    def stencil(step):
+        from harness import frame_seed
+        return F.make_stencil(cfg["h"], cfg["n_surface"], frame_seed(4, step), cfg["index_offset"], None,
+                              lc["eps_grad"], lc["denom"], lc["denom_pow"])
+
+    def one_step(i, xin=None):
+        F.fdsdf_step(model.ctx, params, x if xin is None else xin, n, stencil(i), ls, grad, loss, flags, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        one_step(i)
+    barrier()
+    launches_per_step = model.launch_count()
+
+    # ------------------------------------------------------------------ timed region (device)
+    model.set_kernel_timing(True)
+    model.kernel_times(reset=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    barrier()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        one_step(args.warmup + i)
+        ev[i][1].record(stream)
+    barrier()
+    wall = time.perf_counter() - wall0
+    clocks = clk.stop()
+    model.set_kernel_timing(False)
+    ktimes = model.kernel_times(reset=True)
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    value = 9.0 * n * world / (ms_per_step * 1e-3)
+    assert np.isfinite(loss.cpu().numpy()[4]), "non-finite loss"
+
+    # ------------------------------------------------------------------ e2e (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(cfg["x"]).pin_memory()
+        gh = torch.empty(P, dtype=torch.float32).pin_memory()
+        lh = torch.empty(8, dtype=torch.float64).pin_memory()
+        xd = torch.empty_like(x)
+        for i in range(2):
+            xd.copy_(xh, non_blocking=True)
+            one_step(i, xd)
+            gh.copy_(grad, non_blocking=True)
+            lh.copy_(loss, non_blocking=True)
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            ev2[i][0].record(stream)
+            xd.copy_(xh, non_blocking=True)
+            one_step(args.warmup + i, xd)
+            gh.copy_(grad, non_blocking=True)
+            lh.copy_(loss, non_blocking=True)
+            ev2[i][1].record(stream)
+        barrier()
+        e_ms = sum(a.elapsed_time(b) for a, b in ev2)
+        et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item()) / args.steps
+        e2e = {"value": 9.0 * n * world / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(P * 4 + 8 * 8)}
+
+    # ------------------------------------------------------------------ roofline of the dominant kernel
+    P_mm, P_gemm = p_mm(spec)
+    alg = {  # algorithmic flops per launch: column-units x 2 P_mm x centres
+        "fwd": 20.0 * P_mm * n,      # 9 stencil values + 1 reverse sweep for grad f
+        "bwd": 20.0 * P_mm * n,      # delta through 9 evaluations + the grad-f path
+        "wgrad": 20.0 * P_gemm * n,  # dW of the GEMM layers: 10 column-units
+    }
+    kms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in ktimes.items()}
+    dom = max(("fwd", "bwd", "wgrad"), key=lambda k: kms[k])
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = nsm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    achieved = alg[dom] / (kms[dom] * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(dom)
+        except (OSError, ValueError):
+            traffic = None
+    roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_note": f"fp32 FFMA: {nsm} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz (clocks.max.sm)",
+            "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_max)) if clocks.get("sm_mhz") else None}
+    step_alg = sum(alg.values())
+    kernel_ms = {k: round(v, 4) for k, v in kms.items() if ktimes[k][1]}
+
+    # ------------------------------------------------------------------ CPU oracle baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, per, cores, sample = oracle_rate(cfg)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+               "s_per_step": per}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "steps_per_s": 1e3 / ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded CSG + uniform box; DESIGN.md §3)", "config": cfg["config_json"],
+            "roofline": roof, "step_alg_tflops": step_alg / (ms_per_step * 1e-3) / 1e12,
+            "kernel_ms": kernel_ms, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches_per_step * args.steps), "clocks": clocks,
+            "wall_s_timed_region": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    model.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

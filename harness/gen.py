@@ -257,6 +257,10 @@ SIREN_256x4 = dict(widths=[3, 256, 256, 256, 256, 1], act="sine")
 SP512x8 = dict(widths=[3, 512, 512, 512, 509, 512, 512, 512, 512, 1], act="softplus", skip_at=4)
 
 
+def _dflt(v, d):
+    return d if v is None else int(v)
+
+
 def make_config(name, n_surface=None, n_uniform=None, rank=0, h=None):
     """BASELINE.json configs[0..4] (C1..C5) as plain dicts.  n_surface / n_uniform
     override the counts (e.g. the oracle subsample: the first 1024 + 1024 rows)."""
@@ -264,7 +268,7 @@ def make_config(name, n_surface=None, n_uniform=None, rank=0, h=None):
     if name == "c1":
         spec = mlp_spec([3, 64, 64, 1], "softplus", beta=100.0)
         params = init_params(spec, "xavier", 0)
-        ns, nu = n_surface or 1024, n_uniform or 1024
+        ns, nu = _dflt(n_surface, 1024), _dflt(n_uniform, 1024)
         xs = sphere_surface(ns, 0.5, 1)
         xu = uniform_box(nu, 1.0, 2)
         loss = loss_cfg("ncr", "paper", w_dm=0, lambda_dnm=0, lambda_eik=0, lambda_fd=1)
@@ -273,17 +277,18 @@ def make_config(name, n_surface=None, n_uniform=None, rank=0, h=None):
         spec = mlp_spec(**SIREN_256x4)
         params = init_params(spec, "siren", 0)
         if name == "c2":
-            ns, nu = n_surface or 20_000, n_uniform or 20_000
-            xs = csg_surface(ns, 3, 1)
-            xu = uniform_box(nu, 1.1, 2)
+            ns, nu = _dflt(n_surface, 20_000), _dflt(n_uniform, 20_000)
+            # rank r > 0 (data-parallel weak scaling): a fresh draw of the same distribution
+            xs = csg_surface(ns, 3, 1 + 1000 * rank)
+            xu = uniform_box(nu, 1.1, 2 + 1000 * rank)
             hh = 5e-3
         elif name == "c4":
-            ns, nu = n_surface or 2_000, n_uniform or 20_000
+            ns, nu = _dflt(n_surface, 2_000), _dflt(n_uniform, 20_000)
             xs = csg_cutout_surface(ns, 3, 1, 6)
             xu = uniform_box(nu, 1.1, 2)
             hh = 1e-2
         else:
-            ns, nu = n_surface or 100_000, n_uniform or 100_000
+            ns, nu = _dflt(n_surface, 100_000), _dflt(n_uniform, 100_000)
             xs = csg_surface(ns, 3, 100 + rank)
             xu = uniform_box(nu, 1.1, 200 + rank)
             hh = 5e-3
@@ -291,7 +296,7 @@ def make_config(name, n_surface=None, n_uniform=None, rank=0, h=None):
     elif name == "c3":
         spec = mlp_spec(**SP512x8)
         params = init_params(spec, "xavier", 0)
-        ns, nu = n_surface or 50_000, n_uniform or 50_000
+        ns, nu = _dflt(n_surface, 50_000), _dflt(n_uniform, 50_000)
         xs = csg_surface(ns, 3, 1)
         xs = add_noise(xs, 0.005 * csg_bbox_diag(3), 5)
         xu = uniform_box(nu, 1.1, 2)

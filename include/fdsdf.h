@@ -194,6 +194,24 @@ const char* fdsdf_last_error(const fdsdf_ctx* ctx);
 fdsdf_status fdsdf_get_device_flags(fdsdf_ctx* ctx, uint32_t* out);
 /* Number of kernel launches enqueued by the last eval/step call on this context. */
 int32_t fdsdf_last_launch_count(const fdsdf_ctx* ctx);
+/* Per-kernel timing (for benchmarks).  When enabled, every kernel launch (and the NCCL group)
+ * that fdsdf_eval / fdsdf_step enqueue is bracketed by CUDA events recorded on the SAME
+ * stream.  fdsdf_kernel_times synchronises on the pending events, adds their elapsed times
+ * to per-slot totals and returns, for slots 0..nslots-1 (FDSDF_KSLOT_*), the total
+ * milliseconds and the number of timed launches since the last reset (reset != 0 clears the
+ * totals after reading).  Errors: ctx NULL, nslots < 0, NULL outputs -> FDSDF_E_INVALID;
+ * a failed event query -> FDSDF_E_CUDA. */
+enum {
+  FDSDF_KSLOT_PACK = 0,      /* weight re-layout for the TMA slabs                        */
+  FDSDF_KSLOT_FWD = 1,       /* fused centre + stencil forward + FD epilogue             */
+  FDSDF_KSLOT_BWD = 2,       /* backward through every stencil evaluation                */
+  FDSDF_KSLOT_WGRAD = 3,     /* split-K weight-gradient contraction                      */
+  FDSDF_KSLOT_FINALIZE = 4,  /* fixed-order reduction of partials and loss               */
+  FDSDF_KSLOT_ALLREDUCE = 5, /* NCCL group (not a kernel of this library)                */
+  FDSDF_NUM_KSLOTS = 6
+};
+fdsdf_status fdsdf_set_kernel_timing(fdsdf_ctx* ctx, int enable);
+fdsdf_status fdsdf_kernel_times(fdsdf_ctx* ctx, double* ms_total, int64_t* count, int nslots, int reset);
 /* Library version string. */
 const char* fdsdf_version(void);
 

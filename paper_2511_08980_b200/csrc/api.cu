@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/fdsdf.h"
 #include "kernels.cuh"
@@ -88,7 +89,42 @@ struct fdsdf_ctx {
   int rank = 0, world = 1;
   int launches = 0;
   std::string err;
+  // optional per-kernel CUDA-event timing (fdsdf_set_kernel_timing)
+  bool timing = false;
+  struct Rec {
+    int slot;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> spare;
+  double tot_ms[FDSDF_NUM_KSLOTS]{};
+  int64_t cnt[FDSDF_NUM_KSLOTS]{};
 };
+
+// Enqueue one kernel launch (or collective) on `st`, bracketed by CUDA events on the same
+// stream when timing is enabled; counts the launch.
+template <class F>
+static cudaError_t run_slot(fdsdf_ctx* c, int slot, cudaStream_t st, F&& launch) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->timing) {
+    for (cudaEvent_t* e : {&a, &b}) {
+      if (!c->spare.empty()) {
+        *e = c->spare.back();
+        c->spare.pop_back();
+      } else if (cudaEventCreate(e) != cudaSuccess) {
+        *e = nullptr;
+      }
+    }
+    if (a) cudaEventRecord(a, st);
+  }
+  cudaError_t e = launch();
+  if (c->timing && a && b) {
+    cudaEventRecord(b, st);
+    c->pending.push_back({slot, a, b});
+  }
+  if (slot != FDSDF_KSLOT_ALLREDUCE) c->launches++;
+  return e;
+}
 
 static fdsdf_status fail(fdsdf_ctx* c, fdsdf_status s, const std::string& msg) {
   if (c) c->err = msg;
@@ -163,6 +199,11 @@ void fdsdf_destroy(fdsdf_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  for (auto& r : c->pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : c->spare) cudaEventDestroy(e);
   void* bufs[] = {c->wt, c->wb, c->zf, c->zscr, c->seed, c->lossp, c->del, c->actv, c->bacc, c->part, c->dflags};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -280,9 +321,9 @@ static void fill_net(fdsdf_ctx* c, const float* d_params) {
 static fdsdf_status check_common(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n,
                                  const fdsdf_stencil* st) {
   if (!c) return FDSDF_E_INVALID;
-  if (!d_params || !d_x || !st) return fail(c, FDSDF_E_INVALID, "null pointer argument");
   if (n < 0 || n > c->max_centers) return fail(c, FDSDF_E_INVALID, "n out of range [0, max_centers]");
   if (n == 0) return fail(c, FDSDF_E_EMPTY, "n == 0");
+  if (!d_params || !d_x || !st) return fail(c, FDSDF_E_INVALID, "null pointer argument");
   if (!(st->h > 0.f) || !std::isfinite(st->h)) return fail(c, FDSDF_E_INVALID, "h must be finite and > 0");
   if (!(st->eps_grad >= 0.f) || !std::isfinite(st->eps_grad)) return fail(c, FDSDF_E_INVALID, "eps_grad must be >= 0");
   if (st->denom < 0 || st->denom > 2) return fail(c, FDSDF_E_INVALID, "denom out of range");
@@ -326,8 +367,8 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   if (prev != c->device) cudaSetDevice(c->device);
   fill_net(c, d_params);
   c->launches = 0;
-  cudaError_t e = launch_pack(c->net, c->wt, c->wb, strm);
-  if (c->ngemm > 0) c->launches++;
+  cudaError_t e = cudaSuccess;
+  if (c->ngemm > 0) e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
   if (e != cudaSuccess) {
     if (prev != c->device) cudaSetDevice(prev);
     return cuda_fail(c, e, "pack");
@@ -347,8 +388,7 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
     a.out_mask = out->d_mask;
   }
   const int grid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
-  e = launch_fwd(a, grid, strm);
-  c->launches++;
+  e = run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd(a, grid, strm); });
   if (prev != c->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(c, e, "fwd_kernel");
   return FDSDF_OK;
@@ -386,8 +426,8 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   };
   fill_net(c, d_params);
   c->launches = 0;
-  cudaError_t e = launch_pack(c->net, c->wt, c->wb, strm);
-  if (c->ngemm > 0) c->launches++;
+  cudaError_t e = cudaSuccess;
+  if (c->ngemm > 0) e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "pack"));
 
   FwdArgs a{};
@@ -406,8 +446,7 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   a.zf = c->zf;
   a.seed = c->seed;
   const int fgrid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
-  e = launch_fwd(a, fgrid, strm);
-  c->launches++;
+  e = run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd(a, fgrid, strm); });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "fwd_kernel"));
 
   BwdArgs b{};
@@ -423,8 +462,7 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   b.nacc = c->nacc;
   b.ntiles = (n + c->btile - 1) / c->btile;
   const int bgrid = (int)std::min<int64_t>(c->bgrid, b.ntiles);
-  e = launch_bwd(b, bgrid, strm);
-  c->launches++;
+  e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwd(b, bgrid, strm); });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "bwd_kernel"));
 
   WgradArgs w{};
@@ -436,8 +474,7 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   w.mpad = c->mpad;
   w.nsplit = c->nsplit;
   w.first_layer = 1;
-  e = launch_wgrad(w, c->ngemm, strm);
-  if (c->ngemm > 0) c->launches++;
+  if (c->ngemm > 0) e = run_slot(c, FDSDF_KSLOT_WGRAD, strm, [&] { return launch_wgrad(w, c->ngemm, strm); });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "wgrad_kernel"));
 
   FinArgs f{};
@@ -456,15 +493,18 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   f.dflags = c->dflags;
   f.n_local = n;
   f.P = c->P;
-  e = launch_finalize(f, strm);
-  c->launches++;
+  e = run_slot(c, FDSDF_KSLOT_FINALIZE, strm, [&] { return launch_finalize(f, strm); });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "finalize_kernel"));
 
   if (flags & FDSDF_STEP_ALLREDUCE) {
-    g_nccl.groupStart();
-    int r1 = g_nccl.allReduce(d_grad, d_grad, (size_t)c->P, kNcclFloat32, kNcclSum, c->comm, strm);
-    int r2 = g_nccl.allReduce(d_loss, d_loss, 8, kNcclFloat64, kNcclSum, c->comm, strm);
-    int r3 = g_nccl.groupEnd();
+    int r1 = 0, r2 = 0, r3 = 0;
+    run_slot(c, FDSDF_KSLOT_ALLREDUCE, strm, [&] {
+      g_nccl.groupStart();
+      r1 = g_nccl.allReduce(d_grad, d_grad, (size_t)c->P, kNcclFloat32, kNcclSum, c->comm, strm);
+      r2 = g_nccl.allReduce(d_loss, d_loss, 8, kNcclFloat64, kNcclSum, c->comm, strm);
+      r3 = g_nccl.groupEnd();
+      return cudaSuccess;
+    });
     if (r1 || r2 || r3) return done(fail(c, FDSDF_E_NCCL, "ncclAllReduce failed"));
   }
   return done(FDSDF_OK);
@@ -505,6 +545,46 @@ fdsdf_status fdsdf_allreduce(fdsdf_ctx* c, float* d_buf, int64_t count, void* st
   if (!c->comm) return fail(c, FDSDF_E_UNSUPPORTED, "comm not initialised");
   int r = g_nccl.allReduce(d_buf, d_buf, (size_t)count, kNcclFloat32, kNcclSum, c->comm, (cudaStream_t)stream);
   return r == 0 ? FDSDF_OK : fail(c, FDSDF_E_NCCL, "ncclAllReduce failed");
+}
+
+fdsdf_status fdsdf_set_kernel_timing(fdsdf_ctx* c, int enable) {
+  if (!c) return FDSDF_E_INVALID;
+  c->timing = enable != 0;
+  return FDSDF_OK;
+}
+
+fdsdf_status fdsdf_kernel_times(fdsdf_ctx* c, double* ms_total, int64_t* count, int nslots, int reset) {
+  if (!c || nslots < 0 || (nslots > 0 && (!ms_total || !count))) return FDSDF_E_INVALID;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  cudaError_t err = cudaSuccess;
+  for (auto& r : c->pending) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e == cudaSuccess) {
+      c->tot_ms[r.slot] += ms;
+      c->cnt[r.slot] += 1;
+    } else {
+      err = e;
+    }
+    c->spare.push_back(r.a);
+    c->spare.push_back(r.b);
+  }
+  c->pending.clear();
+  cudaSetDevice(prev);
+  for (int i = 0; i < nslots && i < FDSDF_NUM_KSLOTS; ++i) {
+    ms_total[i] = c->tot_ms[i];
+    count[i] = c->cnt[i];
+  }
+  if (reset)
+    for (int i = 0; i < FDSDF_NUM_KSLOTS; ++i) {
+      c->tot_ms[i] = 0.0;
+      c->cnt[i] = 0;
+    }
+  if (err != cudaSuccess) return cuda_fail(c, err, "kernel_times");
+  return FDSDF_OK;
 }
 
 fdsdf_status fdsdf_get_device_flags(fdsdf_ctx* c, uint32_t* out) {

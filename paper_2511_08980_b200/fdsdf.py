@@ -98,6 +98,10 @@ def lib():
         L.fdsdf_get_device_flags.restype = C.c_int
         L.fdsdf_last_launch_count.argtypes = [vp]
         L.fdsdf_last_launch_count.restype = i32
+        L.fdsdf_set_kernel_timing.argtypes = [vp, C.c_int]
+        L.fdsdf_set_kernel_timing.restype = C.c_int
+        L.fdsdf_kernel_times.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64), C.c_int, C.c_int]
+        L.fdsdf_kernel_times.restype = C.c_int
         L.fdsdf_version.argtypes = []
         L.fdsdf_version.restype = C.c_char_p
         _lib = L
@@ -223,6 +227,21 @@ def fdsdf_get_device_flags(ctx) -> int:
 def fdsdf_last_launch_count(ctx) -> int:
     return int(lib().fdsdf_last_launch_count(ctx))
 
+KSLOTS = ("pack", "fwd", "bwd", "wgrad", "finalize", "allreduce")
+
+
+def fdsdf_set_kernel_timing(ctx, enable: bool):
+    _check(lib().fdsdf_set_kernel_timing(ctx, 1 if enable else 0), ctx)
+
+
+def fdsdf_kernel_times(ctx, reset: bool = False) -> dict:
+    """{slot name: (total ms, launches)} of the event-timed launches since the last reset."""
+    n = len(KSLOTS)
+    ms = (C.c_double * n)()
+    cnt = (C.c_int64 * n)()
+    _check(lib().fdsdf_kernel_times(ctx, ms, cnt, n, 1 if reset else 0), ctx)
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KSLOTS)}
+
 # ----------------------------------------------------------------------------- convenience object
 
 
@@ -301,6 +320,12 @@ class FDSDF:
 
     def launch_count(self) -> int:
         return fdsdf_last_launch_count(self.ctx)
+
+    def set_kernel_timing(self, enable: bool):
+        fdsdf_set_kernel_timing(self.ctx, enable)
+
+    def kernel_times(self, reset: bool = False) -> dict:
+        return fdsdf_kernel_times(self.ctx, reset)
 
 
 def version() -> str:
