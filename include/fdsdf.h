@@ -215,6 +215,17 @@ fdsdf_status fdsdf_kernel_times(fdsdf_ctx* ctx, double* ms_total, int64_t* count
 /* Library version string. */
 const char* fdsdf_version(void);
 
+/* Self-test of the tcgen05 contraction core used by the tensor-pipe kernels:
+ * D[m][n] = sum_k W[m][k] B[n][k] on the 5th-generation tensor cores, with every fp32
+ * operand split exactly into three bf16 pieces and nprod of the piece products summed
+ * (1: plain bf16, 3: the three leading products, 6: the fp32-accurate bf16x6 scheme).
+ * d_W [M][K], d_B [N][K], d_D [M][N]: fp32 row-major device buffers owned by the caller.
+ * One CTA; M in {128, 256}, N a multiple of 16 in [16, 256], K a multiple of 64.
+ * Errors: NULL pointers, shapes or nprod out of range -> FDSDF_E_INVALID (nothing enqueued);
+ * launch failure -> FDSDF_E_CUDA.  Test/diagnostic use only (not on the hot path). */
+fdsdf_status fdsdf_selftest_mma(const float* d_W, const float* d_B, float* d_D, int M, int N, int K,
+                                int nprod, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,124 @@
+// tc.cuh -- tcgen05 (5th-generation tensor core) building blocks for the sm_100a contractions.
+//
+// Precision scheme "bf16x6": every fp32 operand x is split EXACTLY into three
+// bf16 pieces x = x0 + x1 + x2 (x0 = rn(x), x1 = rn(x - x0), x2 = rn(x - x0 - x1); each
+// residual is exactly representable, so the three pieces carry all 24 bits of x).  A product
+// sum_k a_k b_k is formed from the six piece products with i + j <= 2,
+//     a2 b0 + a1 b1 + a0 b2 + a1 b0 + a0 b1 + a0 b0,
+// all accumulated in fp32 in tensor memory.  The dropped terms (a1 b2, a2 b1, a2 b2) are
+// <= 2^-25 |a b|, below fp32 rounding, so the contraction is fp32-accurate while running on
+// the bf16 tensor pipe (6 bf16 MMAs = the cost of 3 tf32 MMAs).  Plain bf16/tf32 fails the
+// BASELINE tolerances and is never used.
+//
+// Operand layout: K-major, 128-byte swizzled bf16 tiles (the canonical UMMA SWIZZLE_128B
+// K-major layout): a tile of R rows and K columns is stored as K/64 column chunks of
+// R x 128 B; row r of a chunk sits at (r/8)*1024 + (r%8)*128 and its 16-byte pieces are
+// XOR-permuted by r%8.  Descriptor: SBO = 1024 B (8-row group stride), LBO unused,
+// layout SWIZZLE_128B; the K sub-step of 16 elements advances the start address by 32 B.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace fdsdf {
+namespace tc {
+
+// ----------------------------------------------------------------------------- bf16 x3 split
+struct Bf3 {
+  __nv_bfloat16 p[3];
+};
+
+__device__ __forceinline__ Bf3 split3(float x) {
+  Bf3 o;
+  o.p[0] = __float2bfloat16_rn(x);
+  float r = x - __bfloat162float(o.p[0]);
+  o.p[1] = __float2bfloat16_rn(r);
+  r = r - __bfloat162float(o.p[1]);
+  o.p[2] = __float2bfloat16_rn(r);
+  return o;
+}
+
+// byte offset of element (r, k) in a K-major SWIZZLE_128B bf16 tile with R rows
+__host__ __device__ __forceinline__ uint32_t sw128_off(int r, int k, int R) {
+  const int kc = k >> 6, kk = k & 63;
+  return (uint32_t)(kc * R * 128 + (r >> 3) * 1024 + (r & 7) * 128 + ((((kk >> 3) ^ (r & 7))) << 4) +
+                    ((kk & 7) << 1));
+}
+
+// ----------------------------------------------------------------------------- descriptors
+// shared-memory matrix descriptor (sm_100 UMMA layout): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version 1 [46,48), layout type [61,64) (2 = SWIZZLE_128B)
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// instruction descriptor, kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
+// both K-major (bits 15, 16 = 0), N>>3 [17,23), M>>4 [24,29)
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ----------------------------------------------------------------------------- tcgen05 PTX
+__device__ __forceinline__ void mma_bf16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// arrive (once) on an mbarrier when every previously issued tcgen05.mma of this thread is done
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// one full warp: allocate ncols TMEM columns (power of two >= 32), base address -> *dst
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// warp-collective: thread t of warp w reads lane 32*(w%4)+t, 8 consecutive fp32 columns
+// starting at column `col` (taddr must carry the warp's lane base in bits 16..31).
+// The load and its wait are one asm statement so no use of v can be scheduled before the wait.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r0, r1, r2, r3, r4, r5, r6, r7;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
+      : "r"(taddr)
+      : "memory");
+  v[0] = __uint_as_float(r0);
+  v[1] = __uint_as_float(r1);
+  v[2] = __uint_as_float(r2);
+  v[3] = __uint_as_float(r3);
+  v[4] = __uint_as_float(r4);
+  v[5] = __uint_as_float(r5);
+  v[6] = __uint_as_float(r6);
+  v[7] = __uint_as_float(r7);
+}
+
+__device__ __forceinline__ uint32_t tmem_lane_base(int warp) { return (uint32_t)(32 * (warp & 3)) << 16; }
+
+// the six piece products (i, j), i + j <= 2, smallest first
+__host__ __device__ constexpr int prod_a(int q) { return q == 0 ? 2 : (q == 1 || q == 3) ? 1 : 0; }
+__host__ __device__ constexpr int prod_b(int q) { return q == 2 ? 2 : (q == 1 || q == 4) ? 1 : 0; }
+
+}  // namespace tc
+}  // namespace fdsdf

@@ -1,0 +1,107 @@
+// tcprobe.cu -- self-test of the tcgen05 bf16x6 contraction core (tc.cuh) on a plain GEMM.
+//
+//   D[m][n] = sum_k W[m][k] * B[n][k]        (W: [M][K] row-major, B: [N][K] row-major)
+//
+// One CTA, synchronous K loop: the 256 threads split each K chunk of W and B into bf16
+// pieces and store them in the K-major SWIZZLE_128B layout, one thread issues the
+// (M/128) x 4 x nprod tcgen05.mma per chunk, tcgen05.commit signals an mbarrier, and at the
+// end every warp reads its TMEM lane quarter with tcgen05.ld.  It exercises exactly the
+// descriptors, instruction descriptor, swizzle and TMEM mapping of the production kernels,
+// so a layout error shows up here as a wrong GEMM rather than as a wrong curvature.
+#include "../../include/fdsdf.h"
+#include "tc.cuh"
+
+namespace fdsdf {
+
+__global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict__ W, const float* __restrict__ B,
+                                                         float* __restrict__ D, int M, int N, int K, int nprod) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // carve: A pieces [3][M x 128 B], B pieces [3][N x 128 B], mbarrier, tmem slot
+  unsigned char* base = smem_raw;
+  {
+    const uint32_t a = smem_u32(base);
+    base += (1024 - (a & 1023)) & 1023;
+  }
+  unsigned char* As = base;
+  unsigned char* Bs = As + 3 * M * 128;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + 3 * N * 128);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int MH = M / 128;
+  uint32_t ncols = 32;
+  while (ncols < (uint32_t)(MH * N)) ncols <<= 1;
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, ncols);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t idesc = tc::idesc_bf16(128, N);
+  const int q0 = nprod == 1 ? 5 : (nprod == 3 ? 3 : 0);
+
+  for (int kc = 0; kc < K / 64; ++kc) {
+    // stage chunk kc: element (r, k) of the chunk, split into 3 pieces
+    for (int i = tid; i < M * 64; i += 256) {
+      const int r = i >> 6, k = i & 63;
+      const tc::Bf3 s = tc::split3(W[(size_t)r * K + kc * 64 + k]);
+      const uint32_t o = tc::sw128_off(r, k, M);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(As + p * M * 128 + o) = s.p[p];
+    }
+    for (int i = tid; i < N * 64; i += 256) {
+      const int r = i >> 6, k = i & 63;
+      const tc::Bf3 s = tc::split3(B[(size_t)r * K + kc * 64 + k]);
+      const uint32_t o = tc::sw128_off(r, k, N);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * N * 128 + o) = s.p[p];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      for (int s = 0; s < 4; ++s)
+        for (int h = 0; h < MH; ++h)
+          for (int q = q0; q < 6; ++q) {
+            const uint32_t aa = smem_u32(As + tc::prod_a(q) * M * 128 + h * 128 * 128 + s * 32);
+            const uint32_t bb = smem_u32(Bs + tc::prod_b(q) * N * 128 + s * 32);
+            tc::mma_bf16(tbase + h * N, tc::sdesc_sw128(aa), tc::sdesc_sw128(bb), idesc,
+                         (kc | s | (q - q0)) != 0 ? 1u : 0u);
+          }
+      tc::mma_commit(bar);
+    }
+    mbar_wait(bar, kc & 1);
+    tc::fence_after();
+  }
+  // epilogue: warp w reads lane quarter w%4 of M-halves h = w/4, w/4 + 2, ...
+  for (int h = warp >> 2; h < MH; h += 2) {
+    const int m = h * 128 + 32 * (warp & 3) + (tid & 31);
+    for (int n0 = 0; n0 < N; n0 += 8) {
+      float v[8];
+      tc::tmem_ld8(tbase + tc::tmem_lane_base(warp) + h * N + n0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) D[(size_t)m * N + n0 + j] = v[j];
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, ncols);
+}
+
+}  // namespace fdsdf
+
+extern "C" fdsdf_status fdsdf_selftest_mma(const float* d_W, const float* d_B, float* d_D, int M, int N, int K,
+                                           int nprod, void* stream) {
+  using namespace fdsdf;
+  if (!d_W || !d_B || !d_D) return FDSDF_E_INVALID;
+  if (M < 128 || M > 256 || M % 128 || N < 16 || N > 256 || N % 16 || K < 64 || K % 64) return FDSDF_E_INVALID;
+  if (nprod != 1 && nprod != 3 && nprod != 6) return FDSDF_E_INVALID;
+  const size_t smem = 3 * (size_t)(M + N) * 128 + 64 + 1024;
+  cudaError_t e = cudaFuncSetAttribute(tcprobe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return FDSDF_E_CUDA;
+  tcprobe_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(d_W, d_B, d_D, M, N, K, nprod);
+  return cudaGetLastError() == cudaSuccess ? FDSDF_OK : FDSDF_E_CUDA;
+}
