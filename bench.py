@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--config", choices=("c2", "c5"), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--path", choices=("default", "ffma", "tensor"), default="default",
+                    help="contraction path of the library (default: the library's choice)")
     return ap.parse_args()
 
 
@@ -215,7 +217,7 @@ def main():
     cfg = workload(args.config, rank, world)
     n = len(cfg["x"])
     spec = cfg["spec"]
-    model = FDSDF(spec, local, max_centers=n)
+    model = FDSDF(spec, local, max_centers=n, path=None if args.path == "default" else args.path)
     P = model.P
     if world > 1:
         uid = F.fdsdf_comm_unique_id() if rank == 0 else bytes(128)

@@ -143,7 +143,14 @@ typedef struct fdsdf_ctx fdsdf_ctx;
  * Errors: invalid spec (width out of range, < 2 layers, beta/omega <= 0, skip_at out of
  * range) -> FDSDF_E_INVALID; no sm_100 device -> FDSDF_E_UNSUPPORTED;
  * allocation failure -> FDSDF_E_NOMEM.  *out is NULL on failure. */
-enum { FDSDF_CREATE_EVAL_ONLY = 1u };
+enum {
+  FDSDF_CREATE_EVAL_ONLY = 1u,  /* no step workspace                                          */
+  FDSDF_CREATE_FFMA = 2u,       /* run every contraction as fp32 FFMA (the validation path)   */
+  FDSDF_CREATE_TENSOR = 4u      /* run the forward contractions on tcgen05 tensor cores with   */
+                                /* the fp32-accurate bf16x6 piece scheme;     */
+                                /* needs hidden widths <= 256 and no skip layer, else         */
+                                /* FDSDF_E_UNSUPPORTED.  Both flags -> FDSDF_E_INVALID.       */
+};
 fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_centers,
                           uint32_t flags, fdsdf_ctx** out);
 
@@ -192,6 +199,9 @@ const char* fdsdf_status_string(fdsdf_status s);
 const char* fdsdf_last_error(const fdsdf_ctx* ctx);
 /* Returns and clears the sticky device flags (synchronises the context's device). */
 fdsdf_status fdsdf_get_device_flags(fdsdf_ctx* ctx, uint32_t* out);
+/* Which contraction path the context runs: FDSDF_PATH_FFMA or FDSDF_PATH_TENSOR (-1: NULL). */
+enum { FDSDF_PATH_FFMA = 0, FDSDF_PATH_TENSOR = 1 };
+int32_t fdsdf_path(const fdsdf_ctx* ctx);
 /* Number of kernel launches enqueued by the last eval/step call on this context. */
 int32_t fdsdf_last_launch_count(const fdsdf_ctx* ctx);
 /* Per-kernel timing (for benchmarks).  When enabled, every kernel launch (and the NCCL group)
@@ -203,12 +213,15 @@ int32_t fdsdf_last_launch_count(const fdsdf_ctx* ctx);
  * a failed event query -> FDSDF_E_CUDA. */
 enum {
   FDSDF_KSLOT_PACK = 0,      /* weight re-layout for the TMA slabs                        */
-  FDSDF_KSLOT_FWD = 1,       /* fused centre + stencil forward + FD epilogue             */
+  FDSDF_KSLOT_FWD = 1,       /* fused centre + stencil forward + FD epilogue (tensor path: */
+                             /* the stencil-pair columns + FD epilogue)                    */
   FDSDF_KSLOT_BWD = 2,       /* backward through every stencil evaluation                */
   FDSDF_KSLOT_WGRAD = 3,     /* split-K weight-gradient contraction                      */
   FDSDF_KSLOT_FINALIZE = 4,  /* fixed-order reduction of partials and loss               */
   FDSDF_KSLOT_ALLREDUCE = 5, /* NCCL group (not a kernel of this library)                */
-  FDSDF_NUM_KSLOTS = 6
+  FDSDF_KSLOT_PACK_TC = 6,   /* bf16x3 weight images for the tensor-core kernels           */
+  FDSDF_KSLOT_FWD_CENTRE = 7,/* tensor path: centre + tangent columns (f, grad f, frame)   */
+  FDSDF_NUM_KSLOTS = 8
 };
 fdsdf_status fdsdf_set_kernel_timing(fdsdf_ctx* ctx, int enable);
 fdsdf_status fdsdf_kernel_times(fdsdf_ctx* ctx, double* ms_total, int64_t* count, int nslots, int reset);

@@ -85,9 +85,15 @@ struct fdsdf_ctx {
   float* bacc = nullptr;
   float* part = nullptr;
   unsigned* dflags = nullptr;
+  // tensor-core (tcgen05 bf16x6) forward
+  bool tc = false;
+  unsigned char* fimg = nullptr;  // packed forward weight image
+  float* cinfo = nullptr;    // [max_centers][16]
+  float* zev = nullptr;      // eval-only contexts: [max_centers][nh][mpad] centre pre-activations
   void* comm = nullptr;
   int rank = 0, world = 1;
   int launches = 0;
+  int last_fgrid = 0;
   std::string err;
   // optional per-kernel CUDA-event timing (fdsdf_set_kernel_timing)
   bool timing = false;
@@ -139,7 +145,11 @@ static int layer_fan_in(const fdsdf_mlp_spec* s, int l) { return s->width[l] + (
 
 extern "C" {
 
-const char* fdsdf_version(void) { return "fdsdf 0.1 (sm_100a, pair-symmetric difference form, fp32 FFMA)"; }
+const char* fdsdf_version(void) {
+  return "fdsdf 0.2 (sm_100a, pair-symmetric difference form; fp32 FFMA and tcgen05 bf16x6 paths)";
+}
+
+int32_t fdsdf_path(const fdsdf_ctx* c) { return c ? (c->tc ? FDSDF_PATH_TENSOR : FDSDF_PATH_FFMA) : -1; }
 
 const char* fdsdf_status_string(fdsdf_status s) {
   switch (s) {
@@ -204,7 +214,8 @@ void fdsdf_destroy(fdsdf_ctx* c) {
     cudaEventDestroy(r.b);
   }
   for (cudaEvent_t e : c->spare) cudaEventDestroy(e);
-  void* bufs[] = {c->wt, c->wb, c->zf, c->zscr, c->seed, c->lossp, c->del, c->actv, c->bacc, c->part, c->dflags};
+  void* bufs[] = {c->wt,   c->wb,   c->zf,     c->zscr,   c->seed,  c->lossp, c->del, c->actv,
+                  c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev};
   for (void* b : bufs)
     if (b) cudaFree(b);
   cudaSetDevice(prev);
@@ -233,6 +244,19 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
   for (int l = 1; l < c->L; ++l) wmax = std::max(wmax, spec->width[l]);
   if (spec->skip_at >= 0) wmax = std::max(wmax, spec->width[spec->skip_at] + 3);
   c->mpad = wmax <= 64 ? 64 : (wmax <= 128 ? 128 : (wmax <= 256 ? 256 : 512));
+  if ((flags & FDSDF_CREATE_FFMA) && (flags & FDSDF_CREATE_TENSOR)) {
+    delete c;
+    return FDSDF_E_INVALID;
+  }
+  if (flags & FDSDF_CREATE_TENSOR) {
+    const int mp_tc = std::max(c->mpad, 128);  // widths <= 64 are zero-padded to one M=128 tile
+    if (!tc_supported(mp_tc, spec->skip_at)) {
+      delete c;
+      return FDSDF_E_UNSUPPORTED;
+    }
+    c->tc = true;
+    c->mpad = mp_tc;
+  }
   c->P = fdsdf_spec_num_params(spec);
   for (int l = 0; l < c->L; ++l) {
     c->offW[l] = fdsdf_spec_param_offset(spec, l, 0);
@@ -276,7 +300,8 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
   ok = ok && alloc((void**)&c->wt, gemm_w);
   ok = ok && alloc((void**)&c->wb, gemm_w);
   ok = ok && alloc((void**)&c->zscr, (size_t)c->fgrid * c->ftile * c->nh * mp * sizeof(float));
-  ok = ok && alloc((void**)&c->lossp, (size_t)c->fgrid * NLOSS * sizeof(double));
+  // per-CTA loss partials of the forward: the FFMA grid, or up to one CTA per SM (tensor path)
+  ok = ok && alloc((void**)&c->lossp, (size_t)std::max(c->fgrid, c->nsm) * NLOSS * sizeof(double));
   ok = ok && alloc((void**)&c->dflags, sizeof(unsigned));
   if (ok && !c->eval_only) {
     ok = ok && alloc((void**)&c->zf, (size_t)max_centers * c->nh * NCOLF * mp * sizeof(float));
@@ -285,6 +310,11 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     ok = ok && alloc((void**)&c->actv, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
     ok = ok && alloc((void**)&c->bacc, (size_t)c->bgrid * c->nacc * sizeof(float));
     ok = ok && alloc((void**)&c->part, (size_t)std::max(0, c->ngemm) * c->nsplit * mp * mp * sizeof(float));
+  }
+  if (ok && c->tc) {
+    ok = ok && alloc((void**)&c->fimg, tc_wimg_bytes(mp, c->ngemm));
+    ok = ok && alloc((void**)&c->cinfo, (size_t)max_centers * 16 * sizeof(float));
+    if (c->eval_only) ok = ok && alloc((void**)&c->zev, (size_t)max_centers * c->nh * mp * sizeof(float));
   }
   if (ok) ok = cudaMemset(c->dflags, 0, sizeof(unsigned)) == cudaSuccess;
   cudaSetDevice(prev);
@@ -355,6 +385,22 @@ static void fill_fwd(fdsdf_ctx* c, FwdArgs& a, const float* d_x, int64_t n, cons
   a.ls.eps_grad = st->eps_grad;
 }
 
+// tensor-core forward: mode 1 (centre + tangents -> f, g, frame) then mode 2 (stencil pairs ->
+// FD epilogue).  Sets a.ntiles per launch; records the mode-2 grid in c->last_fgrid.
+static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t strm) {
+  a.wimg = c->fimg;
+  a.cinfo = c->cinfo;
+  const int64_t n = a.n;
+  a.ntiles = (n + fwd_tc_tile_centres(1) - 1) / fwd_tc_tile_centres(1);
+  const int g1 = (int)std::min<int64_t>(c->nsm, a.ntiles);
+  cudaError_t e = run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc(a, 1, g1, strm); });
+  if (e != cudaSuccess) return e;
+  a.ntiles = (n + fwd_tc_tile_centres(2) - 1) / fwd_tc_tile_centres(2);
+  const int g2 = (int)std::min<int64_t>(c->nsm, a.ntiles);
+  c->last_fgrid = g2;
+  return run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd_tc(a, 2, g2, strm); });
+}
+
 extern "C" {
 
 fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
@@ -368,7 +414,12 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   fill_net(c, d_params);
   c->launches = 0;
   cudaError_t e = cudaSuccess;
-  if (c->ngemm > 0) e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
+  if (c->tc) {
+    if (c->ngemm > 0)
+      e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, nullptr, strm); });
+  } else if (c->ngemm > 0) {
+    e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
+  }
   if (e != cudaSuccess) {
     if (prev != c->device) cudaSetDevice(prev);
     return cuda_fail(c, e, "pack");
@@ -386,6 +437,14 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
     a.out_D = out->d_D;
     a.out_frames = out->d_frames;
     a.out_mask = out->d_mask;
+  }
+  if (c->tc) {
+    a.zf = c->eval_only ? c->zev : c->zf;
+    a.zcols = c->eval_only ? 1 : NCOLF;
+    e = launch_fwd_tc_pair(c, a, strm);
+    if (prev != c->device) cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fwd_tc_kernel");
+    return FDSDF_OK;
   }
   const int grid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
   e = run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd(a, grid, strm); });
@@ -429,6 +488,9 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   cudaError_t e = cudaSuccess;
   if (c->ngemm > 0) e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "pack"));
+  if (c->tc && c->ngemm > 0)
+    e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, nullptr, strm); });
+  if (e != cudaSuccess) return done(cuda_fail(c, e, "pack_tc"));
 
   FwdArgs a{};
   fill_fwd(c, a, d_x, n, st);
@@ -445,8 +507,14 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   a.step = 1;
   a.zf = c->zf;
   a.seed = c->seed;
-  const int fgrid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
-  e = run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd(a, fgrid, strm); });
+  int fgrid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
+  if (c->tc) {
+    a.zcols = NCOLF;
+    e = launch_fwd_tc_pair(c, a, strm);
+    fgrid = c->last_fgrid;
+  } else {
+    e = run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd(a, fgrid, strm); });
+  }
   if (e != cudaSuccess) return done(cuda_fail(c, e, "fwd_kernel"));
 
   BwdArgs b{};

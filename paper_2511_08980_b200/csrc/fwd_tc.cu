@@ -1,0 +1,449 @@
+// fwd_tc.cu -- the forward of the FD curvature step on the 5th-generation tensor cores
+// (precision scheme bf16x6, tc.cuh / DESIGN.md §4b).
+//
+// Two launches of one warp-specialised persistent kernel, one CTA per SM:
+//   mode 1  columns (z, dz/dx, dz/dy, dz/dz) of 16 centres (forward-mode tangents give
+//           g = grad f); last layer -> f, g; per centre the degenerate mask and the
+//           random right-handed frame -> cinfo.
+//   mode 2  the 8 pair columns (A, S) x {u, v, u+v, u-v} of 8 centres in the pair-symmetric
+//           difference form (act.cuh; P:L83-91 regrouped); last layer -> S_p; per centre the
+//           FD epilogue (fdepi.cuh: f_uu, f_vv, f_uv, D_FD, K_FD, Eq. (1), seeds).
+// Every hidden GEMM layer is D[m][n] = sum_k W[m][k] B[k][n] with M = MPAD output neurons
+// (MPAD/128 tcgen05 M-halves), N = 64 columns, K = MPAD:
+//   warp 0      one thread streams the pre-packed bf16x3 weight image through a 2-stage
+//               shared-memory ring with the TMA bulk engine (cp.async.bulk + mbarrier tx);
+//   warp 1      allocates TMEM; one thread issues the 6 piece MMAs per 16-wide K step
+//               (tcgen05.mma kind::f16, fp32 accumulate in TMEM) and commits to mbarriers;
+//   warps 2..9  epilogue: thread = output neuron (TMEM lane), reads its row of D with
+//               tcgen05.ld, applies bias / omega / the activation (centre + tangents, or the
+//               cancellation-free pair maps), stores the pre-activations the backward needs,
+//               splits the outputs into bf16 pieces and writes them into the K-major
+//               SWIZZLE_128B B operand of the next layer.
+// Layer 0 (fan-in 3) and the last layer (fan-out 1) are computed by the epilogue threads
+// directly (FFMA) -- they are not contractions worth a tensor-core pass.
+#include "act.cuh"
+#include "fdepi.cuh"
+#include "tc.cuh"
+
+namespace fdsdf {
+
+template <int MPAD>
+struct FtcCfg {
+  static constexpr int N = 64;                  // GEMM columns per tile
+  static constexpr int MH = MPAD / 128;         // tcgen05 M-halves (M = 128 each)
+  static constexpr int KC = MPAD / 64;          // K chunks (one 128-byte swizzle row each)
+  static constexpr int STAGE = 3 * 128 * 128;   // W stage (kc, h): 3 pieces x 128 rows x 128 B
+  static constexpr int NST = 2;                 // W ring depth
+  static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
+  static constexpr int NEPI = 8;                // epilogue warps
+  static constexpr int NTHR = (2 + NEPI) * 32;
+  static constexpr int EG = NEPI / (4 * MH);    // epilogue warps per (lane quarter, M-half)
+  static constexpr int MAXC = 16;               // max centres per tile
+  static constexpr int OFF_W = 0;
+  static constexpr int OFF_B = NST * STAGE;
+  static constexpr int OFF_RED = OFF_B + 3 * BPIECE;               // float [NEPI][MAXC][4]
+  static constexpr int OFF_CI = OFF_RED + NEPI * MAXC * 4 * 4;     // float [MAXC][16]
+  static constexpr int OFF_LV = OFF_CI + MAXC * NCINFO * 4;        // double [MAXC][NLOSS]
+  static constexpr int OFF_BAR = OFF_LV + MAXC * NLOSS * 8;        // mbarriers + TMEM slot
+  static constexpr int BYTES = OFF_BAR + 128 + 1024;               // + alignment slack
+  static constexpr uint32_t TCOLS = (MH * N) < 32 ? 32 : (uint32_t)(MH * N);
+};
+
+bool tc_supported(int mpad, int skip) { return (mpad == 128 || mpad == 256) && skip < 0; }
+
+size_t tc_wimg_bytes(int mpad, int ngemm) { return (size_t)(ngemm > 0 ? ngemm : 0) * mpad * mpad * 6; }
+
+int fwd_tc_tile_centres(int mode) { return mode == 1 ? 16 : 8; }
+
+// ----------------------------------------------------------------------------- weight images
+// image[g][kc][h][piece][sw128 128 rows x 64 k]: forward A operand = W_l (rows = output
+// neuron m, K = input neuron k); backward A operand = W_l^T (rows = k, K = m).
+__global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char* bimg) {
+  const int mp = net.mpad;
+  const int KC = mp / 64, MH = mp / 128;
+  const int g = blockIdx.y;
+  const int l = g + 1;
+  const int M = net.width[l + 1];
+  const int K = net.width[l];
+  const float* W = net.W[l];
+  const size_t per_layer = (size_t)mp * mp * 6;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < mp * mp; idx += gridDim.x * blockDim.x) {
+    const int r = idx / mp, k = idx % mp;  // A-operand row r, K index k
+    const int h = r >> 7, rr = r & 127, kc = k >> 6, kk = k & 63;
+    const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * FtcCfg<128>::STAGE + tc::sw128_off(rr, kk, 128);
+    {
+      const float v = (r < M && k < K) ? W[(size_t)r * K + k] : 0.f;  // forward: W[m = r][k]
+      const tc::Bf3 s = tc::split3(v);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(fimg + off + p * 16384) = s.p[p];
+    }
+    if (bimg) {
+      const float v = (k < M && r < K) ? W[(size_t)k * K + r] : 0.f;  // backward: W^T[k = r][m = k]
+      const tc::Bf3 s = tc::split3(v);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(bimg + off + p * 16384) = s.p[p];
+    }
+  }
+  (void)KC;
+}
+
+cudaError_t launch_pack_tc(const Net& net, unsigned char* fimg, unsigned char* bimg, cudaStream_t st) {
+  if (net.L <= 2) return cudaSuccess;
+  dim3 grid(64, net.L - 2);
+  pack_tc_kernel<<<grid, 256, 0, st>>>(net, fimg, bimg);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- the kernel
+template <int ACT, int MPAD, int MODE>
+__global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const FwdArgs a) {
+  using C = FtcCfg<MPAD>;
+  using AF = Act<ACT>;
+  constexpr int N = C::N, MH = C::MH, KC = C::KC, NST = C::NST;
+  constexpr int CPC = MODE == 1 ? 4 : 8;  // columns per centre
+  constexpr int CT = N / CPC;             // centres per tile
+  constexpr int CPE = CT / C::EG;         // centres per epilogue thread
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = smem_raw;
+  sm += (1024 - (smem_u32(sm) & 1023)) & 1023;
+  unsigned char* Ws = sm + C::OFF_W;
+  unsigned char* Bs = sm + C::OFF_B;
+  float* red = reinterpret_cast<float*>(sm + C::OFF_RED);
+  float* cis = reinterpret_cast<float*>(sm + C::OFF_CI);
+  double* lvs = reinterpret_cast<double*>(sm + C::OFF_LV);
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* wempty = wfull + NST;
+  uint64_t* bfull = wempty + NST;
+  uint64_t* dfull = bfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + 1);
+
+  const Net& net = a.net;
+  const int L = net.L;
+  const int nh = L - 1;
+  const int ngemm = L - 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
+    }
+    mbar_init(bfull, C::NEPI);
+    mbar_init(dfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, C::TCOLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ W producer
+    if (lane == 0 && ngemm > 0) {
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
+        for (int g = 0; g < ngemm; ++g)
+          for (int kc = 0; kc < KC; ++kc)
+            for (int h = 0; h < MH; ++h, ++it) {
+              const int s = (int)(it % NST);
+              const uint32_t ph = (it / NST) & 1u;
+              mbar_wait(&wempty[s], ph ^ 1u);
+              mbar_arrive_expect_tx(&wfull[s], C::STAGE);
+              bulk_g2s(Ws + s * C::STAGE, a.wimg + (((size_t)g * KC + kc) * MH + h) * C::STAGE, C::STAGE,
+                       &wfull[s]);
+            }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0 && ngemm > 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(128, N);
+      uint32_t it = 0, nb = 0;
+      for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
+        for (int g = 0; g < ngemm; ++g) {
+          mbar_wait(bfull, nb & 1u);
+          ++nb;
+          tc::fence_after();
+          for (int kc = 0; kc < KC; ++kc)
+            for (int h = 0; h < MH; ++h, ++it) {
+              const int s = (int)(it % NST);
+              const uint32_t ph = (it / NST) & 1u;
+              mbar_wait(&wfull[s], ph);
+              tc::fence_after();
+              const uint32_t wa = smem_u32(Ws + s * C::STAGE);
+              const uint32_t ba = smem_u32(Bs + kc * N * 128);
+#pragma unroll
+              for (int sub = 0; sub < 4; ++sub)
+#pragma unroll
+                for (int q = 0; q < 6; ++q) {
+                  const uint64_t ad = tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32);
+                  const uint64_t bd = tc::sdesc_sw128(ba + tc::prod_b(q) * C::BPIECE + sub * 32);
+                  tc::mma_bf16(tbase + h * N, ad, bd, idesc, (kc | sub | q) != 0 ? 1u : 0u);
+                }
+              tc::mma_commit(&wempty[s]);
+            }
+          tc::mma_commit(dfull);
+        }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue warps
+    const int ew = warp - 2;                 // 0..7
+    const int et = tid - 64;                 // 0..255
+    const int q4 = warp & 3;                 // TMEM lane quarter
+    const int hh = (ew >> 2) % MH;           // M-half
+    const int eg = ew / (4 * MH);            // centre group
+    const int m = hh * 128 + 32 * q4 + lane; // output neuron of this thread
+    const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * N;
+    const float beta = net.beta;
+    const float h = a.h;
+    const bool step = a.step != 0;
+    uint32_t nd = 0;
+    double lacc[NLOSS];
+#pragma unroll
+    for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
+
+    // this thread's element of stored pre-activation column `col`, layer l, centre c
+    auto zp = [&](int64_t c, int l, int col) -> float* {
+      return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
+    };
+    auto put_b = [&](int n, float v) {
+      const tc::Bf3 s = tc::split3(v);
+      const uint32_t off = tc::sw128_off(n, m, N);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::BPIECE + off) = s.p[p];
+    };
+
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      const int64_t c0 = tile * CT;
+      if (MODE == 2) {  // the tile's centre info (f, g, frame, mask) from mode 1
+        for (int i = et; i < CT * NCINFO; i += C::NEPI * 32) {
+          const int64_t c = c0 + i / NCINFO;
+          cis[i] = c < a.n ? a.cinfo[c * NCINFO + (i % NCINFO)] : 0.f;
+        }
+        bar_named(1, C::NEPI * 32);
+      }
+      float part[CPE][4];
+#pragma unroll
+      for (int i = 0; i < CPE; ++i) part[i][0] = part[i][1] = part[i][2] = part[i][3] = 0.f;
+
+      for (int l = 0; l <= L - 2; ++l) {
+        const bool last = (l == L - 2);
+        const int M = net.width[l + 1];
+        const float om = net.omega[l];
+        const bool mok = m < M;
+        const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
+        if (l > 0) {
+          mbar_wait(dfull, nd & 1u);
+          ++nd;
+          tc::fence_after();
+        }
+#pragma unroll 1
+        for (int i = 0; i < CPE; ++i) {
+          const int cl = eg + C::EG * i;  // centre slot in the tile
+          const int64_t c = c0 + cl;
+          const bool valid = c < a.n;
+          if (MODE == 1) {
+            float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
+            if (l == 0) {
+              float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+              if (valid) {
+                x0 = a.x[c * 3 + 0];
+                x1 = a.x[c * 3 + 1];
+                x2 = a.x[c * 3 + 2];
+                if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
+              }
+              if (mok) {
+                const float* W0 = net.W[0];
+                const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+                z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + net.b[0][m]);
+                t0 = om * w0;
+                t1 = om * w1;
+                t2 = om * w2;
+              }
+            } else {
+              float v[8];
+              tc::tmem_ld8(taddr + (uint32_t)((cl >> 1) * 8), v);
+              const int o = (cl & 1) * 4;
+              if (mok) {
+                z = om * (v[o] + net.b[l][m]);
+                t0 = om * v[o + 1];
+                t1 = om * v[o + 2];
+                t2 = om * v[o + 3];
+              }
+            }
+            if (valid) {
+              *zp(c, l, 0) = z;
+              if (step) {
+                *zp(c, l, 1) = t0;
+                *zp(c, l, 2) = t1;
+                *zp(c, l, 3) = t2;
+              }
+            }
+            float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+            if (mok) {
+              const typename AF::C cc = AF::centre(z, beta);
+              const float s1 = AF::d1(cc, beta);
+              o0 = AF::value(cc, beta);
+              o1 = s1 * t0;
+              o2 = s1 * t1;
+              o3 = s1 * t2;
+            }
+            if (last) {
+              part[i][0] = fmaf(wl, o0, part[i][0]);
+              part[i][1] = fmaf(wl, o1, part[i][1]);
+              part[i][2] = fmaf(wl, o2, part[i][2]);
+              part[i][3] = fmaf(wl, o3, part[i][3]);
+            } else {
+              put_b(cl * 4 + 0, o0);
+              put_b(cl * 4 + 1, o1);
+              put_b(cl * 4 + 2, o2);
+              put_b(cl * 4 + 3, o3);
+            }
+          } else {
+            const float* ci = cis + cl * NCINFO;
+            float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
+            if (l == 0) {
+              if (mok) {
+                const float* W0 = net.W[0];
+                const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+                const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
+                const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
+                const float hs = om * h;
+                Av[0] = hs * du;
+                Av[1] = hs * dv;
+                Av[2] = hs * (du + dv);
+                Av[3] = hs * (du - dv);
+              }
+            } else {
+              float v[8];
+              tc::tmem_ld8(taddr + (uint32_t)(cl * 8), v);
+              if (mok) {
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                  Av[p] = om * v[2 * p];
+                  Sv[p] = om * v[2 * p + 1];
+                }
+              }
+            }
+            const float z0 = valid ? *zp(c, l, 0) : 0.f;
+            if (step && valid) {
+#pragma unroll
+              for (int p = 0; p < 4; ++p) {
+                *zp(c, l, 4 + 2 * p) = Av[p];
+                *zp(c, l, 5 + 2 * p) = Sv[p];
+              }
+            }
+            float o[8];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) o[p] = 0.f;
+            if (mok) {
+              const typename AF::C cc = AF::centre(z0, beta);
+#pragma unroll
+              for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &o[2 * p], &o[2 * p + 1]);
+            }
+            if (last) {
+#pragma unroll
+              for (int p = 0; p < 4; ++p) part[i][p] = fmaf(wl, o[2 * p + 1], part[i][p]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) put_b(cl * 8 + j, o[j]);
+            }
+          }
+        }
+        if (!last) {  // B operand of layer l+1 complete (this warp's part): hand to the MMA thread
+          tc::fence_before();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bfull);
+        } else if (l > 0) {
+          tc::fence_before();
+        }
+      }
+
+      // ---------------------------------------------------------------- last layer: sum over neurons
+#pragma unroll
+      for (int i = 0; i < CPE; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float v = part[i][j];
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          if (lane == 0) red[(ew * C::MAXC + eg + C::EG * i) * 4 + j] = v;
+        }
+      bar_named(1, C::NEPI * 32);
+      if (et < CT) {
+        const int cl = et;
+        const int64_t c = c0 + cl;
+        const bool valid = c < a.n;
+        float tot[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float v = 0.f;
+          for (int w = 0; w < C::NEPI; ++w)
+            if ((w / (4 * MH)) == (cl % C::EG)) v += red[(w * C::MAXC + cl) * 4 + j];
+          tot[j] = v;
+        }
+        if (MODE == 1) {
+          float* ci = cis + cl * NCINFO;
+          centre_frame(a, c, valid, tot[0] + net.b[L - 1][0], tot[1], tot[2], tot[3], ci);
+          if (valid) {
+#pragma unroll
+            for (int q = 0; q < NCINFO; ++q) a.cinfo[c * NCINFO + q] = ci[q];
+          }
+        } else {
+          double lv[NLOSS];
+          fd_centre(a, c, valid, tot, cis + cl * NCINFO, lv);
+#pragma unroll
+          for (int q = 0; q < NLOSS; ++q) lvs[cl * NLOSS + q] = lv[q];
+        }
+      }
+      bar_named(1, C::NEPI * 32);
+      if (MODE == 2 && et == 0) {  // fixed-order tile reduction of the loss terms
+        for (int s2 = 0; s2 < CT; ++s2)
+#pragma unroll
+          for (int q = 0; q < NLOSS; ++q) lacc[q] += lvs[s2 * NLOSS + q];
+      }
+    }
+    if (MODE == 2 && et == 0) {
+#pragma unroll
+      for (int q = 0; q < NLOSS; ++q) a.lossp[(size_t)blockIdx.x * NLOSS + q] = lacc[q];
+    }
+  }
+
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, C::TCOLS);
+}
+
+// ----------------------------------------------------------------------------- host launch
+template <int ACT, int MPAD, int MODE>
+static cudaError_t launch_fwd_tc_t(const FwdArgs& a, int grid, cudaStream_t st) {
+  using C = FtcCfg<MPAD>;
+  auto k = fwd_tc_kernel<ACT, MPAD, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  if (e != cudaSuccess) return e;
+  k<<<grid, C::NTHR, C::BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd_tc(const FwdArgs& a, int mode, int grid, cudaStream_t st) {
+  const int act = a.net.act, mp = a.net.mpad;
+#define FDSDF_CASE(A, MP, MO) \
+  if (act == A && mp == MP && mode == MO) return launch_fwd_tc_t<A, MP, MO>(a, grid, st);
+  FDSDF_CASE(ACT_SINE, 128, 1)
+  FDSDF_CASE(ACT_SINE, 128, 2)
+  FDSDF_CASE(ACT_SINE, 256, 1)
+  FDSDF_CASE(ACT_SINE, 256, 2)
+  FDSDF_CASE(ACT_SOFTPLUS, 128, 1)
+  FDSDF_CASE(ACT_SOFTPLUS, 128, 2)
+  FDSDF_CASE(ACT_SOFTPLUS, 256, 1)
+  FDSDF_CASE(ACT_SOFTPLUS, 256, 2)
+#undef FDSDF_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fdsdf

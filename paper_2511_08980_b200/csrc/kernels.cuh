@@ -62,6 +62,10 @@ struct FwdArgs {
   double* lossp;         // [gridDim.x][NLOSS]
   unsigned* dflags;      // sticky device flags
   int64_t ntiles;
+  // tensor-core path (fwd_tc.cu)
+  int zcols;             // columns per (centre, layer) in zf: 12 (step) or 1 (eval: z only)
+  const unsigned char* wimg;  // packed bf16x3 forward weight image (pack_tc_kernel)
+  float* cinfo;          // [n][16] per-centre f, g, u, v, mask (written by mode 1, read by mode 2)
 };
 
 struct BwdArgs {
@@ -117,6 +121,12 @@ cudaError_t launch_fwd(const FwdArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bwd(const BwdArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_wgrad(const WgradArgs& a, int nglayers, cudaStream_t st);
 cudaError_t launch_finalize(const FinArgs& a, cudaStream_t st);
+// tensor-core (tcgen05, bf16x6) path: available for padded widths 128 / 256 without skip
+bool tc_supported(int mpad, int skip);
+size_t tc_wimg_bytes(int mpad, int ngemm);          // one packed weight image (fwd or bwd)
+cudaError_t launch_pack_tc(const Net& net, unsigned char* fwd_img, unsigned char* bwd_img, cudaStream_t st);
+cudaError_t launch_fwd_tc(const FwdArgs& a, int mode, int grid, cudaStream_t st);
+int fwd_tc_tile_centres(int mode);                  // 16 (mode 1) / 8 (mode 2)
 int fwd_tile_centres(int mpad);   // centres per forward tile
 int bwd_tile_centres(int mpad);   // centres per backward tile
 size_t fwd_smem_bytes(int mpad);

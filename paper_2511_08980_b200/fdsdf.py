@@ -21,7 +21,8 @@ DENOM = {"paper": 0, "one": 1, "grad": 2}
 KIND = {"ncr": 0, "nsh": 1}
 FD_FORM = {"abs": 0, "square": 1}
 STEP_ACCUMULATE, STEP_ALLREDUCE = 1, 2
-CREATE_EVAL_ONLY = 1
+CREATE_EVAL_ONLY, CREATE_FFMA, CREATE_TENSOR = 1, 2, 4
+PATH = {0: "ffma", 1: "tensor"}
 FLAG_NONFINITE_INPUT, FLAG_NONFINITE_LOSS, FLAG_ALL_FD_SKIPPED = 1, 2, 4
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_EMPTY", 3: "E_CUDA", 4: "E_NCCL", 5: "E_NOMEM",
           6: "E_UNSUPPORTED"}
@@ -96,6 +97,8 @@ def lib():
         L.fdsdf_last_error.restype = C.c_char_p
         L.fdsdf_get_device_flags.argtypes = [vp, C.POINTER(u32)]
         L.fdsdf_get_device_flags.restype = C.c_int
+        L.fdsdf_path.argtypes = [vp]
+        L.fdsdf_path.restype = i32
         L.fdsdf_last_launch_count.argtypes = [vp]
         L.fdsdf_last_launch_count.restype = i32
         L.fdsdf_set_kernel_timing.argtypes = [vp, C.c_int]
@@ -155,11 +158,13 @@ def fdsdf_spec_num_params(spec: dict) -> int:
     return lib().fdsdf_spec_num_params(C.byref(s))
 
 
-def fdsdf_create(spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False):
+def fdsdf_create(spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False,
+                 path: str | None = None):
+    """path: None (library default), "ffma" or "tensor"."""
     s = make_spec(spec)
     h = C.c_void_p()
-    _check(lib().fdsdf_create(C.byref(s), int(device), int(max_centers),
-                              CREATE_EVAL_ONLY if eval_only else 0, C.byref(h)))
+    flags = (CREATE_EVAL_ONLY if eval_only else 0) | {None: 0, "ffma": CREATE_FFMA, "tensor": CREATE_TENSOR}[path]
+    _check(lib().fdsdf_create(C.byref(s), int(device), int(max_centers), flags, C.byref(h)))
     return h
 
 
@@ -229,7 +234,7 @@ def fdsdf_get_device_flags(ctx) -> int:
 def fdsdf_last_launch_count(ctx) -> int:
     return int(lib().fdsdf_last_launch_count(ctx))
 
-KSLOTS = ("pack", "fwd", "bwd", "wgrad", "finalize", "allreduce")
+KSLOTS = ("pack", "fwd", "bwd", "wgrad", "finalize", "allreduce", "pack_tc", "fwd_centre")
 
 
 def fdsdf_set_kernel_timing(ctx, enable: bool):
@@ -250,11 +255,13 @@ def fdsdf_kernel_times(ctx, reset: bool = False) -> dict:
 class FDSDF:
     """A context bound to one device: eval() / step() on torch CUDA tensors."""
 
-    def __init__(self, spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False):
+    def __init__(self, spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False,
+                 path: str | None = None):
         import torch
         self.spec = spec
         self.device = torch.device("cuda", device)
-        self.ctx = fdsdf_create(spec, device, max_centers, eval_only)
+        self.ctx = fdsdf_create(spec, device, max_centers, eval_only, path)
+        self.path = PATH[int(lib().fdsdf_path(self.ctx))]
         self.P = int(lib().fdsdf_num_params(self.ctx))
         self.max_centers = int(max_centers)
 

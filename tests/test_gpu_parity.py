@@ -26,9 +26,18 @@ def _built():
     build()
 
 
-def _model(spec, n, eval_only=False):
+@pytest.fixture(params=["ffma", "tensor"])
+def path(request):
+    return request.param
+
+
+def _model(spec, n, eval_only=False, path=None):
     from paper_2511_08980_b200 import FDSDF
-    return FDSDF(spec, 0, max_centers=n, eval_only=eval_only)
+    if path == "tensor" and (spec.get("skip_at", -1) >= 0 or max(spec["widths"][1:-1]) > 256):
+        pytest.skip("tensor path needs widths <= 256 and no skip layer (C3 runs FFMA)")
+    m = FDSDF(spec, 0, max_centers=n, eval_only=eval_only, path=path)
+    assert path is None or m.path == path
+    return m
 
 
 # (name, n_surface, n_uniform, h): several tiles + a ragged tail
@@ -37,9 +46,9 @@ EVAL_CASES = [("c1", 1024, 1024, None), ("c1", 37, 29, None), ("c2", 300, 213, 1
 
 
 @pytest.mark.parametrize("name,ns,nu,h", EVAL_CASES)
-def test_eval_parity_given_frames(name, ns, nu, h):
+def test_eval_parity_given_frames(name, ns, nu, h, path):
     c = make_config(name, ns, nu, h=h)
-    m = _model(c["spec"], len(c["x"]), eval_only=True)
+    m = _model(c["spec"], len(c["x"]), eval_only=True, path=path)
     g = gpu_eval(m, c)
     o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
                     frames=(g["frames"][:, :3], g["frames"][:, 3:]))
@@ -51,11 +60,11 @@ def test_eval_parity_given_frames(name, ns, nu, h):
 
 
 @pytest.mark.parametrize("name,ns,nu", [("c1", 1024, 1024), ("c2", 200, 200)])
-def test_eval_parity_self_framed(name, ns, nu):
+def test_eval_parity_self_framed(name, ns, nu, path):
     """End-to-end: the GPU draws its own frame from its fp32 gradient; the oracle from its
     fp64 gradient with the same counter-based SplitMix64 angle."""
     c = make_config(name, ns, nu, h=1e-2)
-    m = _model(c["spec"], len(c["x"]), eval_only=True)
+    m = _model(c["spec"], len(c["x"]), eval_only=True, path=path)
     g = gpu_eval(m, c)
     o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frame_seed=c["frame_seed"])
     fr = np.concatenate([o["u"], o["v"]], 1)
@@ -80,13 +89,13 @@ STEP_CASES = [
 
 
 @pytest.mark.parametrize("case", range(len(STEP_CASES)))
-def test_step_parity(case):
+def test_step_parity(case, path):
     name, ns, nu, ls = STEP_CASES[case]
     c = make_config(name, ns, nu)
     if ls is not None:
         c["loss"] = ls
     n = len(c["x"])
-    m = _model(c["spec"], n)
+    m = _model(c["spec"], n, path=path)
     ev = gpu_eval(m, c, denom=c["loss"]["denom"])
     grad, loss = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])
     grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
@@ -104,9 +113,9 @@ def test_step_parity(case):
     assert np.all(gerr <= GRAD_RTOL), gerr
 
 
-def test_step_deterministic_and_accumulate():
+def test_step_deterministic_and_accumulate(path):
     c = make_config("c2", 300, 300)
-    m = _model(c["spec"], 600)
+    m = _model(c["spec"], 600, path=path)
     g1, l1 = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=7)
     g1, l1 = g1.clone(), l1.clone()
     g2, l2 = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=7)
@@ -117,13 +126,13 @@ def test_step_deterministic_and_accumulate():
     assert m.launch_count() >= 4
 
 
-def test_shard_sum_equals_full_step():
+def test_shard_sum_equals_full_step(path):
     """Data-parallel identity on one GPU: steps on two shards with global counts and global
     index offsets sum (grad and loss) to the full step."""
     c = make_config("c1", 512, 512)
     x, ns = c["x"], c["n_surface"]
     N = len(x)
-    m = _model(c["spec"], N)
+    m = _model(c["spec"], N, path=path)
     gf, lf = m.step(c["params"], x, ns, c["h"], c["loss"], frame_seed=9)
     gf, lf = gf.cpu().numpy(), lf.cpu().numpy()
     # shard r: rows [r*N/2, (r+1)*N/2) -- shard 0 is all surface, shard 1 all uniform
@@ -136,10 +145,10 @@ def test_shard_sum_equals_full_step():
     assert np.linalg.norm(g0 + g1 - gf) <= 1e-5 * np.linalg.norm(gf)
 
 
-def test_plane_mlp_zero_curvature():
+def test_plane_mlp_zero_curvature(path):
     spec, params = plane_mlp([0.48, -0.6, 0.64], 0.1, beta=100.0, hidden_layers=3)
     x = np.random.default_rng(0).uniform(-1, 1, (300, 3)).astype(np.float32)
-    m = _model(spec, 300, eval_only=True)
+    m = _model(spec, 300, eval_only=True, path=path)
     o = m.eval(params, x, 150, 1e-2, frame_seed=1)
     for k in ("hess", "K", "D"):
         assert torch.max(torch.abs(o[k])).item() < 1e-3
@@ -147,10 +156,10 @@ def test_plane_mlp_zero_curvature():
     assert np.max(np.abs(o["g"].cpu().numpy() - n)) < 1e-5
 
 
-def test_errors_and_flags():
+def test_errors_and_flags(path):
     from paper_2511_08980_b200 import FdsdfError
     c = make_config("c1", 16, 16)
-    m = _model(c["spec"], 32)
+    m = _model(c["spec"], 32, path=path)
     with pytest.raises(FdsdfError) as e:
         m.eval(c["params"], c["x"][:0], 0, 1e-2)
     assert e.value.code == "E_EMPTY"
@@ -171,9 +180,9 @@ def test_errors_and_flags():
 
 
 @pytest.mark.parametrize("n", [1, 2, 33])
-def test_tiny_batches(n):
+def test_tiny_batches(n, path):
     c = make_config("c2", max(1, n // 2), n - max(1, n // 2))
-    m = _model(c["spec"], n)
+    m = _model(c["spec"], n, path=path)
     g = gpu_eval(m, c)
     o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
                     frames=(g["frames"][:, :3], g["frames"][:, 3:]))
