@@ -88,6 +88,7 @@ struct fdsdf_ctx {
   // tensor-core (tcgen05 bf16x6) forward
   bool tc = false;
   unsigned char* fimg = nullptr;  // packed forward weight image
+  unsigned char* bimg = nullptr;  // packed backward (W^T) weight image
   float* cinfo = nullptr;    // [max_centers][16]
   float* zev = nullptr;      // eval-only contexts: [max_centers][nh][mpad] centre pre-activations
   void* comm = nullptr;
@@ -215,7 +216,7 @@ void fdsdf_destroy(fdsdf_ctx* c) {
   }
   for (cudaEvent_t e : c->spare) cudaEventDestroy(e);
   void* bufs[] = {c->wt,   c->wb,   c->zf,     c->zscr,   c->seed,  c->lossp, c->del, c->actv,
-                  c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev};
+                  c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev, c->bimg};
   for (void* b : bufs)
     if (b) cudaFree(b);
   cudaSetDevice(prev);
@@ -308,13 +309,15 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     ok = ok && alloc((void**)&c->seed, (size_t)max_centers * NSEED * sizeof(float));
     ok = ok && alloc((void**)&c->del, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
     ok = ok && alloc((void**)&c->actv, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
-    ok = ok && alloc((void**)&c->bacc, (size_t)c->bgrid * c->nacc * sizeof(float));
+    const size_t bslots = c->tc ? (size_t)c->nsm * bwd_tc_acc_slots(mp) : (size_t)c->bgrid;
+    ok = ok && alloc((void**)&c->bacc, std::max<size_t>(bslots, c->bgrid) * c->nacc * sizeof(float));
     ok = ok && alloc((void**)&c->part, (size_t)std::max(0, c->ngemm) * c->nsplit * mp * mp * sizeof(float));
   }
   if (ok && c->tc) {
     ok = ok && alloc((void**)&c->fimg, tc_wimg_bytes(mp, c->ngemm));
     ok = ok && alloc((void**)&c->cinfo, (size_t)max_centers * 16 * sizeof(float));
     if (c->eval_only) ok = ok && alloc((void**)&c->zev, (size_t)max_centers * c->nh * mp * sizeof(float));
+    if (!c->eval_only) ok = ok && alloc((void**)&c->bimg, tc_wimg_bytes(mp, c->ngemm));
   }
   if (ok) ok = cudaMemset(c->dflags, 0, sizeof(unsigned)) == cudaSuccess;
   cudaSetDevice(prev);
@@ -486,10 +489,12 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   fill_net(c, d_params);
   c->launches = 0;
   cudaError_t e = cudaSuccess;
-  if (c->ngemm > 0) e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
-  if (e != cudaSuccess) return done(cuda_fail(c, e, "pack"));
-  if (c->tc && c->ngemm > 0)
-    e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, nullptr, strm); });
+  if (c->tc) {
+    if (c->ngemm > 0)
+      e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, c->bimg, strm); });
+  } else if (c->ngemm > 0) {
+    e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
+  }
   if (e != cudaSuccess) return done(cuda_fail(c, e, "pack_tc"));
 
   FwdArgs a{};
@@ -528,9 +533,19 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   b.actv = c->actv;
   b.bacc = c->bacc;
   b.nacc = c->nacc;
-  b.ntiles = (n + c->btile - 1) / c->btile;
-  const int bgrid = (int)std::min<int64_t>(c->bgrid, b.ntiles);
-  e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwd(b, bgrid, strm); });
+  int bgrid, nbslots;
+  if (c->tc) {
+    b.wimg = c->bimg;
+    b.ntiles = (n + bwd_tc_tile_centres() - 1) / bwd_tc_tile_centres();
+    bgrid = (int)std::min<int64_t>(c->nsm, b.ntiles);
+    nbslots = bgrid * bwd_tc_acc_slots(c->mpad);
+    e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwd_tc(b, bgrid, strm); });
+  } else {
+    b.ntiles = (n + c->btile - 1) / c->btile;
+    bgrid = (int)std::min<int64_t>(c->bgrid, b.ntiles);
+    nbslots = bgrid;
+    e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwd(b, bgrid, strm); });
+  }
   if (e != cudaSuccess) return done(cuda_fail(c, e, "bwd_kernel"));
 
   WgradArgs w{};
@@ -551,7 +566,7 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   f.nsplit = c->nsplit;
   f.bacc = c->bacc;
   f.nacc = c->nacc;
-  f.nbcta = bgrid;
+  f.nbcta = nbslots;
   f.lossp = c->lossp;
   f.nfcta = fgrid;
   f.ls = a.ls;

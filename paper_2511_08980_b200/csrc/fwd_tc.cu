@@ -23,30 +23,19 @@
 // directly (FFMA) -- they are not contractions worth a tensor-core pass.
 #include "act.cuh"
 #include "fdepi.cuh"
-#include "tc.cuh"
+#include "tcmlp.cuh"
 
 namespace fdsdf {
 
 template <int MPAD>
-struct FtcCfg {
-  static constexpr int N = 64;                  // GEMM columns per tile
-  static constexpr int MH = MPAD / 128;         // tcgen05 M-halves (M = 128 each)
-  static constexpr int KC = MPAD / 64;          // K chunks (one 128-byte swizzle row each)
-  static constexpr int STAGE = 3 * 128 * 128;   // W stage (kc, h): 3 pieces x 128 rows x 128 B
-  static constexpr int NST = 2;                 // W ring depth
-  static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
-  static constexpr int NEPI = 8;                // epilogue warps
-  static constexpr int NTHR = (2 + NEPI) * 32;
-  static constexpr int EG = NEPI / (4 * MH);    // epilogue warps per (lane quarter, M-half)
-  static constexpr int MAXC = 16;               // max centres per tile
-  static constexpr int OFF_W = 0;
-  static constexpr int OFF_B = NST * STAGE;
-  static constexpr int OFF_RED = OFF_B + 3 * BPIECE;               // float [NEPI][MAXC][4]
-  static constexpr int OFF_CI = OFF_RED + NEPI * MAXC * 4 * 4;     // float [MAXC][16]
-  static constexpr int OFF_LV = OFF_CI + MAXC * NCINFO * 4;        // double [MAXC][NLOSS]
-  static constexpr int OFF_BAR = OFF_LV + MAXC * NLOSS * 8;        // mbarriers + TMEM slot
-  static constexpr int BYTES = OFF_BAR + 128 + 1024;               // + alignment slack
-  static constexpr uint32_t TCOLS = (MH * N) < 32 ? 32 : (uint32_t)(MH * N);
+struct FtcCfg : TcCfg<MPAD, 64> {
+  using B = TcCfg<MPAD, 64>;
+  static constexpr int MAXC = 16;                                   // max centres per tile
+  static constexpr int OFF_RED = B::OFF_X;                          // float [NEPI][MAXC][4]
+  static constexpr int OFF_CI = OFF_RED + B::NEPI * MAXC * 4 * 4;   // float [MAXC][16]
+  static constexpr int OFF_LV = OFF_CI + MAXC * NCINFO * 4;         // double [MAXC][NLOSS]
+  static constexpr int OFF_BAR = OFF_LV + MAXC * NLOSS * 8;         // mbarriers + TMEM slot
+  static constexpr int BYTES = OFF_BAR + tc_bars_bytes<B>() + 1024; // + alignment slack
 };
 
 bool tc_supported(int mpad, int skip) { return (mpad == 128 || mpad == 256) && skip < 0; }
@@ -70,7 +59,7 @@ __global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < mp * mp; idx += gridDim.x * blockDim.x) {
     const int r = idx / mp, k = idx % mp;  // A-operand row r, K index k
     const int h = r >> 7, rr = r & 127, kc = k >> 6, kk = k & 63;
-    const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * FtcCfg<128>::STAGE + tc::sw128_off(rr, kk, 128);
+    const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * TcCfg<128, 64>::STAGE + tc::sw128_off(rr, kk, 128);
     {
       const float v = (r < M && k < K) ? W[(size_t)r * K + k] : 0.f;  // forward: W[m = r][k]
       const tc::Bf3 s = tc::split3(v);
@@ -99,7 +88,7 @@ template <int ACT, int MPAD, int MODE>
 __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const FwdArgs a) {
   using C = FtcCfg<MPAD>;
   using AF = Act<ACT>;
-  constexpr int N = C::N, MH = C::MH, KC = C::KC, NST = C::NST;
+  constexpr int N = C::N, MH = C::MH;
   constexpr int CPC = MODE == 1 ? 4 : 8;  // columns per centre
   constexpr int CT = N / CPC;             // centres per tile
   constexpr int CPE = CT / C::EG;         // centres per epilogue thread
@@ -112,80 +101,19 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
   float* red = reinterpret_cast<float*>(sm + C::OFF_RED);
   float* cis = reinterpret_cast<float*>(sm + C::OFF_CI);
   double* lvs = reinterpret_cast<double*>(sm + C::OFF_LV);
-  uint64_t* wfull = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
-  uint64_t* wempty = wfull + NST;
-  uint64_t* bfull = wempty + NST;
-  uint64_t* dfull = bfull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + 1);
+  const TcBars bars = tc_bars<C>(sm + C::OFF_BAR);
 
   const Net& net = a.net;
   const int L = net.L;
   const int nh = L - 1;
   const int ngemm = L - 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  if (tid == 0) {
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(&wfull[s], 1);
-      mbar_init(&wempty[s], 1);
-    }
-    mbar_init(bfull, C::NEPI);
-    mbar_init(dfull, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tslot, C::TCOLS);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tbase = *tslot;
+  const uint32_t tbase = tc_setup<C>(bars);
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ W producer
-    if (lane == 0 && ngemm > 0) {
-      uint32_t it = 0;
-      for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
-        for (int g = 0; g < ngemm; ++g)
-          for (int kc = 0; kc < KC; ++kc)
-            for (int h = 0; h < MH; ++h, ++it) {
-              const int s = (int)(it % NST);
-              const uint32_t ph = (it / NST) & 1u;
-              mbar_wait(&wempty[s], ph ^ 1u);
-              mbar_arrive_expect_tx(&wfull[s], C::STAGE);
-              bulk_g2s(Ws + s * C::STAGE, a.wimg + (((size_t)g * KC + kc) * MH + h) * C::STAGE, C::STAGE,
-                       &wfull[s]);
-            }
-    }
+    if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 0, a.ntiles, Ws, bars);
   } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0 && ngemm > 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(128, N);
-      uint32_t it = 0, nb = 0;
-      for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
-        for (int g = 0; g < ngemm; ++g) {
-          mbar_wait(bfull, nb & 1u);
-          ++nb;
-          tc::fence_after();
-          for (int kc = 0; kc < KC; ++kc)
-            for (int h = 0; h < MH; ++h, ++it) {
-              const int s = (int)(it % NST);
-              const uint32_t ph = (it / NST) & 1u;
-              mbar_wait(&wfull[s], ph);
-              tc::fence_after();
-              const uint32_t wa = smem_u32(Ws + s * C::STAGE);
-              const uint32_t ba = smem_u32(Bs + kc * N * 128);
-#pragma unroll
-              for (int sub = 0; sub < 4; ++sub)
-#pragma unroll
-                for (int q = 0; q < 6; ++q) {
-                  const uint64_t ad = tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32);
-                  const uint64_t bd = tc::sdesc_sw128(ba + tc::prod_b(q) * C::BPIECE + sub * 32);
-                  tc::mma_bf16(tbase + h * N, ad, bd, idesc, (kc | sub | q) != 0 ? 1u : 0u);
-                }
-              tc::mma_commit(&wempty[s]);
-            }
-          tc::mma_commit(dfull);
-        }
-    }
+    if (lane == 0 && ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
   } else {
     // ------------------------------------------------------------------ epilogue warps
     const int ew = warp - 2;                 // 0..7
@@ -207,12 +135,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
     auto zp = [&](int64_t c, int l, int col) -> float* {
       return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
     };
-    auto put_b = [&](int n, float v) {
-      const tc::Bf3 s = tc::split3(v);
-      const uint32_t off = tc::sw128_off(n, m, N);
-#pragma unroll
-      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::BPIECE + off) = s.p[p];
-    };
+    auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
 
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       const int64_t c0 = tile * CT;
@@ -223,9 +146,6 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
         }
         bar_named(1, C::NEPI * 32);
       }
-      float part[CPE][4];
-#pragma unroll
-      for (int i = 0; i < CPE; ++i) part[i][0] = part[i][1] = part[i][2] = part[i][3] = 0.f;
 
       for (int l = 0; l <= L - 2; ++l) {
         const bool last = (l == L - 2);
@@ -233,8 +153,28 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
         const float om = net.omega[l];
         const bool mok = m < M;
         const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
+        // last layer: sum over this warp's 32 neurons of w_L[m] * out_j, one slot per centre
+        auto reduce4 = [&](int cl, float p0, float p1, float p2, float p3) {
+          float pv[4] = {wl * p0, wl * p1, wl * p2, wl * p3};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float v = pv[j];
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            if (lane == 0) red[(ew * C::MAXC + cl) * 4 + j] = v;
+          }
+        };
+        // mode 2: the centre pre-activation of this neuron, prefetched one centre ahead
+        auto ldz = [&](int i) -> float {
+          const int64_t c = c0 + eg + C::EG * i;
+          return (MODE == 2 && i < CPE && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
+        };
+        float z0n = ldz(0);
         if (l > 0) {
-          mbar_wait(dfull, nd & 1u);
+          mbar_wait(bars.dfull, nd & 1u);
           ++nd;
           tc::fence_after();
         }
@@ -243,6 +183,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
           const int cl = eg + C::EG * i;  // centre slot in the tile
           const int64_t c = c0 + cl;
           const bool valid = c < a.n;
+          const float z0 = z0n;
+          z0n = ldz(i + 1);
           if (MODE == 1) {
             float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
             if (l == 0) {
@@ -290,10 +232,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
               o3 = s1 * t2;
             }
             if (last) {
-              part[i][0] = fmaf(wl, o0, part[i][0]);
-              part[i][1] = fmaf(wl, o1, part[i][1]);
-              part[i][2] = fmaf(wl, o2, part[i][2]);
-              part[i][3] = fmaf(wl, o3, part[i][3]);
+              reduce4(cl, o0, o1, o2, o3);
             } else {
               put_b(cl * 4 + 0, o0);
               put_b(cl * 4 + 1, o1);
@@ -326,7 +265,6 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
                 }
               }
             }
-            const float z0 = valid ? *zp(c, l, 0) : 0.f;
             if (step && valid) {
 #pragma unroll
               for (int p = 0; p < 4; ++p) {
@@ -343,8 +281,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
               for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &o[2 * p], &o[2 * p + 1]);
             }
             if (last) {
-#pragma unroll
-              for (int p = 0; p < 4; ++p) part[i][p] = fmaf(wl, o[2 * p + 1], part[i][p]);
+              reduce4(cl, o[1], o[3], o[5], o[7]);
             } else {
 #pragma unroll
               for (int j = 0; j < 8; ++j) put_b(cl * 8 + j, o[j]);
@@ -352,28 +289,12 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
           }
         }
         if (!last) {  // B operand of layer l+1 complete (this warp's part): hand to the MMA thread
-          tc::fence_before();
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bfull);
+          tc_epi_arrive(bars);
         } else if (l > 0) {
           tc::fence_before();
         }
       }
 
-      // ---------------------------------------------------------------- last layer: sum over neurons
-#pragma unroll
-      for (int i = 0; i < CPE; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float v = part[i][j];
-          v += __shfl_xor_sync(0xffffffffu, v, 16);
-          v += __shfl_xor_sync(0xffffffffu, v, 8);
-          v += __shfl_xor_sync(0xffffffffu, v, 4);
-          v += __shfl_xor_sync(0xffffffffu, v, 2);
-          v += __shfl_xor_sync(0xffffffffu, v, 1);
-          if (lane == 0) red[(ew * C::MAXC + eg + C::EG * i) * 4 + j] = v;
-        }
       bar_named(1, C::NEPI * 32);
       if (et < CT) {
         const int cl = et;
@@ -414,9 +335,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
     }
   }
 
-  tc::fence_before();
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, C::TCOLS);
+  tc_teardown<C>(tbase);
 }
 
 // ----------------------------------------------------------------------------- host launch

@@ -80,6 +80,7 @@ struct BwdArgs {
   float* bacc;           // [gridDim.x][nacc] per-CTA accumulators
   int64_t nacc;
   int64_t ntiles;
+  const unsigned char* wimg;  // tensor path: packed bf16x3 W^T image (pack_tc_kernel)
 };
 
 struct WgradArgs {
@@ -127,6 +128,9 @@ size_t tc_wimg_bytes(int mpad, int ngemm);          // one packed weight image (
 cudaError_t launch_pack_tc(const Net& net, unsigned char* fwd_img, unsigned char* bwd_img, cudaStream_t st);
 cudaError_t launch_fwd_tc(const FwdArgs& a, int mode, int grid, cudaStream_t st);
 int fwd_tc_tile_centres(int mode);                  // 16 (mode 1) / 8 (mode 2)
+cudaError_t launch_bwd_tc(const BwdArgs& a, int grid, cudaStream_t st);
+int bwd_tc_tile_centres();                          // 8
+int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
 int fwd_tile_centres(int mpad);   // centres per forward tile
 int bwd_tile_centres(int mpad);   // centres per backward tile
 size_t fwd_smem_bytes(int mpad);

@@ -1,0 +1,165 @@
+// tcmlp.cuh -- the warp-specialised layer-sequential MLP engine shared by the tensor-core
+// forward (fwd_tc.cu) and backward (bwd_tc.cu) kernels.
+//
+// One CTA per SM walks tiles of N GEMM columns.  For each tile it runs `ngemm` dependent
+// contractions D[r][n] = sum_k A[r][k] B[k][n] (A = a packed bf16x3 weight image streamed
+// from global memory, B = the tile's activations / adjoints written by the epilogue warps):
+//   warp 0      TMA producer: one thread bulk-copies 48 KB weight stages (K chunk of 64 x
+//               128 rows x 3 pieces) into an NST-deep ring (cp.async.bulk + mbarrier tx);
+//   warp 1      TMEM owner + MMA issuer: one thread waits for the B operand of a layer,
+//               issues 4 K-steps x 6 piece products tcgen05.mma per stage into the TMEM
+//               accumulator of its M-half, commits the stage back to the producer and, after
+//               the last stage, commits "D full" to the epilogue;
+//   warps 2..9  epilogue (kernel specific): read D rows with tcgen05.ld, write the next B.
+// Hand-offs: wfull/wempty (producer <-> MMA), bfull (8 epilogue warps -> MMA: B written and
+// the previous D fully read), dfull (MMA -> epilogue).
+#pragma once
+#include "tc.cuh"
+
+namespace fdsdf {
+
+template <int MPAD_, int N_>
+struct TcCfg {
+  static constexpr int MPAD = MPAD_;
+  static constexpr int N = N_;                  // GEMM columns per tile
+  static constexpr int MH = MPAD / 128;         // tcgen05 M-halves (M = 128 each)
+  static constexpr int KC = MPAD / 64;          // K chunks (one 128-byte swizzle row each)
+  static constexpr int STAGE = 3 * 128 * 128;   // weight stage (kc, h): 3 pieces x 128 rows x 128 B
+  static constexpr int NST = 2;                 // weight ring depth
+  static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
+  static constexpr int NEPI = 8;                // epilogue warps
+  static constexpr int NTHR = (2 + NEPI) * 32;
+  static constexpr int EG = NEPI / (4 * MH);    // epilogue warps per (lane quarter, M-half)
+  static constexpr int OFF_W = 0;
+  static constexpr int OFF_B = NST * STAGE;
+  static constexpr int OFF_X = OFF_B + 3 * BPIECE;  // kernel-specific scratch starts here
+  static constexpr uint32_t TCOLS = (MH * N) <= 32 ? 32 : (MH * N) <= 64 ? 64 : (MH * N) <= 128 ? 128
+                                    : (MH * N) <= 256 ? 256 : 512;
+  static_assert(N % 16 == 0 && N >= 16 && N <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
+  static_assert(MH * N <= 512, "TMEM has 512 columns");
+};
+
+struct TcBars {
+  uint64_t* wfull;
+  uint64_t* wempty;
+  uint64_t* bfull;
+  uint64_t* dfull;
+  uint32_t* tslot;
+};
+
+// barrier block: 2*NST + 2 mbarriers + the TMEM slot, at `p` (8-byte aligned)
+template <class C>
+__device__ __forceinline__ TcBars tc_bars(unsigned char* p) {
+  TcBars b;
+  b.wfull = reinterpret_cast<uint64_t*>(p);
+  b.wempty = b.wfull + C::NST;
+  b.bfull = b.wempty + C::NST;
+  b.dfull = b.bfull + 1;
+  b.tslot = reinterpret_cast<uint32_t*>(b.dfull + 1);
+  return b;
+}
+template <class C>
+constexpr int tc_bars_bytes() {
+  return (2 * C::NST + 2) * 8 + 16;
+}
+
+// CTA prologue: barrier init (thread 0), TMEM allocation (warp 1); returns the TMEM base.
+template <class C>
+__device__ __forceinline__ uint32_t tc_setup(const TcBars& b) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(&b.wfull[s], 1);
+      mbar_init(&b.wempty[s], 1);
+    }
+    mbar_init(b.bfull, C::NEPI);
+    mbar_init(b.dfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(b.tslot, C::TCOLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  return *b.tslot;
+}
+
+template <class C>
+__device__ __forceinline__ void tc_teardown(uint32_t tbase) {
+  tc::fence_before();
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 1) tc::tmem_dealloc(tbase, C::TCOLS);
+}
+
+// Producer (one thread): stages of GEMM g, chunk kc, half h for every tile this CTA owns.
+// reverse = 1 streams the layers top-down (backward).
+template <class C>
+__device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm, int reverse, int64_t ntiles,
+                                            unsigned char* Ws, const TcBars& b) {
+  uint32_t it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+    for (int gi = 0; gi < ngemm; ++gi) {
+      const int g = reverse ? ngemm - 1 - gi : gi;
+      for (int kc = 0; kc < C::KC; ++kc)
+        for (int h = 0; h < C::MH; ++h, ++it) {
+          const int s = (int)(it % C::NST);
+          const uint32_t ph = (it / C::NST) & 1u;
+          mbar_wait(&b.wempty[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&b.wfull[s], C::STAGE);
+          bulk_g2s(Ws + s * C::STAGE, img + (((size_t)g * C::KC + kc) * C::MH + h) * C::STAGE, C::STAGE,
+                   &b.wfull[s]);
+        }
+    }
+}
+
+// MMA issuer (one thread): D[h] (TMEM columns h*N ..) = A_stage . B for every GEMM of every tile.
+template <class C>
+__device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned char* Ws,
+                                       const unsigned char* Bs, uint32_t tbase, const TcBars& b) {
+  constexpr uint32_t idesc = tc::idesc_bf16(128, C::N);
+  uint32_t it = 0, nb = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+    for (int g = 0; g < ngemm; ++g) {
+      mbar_wait(b.bfull, nb & 1u);
+      ++nb;
+      tc::fence_after();
+      for (int kc = 0; kc < C::KC; ++kc)
+        for (int h = 0; h < C::MH; ++h, ++it) {
+          const int s = (int)(it % C::NST);
+          const uint32_t ph = (it / C::NST) & 1u;
+          mbar_wait(&b.wfull[s], ph);
+          tc::fence_after();
+          const uint32_t wa = smem_u32(Ws + s * C::STAGE);
+          const uint32_t ba = smem_u32(Bs + kc * C::N * 128);
+#pragma unroll
+          for (int sub = 0; sub < 4; ++sub)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              const uint64_t ad = tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32);
+              const uint64_t bd = tc::sdesc_sw128(ba + tc::prod_b(q) * C::BPIECE + sub * 32);
+              tc::mma_bf16(tbase + h * C::N, ad, bd, idesc, (kc | sub | q) != 0 ? 1u : 0u);
+            }
+          tc::mma_commit(&b.wempty[s]);
+        }
+      tc::mma_commit(b.dfull);
+    }
+}
+
+// epilogue warp: the B operand of the next GEMM is complete (this warp's rows), and its
+// reads of the previous D are finished -> hand over to the MMA thread
+__device__ __forceinline__ void tc_epi_arrive(const TcBars& b) {
+  tc::fence_before();
+  fence_proxy_async();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(b.bfull);
+}
+
+// write v (split into 3 bf16 pieces) at B operand element (column n, K index k)
+template <class C>
+__device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float v) {
+  const tc::Bf3 s = tc::split3(v);
+  const uint32_t off = tc::sw128_off(n, k, C::N);
+#pragma unroll
+  for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::BPIECE + off) = s.p[p];
+}
+
+}  // namespace fdsdf
