@@ -234,10 +234,12 @@ const char* fdsdf_version(void);
  * (1: plain bf16, 3: the three leading products, 6: the fp32-accurate bf16x6 scheme).
  * d_W [M][K], d_B [N][K], d_D [M][N]: fp32 row-major device buffers owned by the caller.
  * One CTA; M in {128, 256}, N a multiple of 16 in [16, 256], K a multiple of 64.
+ * mn_major = 0 stages both operands K-major (the forward / backward kernels' layout);
+ * 1 stages them MN-major (the weight-gradient kernel's layout; N a multiple of 64).
  * Errors: NULL pointers, shapes or nprod out of range -> FDSDF_E_INVALID (nothing enqueued);
  * launch failure -> FDSDF_E_CUDA.  Test/diagnostic use only (not on the hot path). */
 fdsdf_status fdsdf_selftest_mma(const float* d_W, const float* d_B, float* d_D, int M, int N, int K,
-                                int nprod, void* stream);
+                                int nprod, int mn_major, void* stream);
 
 #ifdef __cplusplus
 }

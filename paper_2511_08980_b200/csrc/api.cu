@@ -311,7 +311,8 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     ok = ok && alloc((void**)&c->actv, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
     const size_t bslots = c->tc ? (size_t)c->nsm * bwd_tc_acc_slots(mp) : (size_t)c->bgrid;
     ok = ok && alloc((void**)&c->bacc, std::max<size_t>(bslots, c->bgrid) * c->nacc * sizeof(float));
-    ok = ok && alloc((void**)&c->part, (size_t)std::max(0, c->ngemm) * c->nsplit * mp * mp * sizeof(float));
+    const int nsplit_max = c->tc ? std::max(c->nsplit, c->nsm) : c->nsplit;
+    ok = ok && alloc((void**)&c->part, (size_t)std::max(0, c->ngemm) * nsplit_max * mp * mp * sizeof(float));
   }
   if (ok && c->tc) {
     ok = ok && alloc((void**)&c->fimg, tc_wimg_bytes(mp, c->ngemm));
@@ -555,15 +556,18 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   w.rows = n * NCOLB;
   w.stride_layer = n * NCOLB * c->mpad;
   w.mpad = c->mpad;
-  w.nsplit = c->nsplit;
+  w.nsplit = c->tc ? wgrad_tc_splits(c->nsm, w.rows) : c->nsplit;
   w.first_layer = 1;
-  if (c->ngemm > 0) e = run_slot(c, FDSDF_KSLOT_WGRAD, strm, [&] { return launch_wgrad(w, c->ngemm, strm); });
+  if (c->ngemm > 0)
+    e = run_slot(c, FDSDF_KSLOT_WGRAD, strm, [&] {
+      return c->tc ? launch_wgrad_tc(w, c->ngemm, strm) : launch_wgrad(w, c->ngemm, strm);
+    });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "wgrad_kernel"));
 
   FinArgs f{};
   f.net = c->net;
   f.part = c->part;
-  f.nsplit = c->nsplit;
+  f.nsplit = w.nsplit;
   f.bacc = c->bacc;
   f.nacc = c->nacc;
   f.nbcta = nbslots;

@@ -1,5 +1,6 @@
 // kernels.cuh -- kernel argument blocks and launch entry points shared by the C-ABI layer.
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -131,6 +132,8 @@ int fwd_tc_tile_centres(int mode);                  // 16 (mode 1) / 8 (mode 2)
 cudaError_t launch_bwd_tc(const BwdArgs& a, int grid, cudaStream_t st);
 int bwd_tc_tile_centres();                          // 8
 int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
+cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, cudaStream_t st);
+int wgrad_tc_splits(int nsm, int64_t rows);         // split-K factor of the tensor wgrad
 int fwd_tile_centres(int mpad);   // centres per forward tile
 int bwd_tile_centres(int mpad);   // centres per backward tile
 size_t fwd_smem_bytes(int mpad);

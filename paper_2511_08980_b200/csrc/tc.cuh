@@ -58,10 +58,30 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
+// MN-major SWIZZLE_128B bf16 tile, `mn` = extent along M/N (multiple of 64): swizzle atoms of
+// 64 MN-elements (one 128-byte row) x 8 K-rows, atoms ordered MN-fastest; byte offset of
+// element (r = MN index, k = K index)
+__host__ __device__ __forceinline__ uint32_t sw128mn_off(int r, int k, int mn) {
+  const int ma = r >> 6, ka = k >> 3, k8 = k & 7, r64 = r & 63;
+  return (uint32_t)((ka * (mn >> 6) + ma) * 1024 + k8 * 128 + ((((r64 >> 3) ^ k8)) << 4) + ((r64 & 7) << 1));
+}
+
+// MN-major SWIZZLE_128B descriptor: lbo = byte stride between atoms along MN, sbo = along K
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // instruction descriptor, kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
 // both K-major (bits 15, 16 = 0), N>>3 [17,23), M>>4 [24,29)
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn = 0, int b_mn = 0) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // ----------------------------------------------------------------------------- tcgen05 PTX

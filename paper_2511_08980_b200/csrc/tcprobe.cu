@@ -14,7 +14,8 @@
 namespace fdsdf {
 
 __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict__ W, const float* __restrict__ B,
-                                                         float* __restrict__ D, int M, int N, int K, int nprod) {
+                                                         float* __restrict__ D, int M, int N, int K, int nprod,
+                                                         int mn) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // carve: A pieces [3][M x 128 B], B pieces [3][N x 128 B], mbarrier, tmem slot
   unsigned char* base = smem_raw;
@@ -40,7 +41,9 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t idesc = tc::idesc_bf16(128, N);
+  const uint32_t idesc = mn ? tc::idesc_bf16(128, N, 1, 1) : tc::idesc_bf16(128, N);
+  // MN-major strides: atoms along MN are 1024 B apart, along K (M/64)*1024 resp. (N/64)*1024
+  const uint32_t a_mn = 1024, a_k = (uint32_t)(M / 64) * 1024, b_mn = 1024, b_k = (uint32_t)(N / 64) * 1024;
   const int q0 = nprod == 1 ? 5 : (nprod == 3 ? 3 : 0);
 
   for (int kc = 0; kc < K / 64; ++kc) {
@@ -48,14 +51,14 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
     for (int i = tid; i < M * 64; i += 256) {
       const int r = i >> 6, k = i & 63;
       const tc::Bf3 s = tc::split3(W[(size_t)r * K + kc * 64 + k]);
-      const uint32_t o = tc::sw128_off(r, k, M);
+      const uint32_t o = mn ? tc::sw128mn_off(r, k, M) : tc::sw128_off(r, k, M);
 #pragma unroll
       for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(As + p * M * 128 + o) = s.p[p];
     }
     for (int i = tid; i < N * 64; i += 256) {
       const int r = i >> 6, k = i & 63;
       const tc::Bf3 s = tc::split3(B[(size_t)r * K + kc * 64 + k]);
-      const uint32_t o = tc::sw128_off(r, k, N);
+      const uint32_t o = mn ? tc::sw128mn_off(r, k, N) : tc::sw128_off(r, k, N);
 #pragma unroll
       for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * N * 128 + o) = s.p[p];
     }
@@ -66,10 +69,18 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
       for (int s = 0; s < 4; ++s)
         for (int h = 0; h < MH; ++h)
           for (int q = q0; q < 6; ++q) {
-            const uint32_t aa = smem_u32(As + tc::prod_a(q) * M * 128 + h * 128 * 128 + s * 32);
-            const uint32_t bb = smem_u32(Bs + tc::prod_b(q) * N * 128 + s * 32);
-            tc::mma_bf16(tbase + h * N, tc::sdesc_sw128(aa), tc::sdesc_sw128(bb), idesc,
-                         (kc | s | (q - q0)) != 0 ? 1u : 0u);
+            uint64_t ad, bd;
+            if (!mn) {
+              ad = tc::sdesc_sw128(smem_u32(As + tc::prod_a(q) * M * 128 + h * 128 * 128 + s * 32));
+              bd = tc::sdesc_sw128(smem_u32(Bs + tc::prod_b(q) * N * 128 + s * 32));
+            } else {
+              // K step s = 16 K = 2 atoms along K; M-half h = 2 atoms along M
+              const uint32_t aa = smem_u32(As + tc::prod_a(q) * M * 128 + 2 * s * a_k + 2 * h * a_mn);
+              const uint32_t bb = smem_u32(Bs + tc::prod_b(q) * N * 128 + 2 * s * b_k);
+              ad = tc::sdesc_sw128_mn(aa, a_mn, a_k);
+              bd = tc::sdesc_sw128_mn(bb, b_mn, b_k);
+            }
+            tc::mma_bf16(tbase + h * N, ad, bd, idesc, (kc | s | (q - q0)) != 0 ? 1u : 0u);
           }
       tc::mma_commit(bar);
     }
@@ -94,14 +105,15 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
 }  // namespace fdsdf
 
 extern "C" fdsdf_status fdsdf_selftest_mma(const float* d_W, const float* d_B, float* d_D, int M, int N, int K,
-                                           int nprod, void* stream) {
+                                           int nprod, int mn_major, void* stream) {
   using namespace fdsdf;
   if (!d_W || !d_B || !d_D) return FDSDF_E_INVALID;
   if (M < 128 || M > 256 || M % 128 || N < 16 || N > 256 || N % 16 || K < 64 || K % 64) return FDSDF_E_INVALID;
   if (nprod != 1 && nprod != 3 && nprod != 6) return FDSDF_E_INVALID;
+  if (mn_major < 0 || mn_major > 1 || (mn_major && (N % 64))) return FDSDF_E_INVALID;
   const size_t smem = 3 * (size_t)(M + N) * 128 + 64 + 1024;
   cudaError_t e = cudaFuncSetAttribute(tcprobe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return FDSDF_E_CUDA;
-  tcprobe_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(d_W, d_B, d_D, M, N, K, nprod);
+  tcprobe_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(d_W, d_B, d_D, M, N, K, nprod, mn_major);
   return cudaGetLastError() == cudaSuccess ? FDSDF_OK : FDSDF_E_CUDA;
 }

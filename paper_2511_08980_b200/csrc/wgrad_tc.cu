@@ -1,0 +1,196 @@
+// wgrad_tc.cu -- the weight-gradient contraction on the tensor cores (
+// bf16x6, tc.cuh / DESIGN.md §4b):
+//
+//   dW_l[m][k] = sum_j delta_l[j][m] * a_{l-1}[j][k]     j over (centre, column): 10 per centre
+//
+// Split-K: CTA (s, l) owns a contiguous j-range of GEMM layer l and computes the full
+// MPAD x MPAD block into TMEM (M = MPAD rows in 128-row halves, N = MPAD), then writes its partial
+// (never atomically added); finalize_kernel sums the partials in split order, so the result
+// is bitwise reproducible.
+//   warp 0      TMEM owner + MMA issuer (one thread): per 32-wide j chunk, 2 K-steps x
+//               M-halves x 6 piece products, tcgen05.mma kind::f16 with BOTH operands
+//               MN-major (delta and a are stored j-major, m / k contiguous);
+//   warps 1..8  stagers: read the fp32 chunk of delta_l and a_{l-1} (float4, coalesced), split
+//               every value into 3 bf16 pieces and store them in the MN-major SWIZZLE_128B
+//               layout of a 2-deep ring (8-byte st.shared per piece); after the last chunk of
+//               a layer they read the accumulator back (tcgen05.ld) and write the partial.
+#include "kernels.cuh"
+#include "tc.cuh"
+
+namespace fdsdf {
+
+template <int MPAD>
+struct WtcCfg {
+  static constexpr int JC = 32;                     // j per stage (4 swizzle atoms along K)
+  static constexpr int MH = MPAD / 128;
+  static constexpr int PIECE = MPAD * JC * 2;       // one bf16 piece of one operand chunk
+  static constexpr int OPER = 3 * PIECE;            // one operand chunk (3 pieces)
+  static constexpr int STAGE = 2 * OPER;            // delta chunk + a chunk
+  static constexpr int NST = 2;
+  static constexpr int KSTRIDE = (MPAD / 64) * 1024;  // byte stride between swizzle atoms along K
+  static constexpr int NSTG = 8;                    // stager warps
+  static constexpr int NTHR = (1 + NSTG) * 32;
+  static constexpr int OFF_BAR = NST * STAGE;
+  static constexpr int BYTES = OFF_BAR + 64 + 1024;
+  static constexpr uint32_t TCOLS = MH * MPAD <= 128 ? 128 : (MH * MPAD <= 256 ? 256 : 512);
+};
+
+int wgrad_tc_splits(int nsm, int64_t rows) {
+  const int64_t chunks = (rows + 31) / 32;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(nsm, chunks));
+}
+
+template <int MPAD>
+__global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const WgradArgs a) {
+  using C = WtcCfg<MPAD>;
+  constexpr int JC = C::JC, MH = C::MH, NST = C::NST;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = smem_raw;
+  sm += (1024 - (smem_u32(sm) & 1023)) & 1023;
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* sempty = sfull + NST;
+  uint64_t* dfull = sempty + NST;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&sfull[s], C::NSTG);
+      mbar_init(&sempty[s], 1);
+    }
+    mbar_init(dfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, C::TCOLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *tslot;
+
+  const int split = blockIdx.x;
+  const int64_t per = ((a.rows + a.nsplit - 1) / a.nsplit + JC - 1) / JC * JC;
+  const int64_t j0 = (int64_t)split * per;
+  const int64_t j1 = min(a.rows, j0 + per);
+  const int nchunk = j1 > j0 ? (int)((j1 - j0 + JC - 1) / JC) : 0;
+  const int li = blockIdx.y;  // GEMM layer first_layer + li
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(128, MPAD, 1, 1);
+      uint32_t it = 0;
+      {
+        for (int ch = 0; ch < nchunk; ++ch, ++it) {
+          const int s = (int)(it % NST);
+          mbar_wait(&sfull[s], (it / NST) & 1u);
+          tc::fence_after();
+          const uint32_t da = smem_u32(sm + s * C::STAGE);
+          const uint32_t aa = da + C::OPER;
+#pragma unroll
+          for (int ks = 0; ks < JC / 16; ++ks)
+#pragma unroll
+            for (int h = 0; h < MH; ++h)
+#pragma unroll
+              for (int q = 0; q < 6; ++q) {
+                const uint64_t ad = tc::sdesc_sw128_mn(da + tc::prod_a(q) * C::PIECE + ks * 2 * C::KSTRIDE +
+                                                           h * 2 * 1024,
+                                                       1024, C::KSTRIDE);
+                const uint64_t bd =
+                    tc::sdesc_sw128_mn(aa + tc::prod_b(q) * C::PIECE + ks * 2 * C::KSTRIDE, 1024, C::KSTRIDE);
+                tc::mma_bf16(tbase + h * MPAD, ad, bd, idesc, (ch | ks | q) != 0 ? 1u : 0u);
+              }
+          tc::mma_commit(&sempty[s]);
+        }
+        tc::mma_commit(dfull);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ stagers + readback
+    const int sw = warp - 1;        // 0..7
+    const int st = tid - 32;        // 0..255
+    uint32_t it = 0;
+    constexpr int QUADS = MPAD / 4;  // float4 per j row
+    {
+      const int layer = a.first_layer + li;
+      const float* D = a.del + (size_t)layer * a.stride_layer;
+      const float* A = a.actv + (size_t)(layer - 1) * a.stride_layer;
+      for (int ch = 0; ch < nchunk; ++ch, ++it) {
+        const int s = (int)(it % NST);
+        mbar_wait(&sempty[s], ((it / NST) & 1u) ^ 1u);
+        unsigned char* dst = sm + s * C::STAGE;
+        const int64_t jb = j0 + (int64_t)ch * JC;
+#pragma unroll 2
+        for (int item = st; item < JC * QUADS; item += C::NSTG * 32) {
+          const int jj = item / QUADS, r = (item % QUADS) * 4;
+          const int64_t j = jb + jj;
+          float4 dv = make_float4(0.f, 0.f, 0.f, 0.f), av = dv;
+          if (j < j1) {
+            dv = __ldg(reinterpret_cast<const float4*>(D + j * MPAD + r));
+            av = __ldg(reinterpret_cast<const float4*>(A + j * MPAD + r));
+          }
+          const uint32_t off = tc::sw128mn_off(r, jj, MPAD);
+          const tc::Bf3 d0 = tc::split3(dv.x), d1 = tc::split3(dv.y), d2 = tc::split3(dv.z), d3 = tc::split3(dv.w);
+          const tc::Bf3 a0 = tc::split3(av.x), a1 = tc::split3(av.y), a2 = tc::split3(av.z), a3 = tc::split3(av.w);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            uint2 wd, wa;
+            wd.x = (uint32_t)__bfloat16_as_ushort(d0.p[p]) | ((uint32_t)__bfloat16_as_ushort(d1.p[p]) << 16);
+            wd.y = (uint32_t)__bfloat16_as_ushort(d2.p[p]) | ((uint32_t)__bfloat16_as_ushort(d3.p[p]) << 16);
+            wa.x = (uint32_t)__bfloat16_as_ushort(a0.p[p]) | ((uint32_t)__bfloat16_as_ushort(a1.p[p]) << 16);
+            wa.y = (uint32_t)__bfloat16_as_ushort(a2.p[p]) | ((uint32_t)__bfloat16_as_ushort(a3.p[p]) << 16);
+            *reinterpret_cast<uint2*>(dst + p * C::PIECE + off) = wd;
+            *reinterpret_cast<uint2*>(dst + C::OPER + p * C::PIECE + off) = wa;
+          }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfull[s]);
+      }
+      // readback of this layer's partial: warp sw -> lane quarter sw % 4, halves (sw / 4) + 2i
+      mbar_wait(dfull, 0u);
+      tc::fence_after();
+      float* out = a.part + ((size_t)li * a.nsplit + split) * MPAD * MPAD;
+      for (int h = sw >> 2; h < MH; h += 2) {
+        const int q4 = (warp & 3);
+        const int m = h * 128 + 32 * q4 + lane;
+        const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + h * MPAD;
+        float* row = out + (size_t)m * MPAD;
+#pragma unroll 1
+        for (int k0 = 0; k0 < MPAD; k0 += 16) {
+          float v[16];
+          tc::tmem_ld16(taddr + k0, v);
+          if (nchunk == 0) {  // empty j-range: the accumulator was never written
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < 16; q += 4)
+            *reinterpret_cast<float4*>(row + k0 + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+        }
+      }
+      tc::fence_before();
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, C::TCOLS);
+}
+
+template <int MPAD>
+static cudaError_t launch_wgrad_tc_t(const WgradArgs& a, int nglayers, cudaStream_t st) {
+  using C = WtcCfg<MPAD>;
+  cudaError_t e = cudaFuncSetAttribute(wgrad_tc_kernel<MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  if (e != cudaSuccess) return e;
+  wgrad_tc_kernel<MPAD><<<dim3(a.nsplit, nglayers), C::NTHR, C::BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, cudaStream_t st) {
+  if (nglayers <= 0) return cudaSuccess;
+  if (a.mpad == 256) return launch_wgrad_tc_t<256>(a, nglayers, st);
+  if (a.mpad == 128) return launch_wgrad_tc_t<128>(a, nglayers, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fdsdf

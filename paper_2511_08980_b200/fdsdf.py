@@ -105,7 +105,7 @@ def lib():
         L.fdsdf_set_kernel_timing.restype = C.c_int
         L.fdsdf_kernel_times.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(i64), C.c_int, C.c_int]
         L.fdsdf_kernel_times.restype = C.c_int
-        L.fdsdf_selftest_mma.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+        L.fdsdf_selftest_mma.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp]
         L.fdsdf_selftest_mma.restype = C.c_int
         L.fdsdf_version.argtypes = []
         L.fdsdf_version.restype = C.c_char_p
@@ -337,14 +337,14 @@ class FDSDF:
         return fdsdf_kernel_times(self.ctx, reset)
 
 
-def fdsdf_selftest_mma(W, B, nprod=6, stream=None):
+def fdsdf_selftest_mma(W, B, nprod=6, mn_major=0, stream=None):
     """D = W @ B.T on the tcgen05 bf16-piece core (W [M,K], B [N,K] fp32 CUDA tensors)."""
     import torch
     M, K = W.shape
     N = B.shape[0]
     D = torch.empty(M, N, device=W.device, dtype=torch.float32)
     _check(lib().fdsdf_selftest_mma(_ptr(W.contiguous()), _ptr(B.contiguous()), _ptr(D), M, N, K, int(nprod),
-                                    _stream(stream)))
+                                    int(mn_major), _stream(stream)))
     return D
 
 

@@ -19,7 +19,7 @@ def _built():
     build()
 
 
-def _run(M, N, K, nprod, seed=0, structured=False):
+def _run(M, N, K, nprod, seed=0, structured=False, mn=0):
     from paper_2511_08980_b200.fdsdf import fdsdf_selftest_mma
     rng = np.random.default_rng(seed)
     if structured:
@@ -30,7 +30,7 @@ def _run(M, N, K, nprod, seed=0, structured=False):
     else:
         W = rng.standard_normal((M, K)).astype(np.float32)
         B = (rng.standard_normal((N, K)) * np.exp(rng.uniform(-8, 0, (N, 1)))).astype(np.float32)
-    D = fdsdf_selftest_mma(torch.from_numpy(W).cuda(), torch.from_numpy(B).cuda(), nprod)
+    D = fdsdf_selftest_mma(torch.from_numpy(W).cuda(), torch.from_numpy(B).cuda(), nprod, mn)
     torch.cuda.synchronize()
     ref = W.astype(np.float64) @ B.astype(np.float64).T
     scale = np.abs(W.astype(np.float64)) @ np.abs(B.astype(np.float64)).T
@@ -62,3 +62,15 @@ def test_mma_bf16x6_is_fp32_accurate(M, N, K):
     err1 = np.max(np.abs(D1 - ref) / (scale * 2.0 ** -24))
     print("bf16x1 err:", err1)
     assert err1 > 100.0
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (128, 64, 64), (256, 128, 256), (128, 192, 128)])
+def test_mma_mn_major(M, N, K):
+    """MN-major operands (LBO = stride between swizzle atoms along M/N, SBO = along K), the
+    layout of the weight-gradient kernel."""
+    D, ref, scale = _run(M, N, K, 6, seed=7, mn=1)
+    err = np.max(np.abs(D - ref) / (scale * 2.0 ** -24))
+    print("mn-major", M, N, K, "err ulps", err)
+    assert err <= 24.0
+    Ds, refs, _ = _run(M, N, K, 6, structured=True, mn=1)
+    assert np.max(np.abs(Ds - refs)) < 1e-3
