@@ -52,6 +52,17 @@ def parse():
     return ap.parse_args()
 
 
+def measured_bf16_peak():
+    """Dense bf16 TFLOP/s: MEASURED_PEAKS.json (driver-written, burst figure), else the
+    B200_PROFILING.md fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = float(json.load(open(p))["bf16_tflops"])
+        return v, "measured (MEASURED_PEAKS.json, burst)"
+    except (OSError, ValueError, KeyError):
+        return 1590.0, "fallback (B200_PROFILING.md)"
+
+
 def p_mm(spec):
     from harness import layer_shapes
     sh = layer_shapes(spec)
@@ -314,16 +325,26 @@ def main():
 
     # ------------------------------------------------------------------ roofline of the dominant kernel
     P_mm, P_gemm = p_mm(spec)
-    alg = {  # algorithmic flops per launch: column-units x 2 P_mm x centres
-        "fwd": 20.0 * P_mm * n,      # 9 stencil values + 1 reverse sweep for grad f
-        "bwd": 20.0 * P_mm * n,      # delta through 9 evaluations + the grad-f path
-        "wgrad": 20.0 * P_gemm * n,  # dW of the GEMM layers: 10 column-units
-    }
+    path = model.path
+    # algorithmic flops per launch: column-units x 2 P_mm x centres
+    if path == "tensor":
+        alg = {
+            "fwd": 16.0 * P_mm * n,        # the 8 stencil-neighbour evaluations (pair kernel)
+            "fwd_centre": 4.0 * P_mm * n,  # f(x0) + the grad-f sweep (centre kernel)
+            "bwd": 20.0 * P_mm * n,        # delta through 9 evaluations + the grad-f path
+            "wgrad": 20.0 * P_gemm * n,    # dW of the GEMM layers: 10 column-units
+        }
+    else:
+        alg = {
+            "fwd": 20.0 * P_mm * n,      # 9 stencil values + 1 reverse sweep for grad f
+            "bwd": 20.0 * P_mm * n,      # delta through 9 evaluations + the grad-f path
+            "wgrad": 20.0 * P_gemm * n,  # dW of the GEMM layers: 10 column-units
+        }
     kms = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in ktimes.items()}
-    dom = max(("fwd", "bwd", "wgrad"), key=lambda k: kms[k])
+    dom = max(alg, key=lambda k: kms[k])
     sm_max = clocks.get("sm_max_mhz") or 1965.0
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = nsm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    ffma_peak = nsm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
     achieved = alg[dom] / (kms[dom] * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
@@ -332,10 +353,22 @@ def main():
             traffic = json.load(open(prof)).get(dom)
         except (OSError, ValueError):
             traffic = None
-    roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "peak_note": f"fp32 FFMA: {nsm} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz (clocks.max.sm)",
-            "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_max)) if clocks.get("sm_mhz") else None}
+    if path == "tensor":
+        # fp32-accurate contraction as 6 bf16 tensor-core products (bf16x6):
+        # its ceiling is the measured dense bf16 peak / 6
+        bf16, src = measured_bf16_peak()
+        peak = bf16 / 6.0
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_note": f"bf16x6: {src} dense bf16 {bf16:.1f} TFLOP/s / 6 bf16 MMAs per fp32-accurate MAC",
+                "frac_of_fp32_ffma_peak": achieved / ffma_peak,
+                "frac_at_run_clock": None}
+    else:
+        peak = ffma_peak
+        roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_note": f"fp32 FFMA: {nsm} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz (clocks.max.sm)",
+                "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_max)) if clocks.get("sm_mhz") else None}
     step_alg = sum(alg.values())
     kernel_ms = {k: round(v, 4) for k, v in kms.items() if ktimes[k][1]}
 
@@ -353,7 +386,9 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded CSG + uniform box; DESIGN.md §3)", "config": cfg["config_json"],
             "roofline": roof, "step_alg_tflops": step_alg / (ms_per_step * 1e-3) / 1e12,
-            "kernel_ms": kernel_ms, "cpu_baseline": cpu, "e2e": e2e,
+            "kernel_ms": kernel_ms, "path": path,
+            "precision": ("bf16x6: fp32 operands split exactly into 3 bf16 pieces, 6 tcgen05 products, fp32 "
+                          "accumulation" if path == "tensor" else "fp32 FFMA"), "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps), "clocks": clocks,
             "wall_s_timed_region": wall,
         }

@@ -146,10 +146,12 @@ typedef struct fdsdf_ctx fdsdf_ctx;
 enum {
   FDSDF_CREATE_EVAL_ONLY = 1u,  /* no step workspace                                          */
   FDSDF_CREATE_FFMA = 2u,       /* run every contraction as fp32 FFMA (the validation path)   */
-  FDSDF_CREATE_TENSOR = 4u      /* run the forward contractions on tcgen05 tensor cores with   */
-                                /* the fp32-accurate bf16x6 piece scheme;     */
-                                /* needs hidden widths <= 256 and no skip layer, else         */
-                                /* FDSDF_E_UNSUPPORTED.  Both flags -> FDSDF_E_INVALID.       */
+  FDSDF_CREATE_TENSOR = 4u      /* require the tcgen05 tensor-core path: every MLP contraction */
+                                /* (forward, backward, weight gradient) with the fp32-accurate */
+                                /* bf16x6 piece scheme; needs hidden widths   */
+                                /* <= 256 and no skip layer, else FDSDF_E_UNSUPPORTED.        */
+                                /* Neither flag: the tensor path where supported, else FFMA.  */
+                                /* Both flags -> FDSDF_E_INVALID.                             */
 };
 fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_centers,
                           uint32_t flags, fdsdf_ctx** out);

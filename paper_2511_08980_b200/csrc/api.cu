@@ -249,14 +249,19 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     delete c;
     return FDSDF_E_INVALID;
   }
-  if (flags & FDSDF_CREATE_TENSOR) {
+  {
+    // default path: the tensor cores wherever the spec allows it (hidden widths <= 256, no
+    // skip layer); FDSDF_CREATE_FFMA forces the fp32 FFMA kernels
     const int mp_tc = std::max(c->mpad, 128);  // widths <= 64 are zero-padded to one M=128 tile
-    if (!tc_supported(mp_tc, spec->skip_at)) {
+    const bool ok_tc = tc_supported(mp_tc, spec->skip_at);
+    if ((flags & FDSDF_CREATE_TENSOR) && !ok_tc) {
       delete c;
       return FDSDF_E_UNSUPPORTED;
     }
-    c->tc = true;
-    c->mpad = mp_tc;
+    if (ok_tc && !(flags & FDSDF_CREATE_FFMA)) {
+      c->tc = true;
+      c->mpad = mp_tc;
+    }
   }
   c->P = fdsdf_spec_num_params(spec);
   for (int l = 0; l < c->L; ++l) {
