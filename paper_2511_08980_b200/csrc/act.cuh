@@ -50,8 +50,8 @@ struct Act<ACT_SINE> {
   __device__ __forceinline__ static P2 pre(const C& c, float A, float S) {
     P2 p;
     float sh, ch, ss, cs;
-    sincos_acc(0.5f * A, &sh, &ch);
-    sincos_acc(0.25f * S, &ss, &cs);
+    sincos_small(0.5f * A, &sh, &ch);
+    sincos_small(0.25f * S, &ss, &cs);
     p.sA = 2.0f * sh * ch;
     p.s2A = sh * sh;
     p.cA = fmaf(-2.0f, p.s2A, 1.0f);

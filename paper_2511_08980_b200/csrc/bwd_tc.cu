@@ -16,9 +16,12 @@
 
 namespace fdsdf {
 
+#ifndef BWD_TC_NEPI
+#define BWD_TC_NEPI 16
+#endif
 template <int MPAD>
-struct BtcCfg : TcCfg<MPAD, 80> {
-  using B = TcCfg<MPAD, 80>;
+struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI> {
+  using B = TcCfg<MPAD, 80, BWD_TC_NEPI>;
   static constexpr int CT = 8;                                      // centres per tile
   static constexpr int OFF_SD = B::OFF_X;                           // float [CT][20]: seeds + x
   static constexpr int OFF_BAR = OFF_SD + CT * 20 * 4;
@@ -26,7 +29,7 @@ struct BtcCfg : TcCfg<MPAD, 80> {
 };
 
 int bwd_tc_tile_centres() { return 8; }
-int bwd_tc_acc_slots(int mpad) { return 8 / (4 * (mpad / 128)); }  // accumulator slots per CTA (EG)
+int bwd_tc_acc_slots(int mpad) { return BWD_TC_NEPI / (4 * (mpad / 128)); }  // accumulator slots per CTA (EG)
 
 template <int ACT, int MPAD>
 __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const BwdArgs a) {

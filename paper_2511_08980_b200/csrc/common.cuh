@@ -98,6 +98,23 @@ __device__ __forceinline__ void sincos_acc(float x, float* s, float* c) {
   *c = cv;
 }
 
+// sincos_acc for the small arguments of the pair maps (A/2, S/4): |x| <= pi/4 needs no range
+// reduction (k = 0, r = x), so the polynomial alone gives bit-identical results; larger |x|
+// (rare) take the full path.
+__device__ __forceinline__ void sincos_small(float x, float* s, float* c) {
+  if (fabsf(x) <= 0.78539816339744831f) {
+    const float z = x * x;
+    float ps = fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f);
+    ps = fmaf(ps * z, x, x);
+    float pc = fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z, 4.166664568298827e-2f);
+    pc = fmaf(pc * z, z, fmaf(-0.5f, z, 1.0f));
+    *s = ps;
+    *c = pc;
+  } else {
+    sincos_acc(x, s, c);
+  }
+}
+
 // logistic s(t) = 1/(1+exp(-t)), accurate, saturating without NaN
 __device__ __forceinline__ float logistic_acc(float t) { return 1.0f / (1.0f + expf(-t)); }
 

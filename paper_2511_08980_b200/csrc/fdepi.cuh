@@ -18,6 +18,17 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// x^p for an integer p >= 0 (the |g|^p denominator, P:L112 p = 4) by repeated squaring
+__device__ __forceinline__ double ipow_d(double x, int p) {
+  double r = 1.0;
+  while (p > 0) {
+    if (p & 1) r *= x;
+    x *= x;
+    p >>= 1;
+  }
+  return r;
+}
+
 // cinfo layout per centre (16 floats): f, g0, g1, g2, u0, u1, u2, v0, v1, v2, mask, 0...
 constexpr int NCINFO = 16;
 
@@ -101,7 +112,7 @@ __device__ __forceinline__ void fd_centre(const FwdArgs& a, int64_t cc, bool val
   bool den_live = false;
   double den = 1.0;
   if (ls.denom == 2 || (ls.denom == 0 && !surf)) {
-    den = pow(gn, (double)ls.denom_pow);
+    den = ipow_d(gn, ls.denom_pow);
     den_live = true;
   }
   if (!msk) {

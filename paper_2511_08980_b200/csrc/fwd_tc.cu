@@ -27,9 +27,12 @@
 
 namespace fdsdf {
 
+#ifndef FWD_TC_NEPI
+#define FWD_TC_NEPI 16
+#endif
 template <int MPAD>
-struct FtcCfg : TcCfg<MPAD, 64> {
-  using B = TcCfg<MPAD, 64>;
+struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI> {
+  using B = TcCfg<MPAD, 64, FWD_TC_NEPI>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   static constexpr int OFF_RED = B::OFF_X;                          // float [NEPI][MAXC][4]
   static constexpr int OFF_CI = OFF_RED + B::NEPI * MAXC * 4 * 4;   // float [MAXC][16]
@@ -59,7 +62,7 @@ __global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < mp * mp; idx += gridDim.x * blockDim.x) {
     const int r = idx / mp, k = idx % mp;  // A-operand row r, K index k
     const int h = r >> 7, rr = r & 127, kc = k >> 6, kk = k & 63;
-    const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * TcCfg<128, 64>::STAGE + tc::sw128_off(rr, kk, 128);
+    const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * TcCfg<128, 64, 8>::STAGE + tc::sw128_off(rr, kk, 128);
     {
       const float v = (r < M && k < K) ? W[(size_t)r * K + k] : 0.f;  // forward: W[m = r][k]
       const tc::Bf3 s = tc::split3(v);

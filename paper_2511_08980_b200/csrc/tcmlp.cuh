@@ -18,7 +18,7 @@
 
 namespace fdsdf {
 
-template <int MPAD_, int N_>
+template <int MPAD_, int N_, int NEPI_ = 8>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
@@ -27,7 +27,7 @@ struct TcCfg {
   static constexpr int STAGE = 3 * 128 * 128;   // weight stage (kc, h): 3 pieces x 128 rows x 128 B
   static constexpr int NST = 2;                 // weight ring depth
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
-  static constexpr int NEPI = 8;                // epilogue warps
+  static constexpr int NEPI = NEPI_;            // epilogue warps (a multiple of 4 * MH)
   static constexpr int NTHR = (2 + NEPI) * 32;
   static constexpr int EG = NEPI / (4 * MH);    // epilogue warps per (lane quarter, M-half)
   static constexpr int OFF_W = 0;
@@ -37,6 +37,7 @@ struct TcCfg {
                                     : (MH * N) <= 256 ? 256 : 512;
   static_assert(N % 16 == 0 && N >= 16 && N <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
   static_assert(MH * N <= 512, "TMEM has 512 columns");
+  static_assert(NEPI % (4 * MH) == 0, "every (lane quarter, M-half) needs the same number of epilogue warps");
 };
 
 struct TcBars {

@@ -23,7 +23,12 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
-OURS = re.compile(r"(fwd_kernel|bwd_kernel|wgrad_kernel|finalize_kernel|pack_kernel)")
+TAG = ""
+OURS = re.compile(r"(fwd_kernel|bwd_kernel|wgrad_kernel|finalize_kernel|pack_kernel|fwd_tc_kernel|bwd_tc_kernel|"
+                  r"wgrad_tc_kernel|pack_tc_kernel)")
+FWD_TC_MODE = re.compile(r"fwd_tc_kernel<\s*(?:\(int\))?\d+,\s*(?:\(int\))?\d+,\s*(?:\(int\))?([12])>")
+# kernel -> the bench's timing slot name (bench.py kernel_ms keys)
+TC_SLOT = {"bwd_tc_kernel": "bwd", "wgrad_tc_kernel": "wgrad", "pack_tc_kernel": "pack_tc"}
 
 FULL_METRICS = [
     ("gpu__time_duration.sum", "duration"),
@@ -46,12 +51,17 @@ FULL_METRICS = [
 
 
 def short(name):
+    m = FWD_TC_MODE.search(name)
+    if m:
+        return "fwd_centre" if m.group(1) == "1" else "fwd"
     m = OURS.search(name)
-    return m.group(1).replace("_kernel", "") if m else name.split("(")[0][:60]
+    if not m:
+        return name.split("(")[0][:60]
+    return TC_SLOT.get(m.group(1), m.group(1).replace("_kernel", ""))
 
 
 def launches(path, rnd):
-    shutil.copy(path, os.path.join(PROF, f"r{rnd:02d}_launches.csv"))
+    shutil.copy(path, os.path.join(PROF, f"r{rnd:02d}{TAG}_launches.csv"))
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     ki, vi, mi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
@@ -63,15 +73,16 @@ def launches(path, rnd):
         a = agg.setdefault(k, [0, 0.0])
         a[0] += 1
         a[1] += float(r[vi])
-    ours_tot = sum(v[1] for k, v in agg.items() if OURS.search(k + "_kernel"))
+    mine = {"fwd", "fwd_centre", "bwd", "wgrad", "finalize", "pack", "pack_tc"}
+    ours_tot = sum(v[1] for k, v in agg.items() if k in mine)
     out = [f"# Round {rnd} launch list summary (ncu --metrics gpu__time_duration.sum --clock-control none)",
            "", "Cold-cache, serialised per-launch times: compare SHARES, not absolutes.", "",
            "| kernel | launches | total ms | mean ms | share of fdsdf kernel time |", "|---|---|---|---|---|"]
     for k, (n, t) in agg.items():
-        ours = OURS.search(k + "_kernel") is not None
+        ours = k in mine
         share = f"{100 * t / ours_tot:.1f}%" if ours and ours_tot else "(torch / harness)"
         out.append(f"| {k} | {n} | {t / 1e6:.3f} | {t / n / 1e6:.4f} | {share} |")
-    open(os.path.join(PROF, f"r{rnd:02d}_launch_shares.md"), "w").write("\n".join(out) + "\n")
+    open(os.path.join(PROF, f"r{rnd:02d}{TAG}_launch_shares.md"), "w").write("\n".join(out) + "\n")
     print("\n".join(out))
 
 
@@ -103,7 +114,7 @@ def full(rep, rnd):
         if max(vals) > 0.05:
             out.append(f"| {h[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]} | "
                        + " | ".join(f"{v:.2f}" for v in vals) + " |")
-    open(os.path.join(PROF, f"r{rnd:02d}_ncu_full.md"), "w").write("\n".join(out) + "\n")
+    open(os.path.join(PROF, f"r{rnd:02d}{TAG}_ncu_full.md"), "w").write("\n".join(out) + "\n")
     json.dump(dram, open(os.path.join(PROF, "ncu_dram_per_launch.json"), "w"), indent=1)
     print("\n".join(out))
 
@@ -113,7 +124,9 @@ if __name__ == "__main__":
     ap.add_argument("--round", type=int, required=True)
     ap.add_argument("--launches")
     ap.add_argument("--rep")
+    ap.add_argument("--tag", default="", help="file-name suffix, e.g. _tc")
     a = ap.parse_args()
+    TAG = a.tag
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
         launches(a.launches, a.round)
