@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     const int hh = (ew >> 2) % MH;
     const int eg = ew / (4 * MH);
     const int m = hh * 128 + 32 * q4 + lane;
-    const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * N;
+    const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * C::DH;
     const float beta = net.beta;
     const float h = a.h;
     const int64_t nrows = a.n * NCOLB;
@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             for (int j = 0; j < NCOLB; ++j) X[j] = wl * dL[j];
           } else {
             float v8[8], v2[2];
-            tc::tmem_ld8(taddr + (uint32_t)(cl * NCOLB), v8);
-            tc::tmem_ld2(taddr + (uint32_t)(cl * NCOLB + 8), v2);
+            tc_ld_sum8<C>(taddr, cl * NCOLB, v8);
+            tc_ld_sum2<C>(taddr, cl * NCOLB + 8, v2);
 #pragma unroll
             for (int j = 0; j < 8; ++j) X[j] = v8[j];
             X[8] = v2[0];

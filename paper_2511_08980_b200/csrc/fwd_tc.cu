@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
     const int hh = (ew >> 2) % MH;           // M-half
     const int eg = ew / (4 * MH);            // centre group
     const int m = hh * 128 + 32 * q4 + lane; // output neuron of this thread
-    const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * N;
+    const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * C::DH;
     const float beta = net.beta;
     const float h = a.h;
     const bool step = a.step != 0;
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
               }
             } else {
               float v[8];
-              tc::tmem_ld8(taddr + (uint32_t)((cl >> 1) * 8), v);
+              tc_ld_sum8<C>(taddr, (cl >> 1) * 8, v);
               const int o = (cl & 1) * 4;
               if (mok) {
                 z = om * (v[o] + net.b[l][m]);
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
               }
             } else {
               float v[8];
-              tc::tmem_ld8(taddr + (uint32_t)(cl * 8), v);
+              tc_ld_sum8<C>(taddr, cl * 8, v);
               if (mok) {
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {

@@ -27,16 +27,19 @@ struct TcCfg {
   static constexpr int STAGE = 3 * 128 * 128;   // weight stage (kc, h): 3 pieces x 128 rows x 128 B
   static constexpr int NST = 2;                 // weight ring depth
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
+  static constexpr int BKC = 3 * N * 128;       // one K chunk of B: the 3 pieces as consecutive row blocks
   static constexpr int NEPI = NEPI_;            // epilogue warps (a multiple of 4 * MH)
   static constexpr int NTHR = (2 + NEPI) * 32;
   static constexpr int EG = NEPI / (4 * MH);    // epilogue warps per (lane quarter, M-half)
   static constexpr int OFF_W = 0;
   static constexpr int OFF_B = NST * STAGE;
   static constexpr int OFF_X = OFF_B + 3 * BPIECE;  // kernel-specific scratch starts here
-  static constexpr uint32_t TCOLS = (MH * N) <= 32 ? 32 : (MH * N) <= 64 ? 64 : (MH * N) <= 128 ? 128
-                                    : (MH * N) <= 256 ? 256 : 512;
-  static_assert(N % 16 == 0 && N >= 16 && N <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
-  static_assert(MH * N <= 512, "TMEM has 512 columns");
+  // TMEM: per M-half three accumulator ranges of N columns (see tc_mma)
+  static constexpr int DH = 3 * N;
+  static constexpr uint32_t TCOLS = (MH * DH) <= 32 ? 32 : (MH * DH) <= 64 ? 64 : (MH * DH) <= 128 ? 128
+                                    : (MH * DH) <= 256 ? 256 : 512;
+  static_assert(N % 16 == 0 && N >= 16 && 3 * N <= 256, "tcgen05 M=128 needs N % 16 == 0 and 3N <= 256");
+  static_assert(MH * DH <= 512, "TMEM has 512 columns");
   static_assert(NEPI % (4 * MH) == 0, "every (lane quarter, M-half) needs the same number of epilogue warps");
 };
 
@@ -112,11 +115,20 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
     }
 }
 
-// MMA issuer (one thread): D[h] (TMEM columns h*N ..) = A_stage . B for every GEMM of every tile.
+// MMA issuer (one thread): for every GEMM of every tile and every weight stage (kc, h), per
+// 16-wide K step three MMAs, one per A piece, against the B pieces stored as consecutive row
+// blocks [b0 | b1 | b2] of the K chunk:
+//     a0 . [b0|b1|b2]  (N = 3N) -> TMEM ranges 0, 1, 2 of half h
+//     a1 . [b0|b1]     (N = 2N) -> ranges 0, 1
+//     a2 . [b0]        (N =  N) -> range 0
+// i.e. exactly the six bf16x6 products, with range r = sum of the products a_i b_r; the
+// epilogue adds the ranges (tc_ld_sum).  Each A piece is read from shared memory once per K
+// step instead of once per product, which is what bounds the MMA phase at N = 64.
 template <class C>
 __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned char* Ws,
                                        const unsigned char* Bs, uint32_t tbase, const TcBars& b) {
-  constexpr uint32_t idesc = tc::idesc_bf16(128, C::N);
+  constexpr uint32_t id3 = tc::idesc_bf16(128, 3 * C::N), id2 = tc::idesc_bf16(128, 2 * C::N),
+                     id1 = tc::idesc_bf16(128, C::N);
   uint32_t it = 0, nb = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
     for (int g = 0; g < ngemm; ++g) {
@@ -130,15 +142,15 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
           mbar_wait(&b.wfull[s], ph);
           tc::fence_after();
           const uint32_t wa = smem_u32(Ws + s * C::STAGE);
-          const uint32_t ba = smem_u32(Bs + kc * C::N * 128);
+          const uint32_t ba = smem_u32(Bs + kc * C::BKC);
+          const uint32_t d = tbase + h * C::DH;
 #pragma unroll
-          for (int sub = 0; sub < 4; ++sub)
-#pragma unroll
-            for (int q = 0; q < 6; ++q) {
-              const uint64_t ad = tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32);
-              const uint64_t bd = tc::sdesc_sw128(ba + tc::prod_b(q) * C::BPIECE + sub * 32);
-              tc::mma_bf16(tbase + h * C::N, ad, bd, idesc, (kc | sub | q) != 0 ? 1u : 0u);
-            }
+          for (int sub = 0; sub < 4; ++sub) {
+            const uint64_t bd = tc::sdesc_sw128(ba + sub * 32);
+            tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
+            tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
+            tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+          }
           tc::mma_commit(&b.wempty[s]);
         }
       tc::mma_commit(b.dfull);
@@ -154,13 +166,35 @@ __device__ __forceinline__ void tc_epi_arrive(const TcBars& b) {
   if ((threadIdx.x & 31) == 0) mbar_arrive(b.bfull);
 }
 
-// write v (split into 3 bf16 pieces) at B operand element (column n, K index k)
+// write v (split into 3 bf16 pieces) at B operand element (column n, K index k): K chunk
+// k/64 holds the pieces as row blocks [b0 | b1 | b2] of N rows each (SWIZZLE_128B rows)
 template <class C>
 __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float v) {
   const tc::Bf3 s = tc::split3(v);
-  const uint32_t off = tc::sw128_off(n, k, C::N);
+  const uint32_t off = (uint32_t)((k >> 6) * C::BKC) + tc::sw128_off(n, k & 63, C::N);
 #pragma unroll
-  for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::BPIECE + off) = s.p[p];
+  for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::N * 128 + off) = s.p[p];
+}
+
+// accumulator of columns [col, col + W) of this warp's lane quarter: the sum of the three
+// TMEM ranges (range 0 + (range 1 + range 2), smallest terms first)
+template <class C>
+__device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8]) {
+  float r1[8], r2[8];
+  tc::tmem_ld8(taddr + col, v);
+  tc::tmem_ld8(taddr + C::N + col, r1);
+  tc::tmem_ld8(taddr + 2 * C::N + col, r2);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] += r1[j] + r2[j];
+}
+template <class C>
+__device__ __forceinline__ void tc_ld_sum2(uint32_t taddr, int col, float (&v)[2]) {
+  float r1[2], r2[2];
+  tc::tmem_ld2(taddr + col, v);
+  tc::tmem_ld2(taddr + C::N + col, r1);
+  tc::tmem_ld2(taddr + 2 * C::N + col, r2);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) v[j] += r1[j] + r2[j];
 }
 
 }  // namespace fdsdf
