@@ -38,6 +38,19 @@ __device__ __forceinline__ Bf3 split3(float x) {
   return o;
 }
 
+// the same exact split for two values at once, as packed bf16x2 words (lo half = x, hi = y):
+// cvt.rn.bf16x2.f32 runs on the ALU pipe, the scalar conversion on the quarter-rate XU
+__device__ __forceinline__ void split3x2(float x, float y, uint32_t (&w)[3]) {
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const __nv_bfloat162 b = __floats2bfloat162_rn(x, y);
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(&b);
+    w[p] = u;
+    x -= __uint_as_float(u << 16);
+    y -= __uint_as_float(u & 0xFFFF0000u);
+  }
+}
+
 // byte offset of element (r, k) in a K-major SWIZZLE_128B bf16 tile with R rows
 __host__ __device__ __forceinline__ uint32_t sw128_off(int r, int k, int R) {
   const int kc = k >> 6, kk = k & 63;

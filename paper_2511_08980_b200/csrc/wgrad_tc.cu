@@ -120,27 +120,36 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
         mbar_wait(&sempty[s], ((it / NST) & 1u) ^ 1u);
         unsigned char* dst = sm + s * C::STAGE;
         const int64_t jb = j0 + (int64_t)ch * JC;
-#pragma unroll 2
-        for (int item = st; item < JC * QUADS; item += C::NSTG * 32) {
+        // all loads of this thread's items first (8 float4 of delta + 8 of a in flight), then
+        // split and store
+        constexpr int NIT = JC * QUADS / (C::NSTG * 32);
+        float4 dv[NIT], av[NIT];
+#pragma unroll
+        for (int q = 0; q < NIT; ++q) {
+          const int item = st + q * C::NSTG * 32;
           const int jj = item / QUADS, r = (item % QUADS) * 4;
           const int64_t j = jb + jj;
-          float4 dv = make_float4(0.f, 0.f, 0.f, 0.f), av = dv;
+          dv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          av[q] = dv[q];
           if (j < j1) {
-            dv = __ldg(reinterpret_cast<const float4*>(D + j * MPAD + r));
-            av = __ldg(reinterpret_cast<const float4*>(A + j * MPAD + r));
+            dv[q] = __ldg(reinterpret_cast<const float4*>(D + j * MPAD + r));
+            av[q] = __ldg(reinterpret_cast<const float4*>(A + j * MPAD + r));
           }
+        }
+#pragma unroll
+        for (int q = 0; q < NIT; ++q) {
+          const int item = st + q * C::NSTG * 32;
+          const int jj = item / QUADS, r = (item % QUADS) * 4;
           const uint32_t off = tc::sw128mn_off(r, jj, MPAD);
-          const tc::Bf3 d0 = tc::split3(dv.x), d1 = tc::split3(dv.y), d2 = tc::split3(dv.z), d3 = tc::split3(dv.w);
-          const tc::Bf3 a0 = tc::split3(av.x), a1 = tc::split3(av.y), a2 = tc::split3(av.z), a3 = tc::split3(av.w);
+          uint32_t d01[3], d23[3], a01[3], a23[3];
+          tc::split3x2(dv[q].x, dv[q].y, d01);
+          tc::split3x2(dv[q].z, dv[q].w, d23);
+          tc::split3x2(av[q].x, av[q].y, a01);
+          tc::split3x2(av[q].z, av[q].w, a23);
 #pragma unroll
           for (int p = 0; p < 3; ++p) {
-            uint2 wd, wa;
-            wd.x = (uint32_t)__bfloat16_as_ushort(d0.p[p]) | ((uint32_t)__bfloat16_as_ushort(d1.p[p]) << 16);
-            wd.y = (uint32_t)__bfloat16_as_ushort(d2.p[p]) | ((uint32_t)__bfloat16_as_ushort(d3.p[p]) << 16);
-            wa.x = (uint32_t)__bfloat16_as_ushort(a0.p[p]) | ((uint32_t)__bfloat16_as_ushort(a1.p[p]) << 16);
-            wa.y = (uint32_t)__bfloat16_as_ushort(a2.p[p]) | ((uint32_t)__bfloat16_as_ushort(a3.p[p]) << 16);
-            *reinterpret_cast<uint2*>(dst + p * C::PIECE + off) = wd;
-            *reinterpret_cast<uint2*>(dst + C::OPER + p * C::PIECE + off) = wa;
+            *reinterpret_cast<uint2*>(dst + p * C::PIECE + off) = make_uint2(d01[p], d23[p]);
+            *reinterpret_cast<uint2*>(dst + C::OPER + p * C::PIECE + off) = make_uint2(a01[p], a23[p]);
           }
         }
         fence_proxy_async();
