@@ -133,7 +133,9 @@ enum {
 enum {                          /* sticky device flags                                     */
   FDSDF_FLAG_NONFINITE_INPUT = 1u,  /* a centre coordinate was not finite          */
   FDSDF_FLAG_NONFINITE_LOSS = 2u,   /* the loss was not finite                     */
-  FDSDF_FLAG_ALL_FD_SKIPPED = 4u    /* every centre was masked: L_fd = 0           */
+  FDSDF_FLAG_ALL_FD_SKIPPED = 4u,   /* every centre was masked: L_fd = 0           */
+  FDSDF_FLAG_NONFINITE_GRAD = 8u    /* fdsdf_adam met a non-finite gradient entry; that     */
+                                    /* parameter was left unchanged                */
 };
 
 typedef struct fdsdf_ctx fdsdf_ctx;
@@ -196,6 +198,36 @@ fdsdf_status fdsdf_comm_unique_id(uint8_t id[128]);
 fdsdf_status fdsdf_comm_init(fdsdf_ctx* ctx, const uint8_t id[128], int rank, int world);
 fdsdf_status fdsdf_allreduce(fdsdf_ctx* ctx, float* d_buf, int64_t count, void* stream);
 
+/* ---------------------------------------------------------------- training iteration
+ * (§4).  A full iteration is, on one stream:
+ *   fdsdf_sample -> fdsdf_step (FDSDF_STEP_ALLREDUCE when data-parallel) -> fdsdf_adam. */
+
+/* Per-iteration batch ("we sample 30k surface points; 20k are used per iteration,
+ * with 20k off-surface samples drawn uniformly in the bounding box").  Writes d_x_out
+ * [n_pick + n_uniform][3] (device, caller-owned): rows [0, n_pick) are n_pick DISTINCT rows
+ * of d_pool [n_pool][3] (sampling without replacement: pool index pi(row), pi a keyed
+ * pseudo-random permutation -- 4-round Feistel network, cycle-walked; key from (seed,
+ * iteration)), rows [n_pick, n_pick + n_uniform) are points uniform in [-box_half, box_half]^3
+ * (SplitMix64 of (seed, iteration, row, coordinate)).  Deterministic: same arguments, same
+ * output bits (train.cu documents both generators; oracle/train_oracle.py implements them).
+ * Errors (checked in this order): ctx NULL, n_pick < 0, n_uniform < 0, iteration < 0,
+ * n_pick > n_pool, d_pool NULL while n_pick > 0, box_half not finite or <= 0 ->
+ * FDSDF_E_INVALID; n_pick + n_uniform == 0 -> FDSDF_E_EMPTY; d_x_out NULL -> FDSDF_E_INVALID. */
+fdsdf_status fdsdf_sample(fdsdf_ctx* ctx, const float* d_pool, int64_t n_pool, int64_t n_pick,
+                          float box_half, int64_t n_uniform, uint64_t seed, int64_t iteration,
+                          float* d_x_out, void* stream);
+
+/* In-place Adam update of d_params [P] from d_grad [P] with first / second moment buffers
+ * d_m, d_v [P] (device, caller-owned, zero before step 1), step t >= 1 ("Adam
+ * optimizer (5e-5)"; standard bias-corrected form):
+ *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+ *   p -= lr / (1 - b1^t) * m / (sqrt(v / (1 - b2^t)) + eps).
+ * A non-finite gradient entry leaves that parameter and its moments unchanged and sets
+ * FDSDF_FLAG_NONFINITE_GRAD.  Errors: NULL pointers, t < 1, lr not finite or <= 0, b1 or b2
+ * outside [0, 1), eps < 0 -> FDSDF_E_INVALID. */
+fdsdf_status fdsdf_adam(fdsdf_ctx* ctx, float* d_params, const float* d_grad, float* d_m, float* d_v,
+                        int64_t t, float lr, float beta1, float beta2, float eps, void* stream);
+
 /* Diagnostics (synchronous). */
 const char* fdsdf_status_string(fdsdf_status s);
 const char* fdsdf_last_error(const fdsdf_ctx* ctx);
@@ -223,7 +255,9 @@ enum {
   FDSDF_KSLOT_ALLREDUCE = 5, /* NCCL group (not a kernel of this library)                */
   FDSDF_KSLOT_PACK_TC = 6,   /* bf16x3 weight images for the tensor-core kernels           */
   FDSDF_KSLOT_FWD_CENTRE = 7,/* tensor path: centre + tangent columns (f, grad f, frame)   */
-  FDSDF_NUM_KSLOTS = 8
+  FDSDF_KSLOT_SAMPLE = 8,    /* fdsdf_sample                                               */
+  FDSDF_KSLOT_ADAM = 9,      /* fdsdf_adam                                                 */
+  FDSDF_NUM_KSLOTS = 10
 };
 fdsdf_status fdsdf_set_kernel_timing(fdsdf_ctx* ctx, int enable);
 fdsdf_status fdsdf_kernel_times(fdsdf_ctx* ctx, double* ms_total, int64_t* count, int nslots, int reset);

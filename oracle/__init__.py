@@ -6,3 +6,4 @@ The product path (paper_2511_08980_b200) never imports it and shares no code,
 constants or helpers with it.
 """
 from .fdsdf_oracle import *  # noqa: F401,F403
+from .train_oracle import *  # noqa: F401,F403

@@ -602,6 +602,44 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   return done(FDSDF_OK);
 }
 
+fdsdf_status fdsdf_sample(fdsdf_ctx* c, const float* d_pool, int64_t n_pool, int64_t n_pick, float box_half,
+                          int64_t n_uniform, uint64_t seed, int64_t iteration, float* d_x_out, void* stream) {
+  if (!c) return FDSDF_E_INVALID;
+  if (n_pick < 0 || n_uniform < 0 || iteration < 0) return fail(c, FDSDF_E_INVALID, "negative count or iteration");
+  if (n_pick > 0 && (!d_pool || n_pick > n_pool)) return fail(c, FDSDF_E_INVALID, "need n_pick <= n_pool and a pool");
+  if (!(box_half > 0.f) || !std::isfinite(box_half)) return fail(c, FDSDF_E_INVALID, "box_half must be finite and > 0");
+  if (n_pick + n_uniform == 0) return fail(c, FDSDF_E_EMPTY, "empty batch");
+  if (!d_x_out) return fail(c, FDSDF_E_INVALID, "null output pointer");
+  cudaStream_t strm = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != c->device) cudaSetDevice(c->device);
+  const cudaError_t e = run_slot(c, FDSDF_KSLOT_SAMPLE, strm, [&] {
+    return launch_sample(d_pool, n_pool, n_pick, box_half, n_uniform, seed, iteration, d_x_out, strm);
+  });
+  if (prev != c->device) cudaSetDevice(prev);
+  return e == cudaSuccess ? FDSDF_OK : cuda_fail(c, e, "sample_kernel");
+}
+
+fdsdf_status fdsdf_adam(fdsdf_ctx* c, float* d_params, const float* d_grad, float* d_m, float* d_v, int64_t t,
+                        float lr, float beta1, float beta2, float eps, void* stream) {
+  if (!c || !d_params || !d_grad || !d_m || !d_v) return fail(c, FDSDF_E_INVALID, "null pointer argument");
+  if (t < 1) return fail(c, FDSDF_E_INVALID, "Adam step t must be >= 1");
+  if (!(lr > 0.f) || !std::isfinite(lr)) return fail(c, FDSDF_E_INVALID, "lr must be finite and > 0");
+  if (!(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f))
+    return fail(c, FDSDF_E_INVALID, "betas must lie in [0, 1)");
+  if (!(eps >= 0.f) || !std::isfinite(eps)) return fail(c, FDSDF_E_INVALID, "eps must be finite and >= 0");
+  cudaStream_t strm = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != c->device) cudaSetDevice(c->device);
+  const cudaError_t e = run_slot(c, FDSDF_KSLOT_ADAM, strm, [&] {
+    return launch_adam(d_params, d_grad, d_m, d_v, c->P, lr, beta1, beta2, eps, t, c->dflags, strm);
+  });
+  if (prev != c->device) cudaSetDevice(prev);
+  return e == cudaSuccess ? FDSDF_OK : cuda_fail(c, e, "adam_kernel");
+}
+
 fdsdf_status fdsdf_comm_unique_id(uint8_t id[128]) {
   if (!id) return FDSDF_E_INVALID;
   std::string err;

@@ -134,6 +134,12 @@ int bwd_tc_tile_centres();                          // 8
 int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
 cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, cudaStream_t st);
 int wgrad_tc_splits(int nsm, int64_t rows);         // split-K factor of the tensor wgrad
+// training iteration (train.cu)
+int feistel_half_bits(int64_t n_pool);
+cudaError_t launch_sample(const float* pool, int64_t n_pool, int64_t n_pick, float half, int64_t n_uniform,
+                          uint64_t seed, int64_t iteration, float* out, cudaStream_t st);
+cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                        float eps, int64_t t, unsigned* dflags, cudaStream_t st);
 int fwd_tile_centres(int mpad);   // centres per forward tile
 int bwd_tile_centres(int mpad);   // centres per backward tile
 size_t fwd_smem_bytes(int mpad);

@@ -23,7 +23,7 @@ FD_FORM = {"abs": 0, "square": 1}
 STEP_ACCUMULATE, STEP_ALLREDUCE = 1, 2
 CREATE_EVAL_ONLY, CREATE_FFMA, CREATE_TENSOR = 1, 2, 4
 PATH = {0: "ffma", 1: "tensor"}
-FLAG_NONFINITE_INPUT, FLAG_NONFINITE_LOSS, FLAG_ALL_FD_SKIPPED = 1, 2, 4
+FLAG_NONFINITE_INPUT, FLAG_NONFINITE_LOSS, FLAG_ALL_FD_SKIPPED, FLAG_NONFINITE_GRAD = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_EMPTY", 3: "E_CUDA", 4: "E_NCCL", 5: "E_NOMEM",
           6: "E_UNSUPPORTED"}
 
@@ -97,6 +97,10 @@ def lib():
         L.fdsdf_last_error.restype = C.c_char_p
         L.fdsdf_get_device_flags.argtypes = [vp, C.POINTER(u32)]
         L.fdsdf_get_device_flags.restype = C.c_int
+        L.fdsdf_sample.argtypes = [vp, vp, i64, i64, C.c_float, i64, C.c_uint64, i64, vp, vp]
+        L.fdsdf_sample.restype = C.c_int
+        L.fdsdf_adam.argtypes = [vp, vp, vp, vp, vp, i64, C.c_float, C.c_float, C.c_float, C.c_float, vp]
+        L.fdsdf_adam.restype = C.c_int
         L.fdsdf_path.argtypes = [vp]
         L.fdsdf_path.restype = i32
         L.fdsdf_last_launch_count.argtypes = [vp]
@@ -210,6 +214,17 @@ def fdsdf_step(ctx, params, x, n, stencil: Stencil, loss: Loss, grad, loss_out, 
                             _ptr(grad), _ptr(loss_out), int(flags), _stream(stream)), ctx)
 
 
+def fdsdf_sample(ctx, pool, n_pick, box_half, n_uniform, seed, iteration, out, stream=None):
+    _check(lib().fdsdf_sample(ctx, _ptr(pool), int(pool.shape[0]) if pool is not None else 0, int(n_pick),
+                              float(box_half), int(n_uniform), int(seed) & ((1 << 64) - 1), int(iteration),
+                              _ptr(out), _stream(stream)), ctx)
+
+
+def fdsdf_adam(ctx, params, grad, m, v, t, lr=5e-5, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+    _check(lib().fdsdf_adam(ctx, _ptr(params), _ptr(grad), _ptr(m), _ptr(v), int(t), float(lr), float(beta1),
+                            float(beta2), float(eps), _stream(stream)), ctx)
+
+
 def fdsdf_comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().fdsdf_comm_unique_id(buf))
@@ -234,7 +249,7 @@ def fdsdf_get_device_flags(ctx) -> int:
 def fdsdf_last_launch_count(ctx) -> int:
     return int(lib().fdsdf_last_launch_count(ctx))
 
-KSLOTS = ("pack", "fwd", "bwd", "wgrad", "finalize", "allreduce", "pack_tc", "fwd_centre")
+KSLOTS = ("pack", "fwd", "bwd", "wgrad", "finalize", "allreduce", "pack_tc", "fwd_centre", "sample", "adam")
 
 
 def fdsdf_set_kernel_timing(ctx, enable: bool):
@@ -321,6 +336,19 @@ class FDSDF:
         fdsdf_step(self.ctx, params, x, n, st, ls, grad, loss, flags, stream)
         return grad, loss
 
+    def sample(self, pool, n_pick, box_half, n_uniform, seed, iteration, out=None, stream=None):
+        """Per-iteration batch on the device: n_pick distinct pool rows + n_uniform box points."""
+        import torch
+        pool = self._dev(pool, torch.float32).reshape(-1, 3)
+        if out is None:
+            out = torch.empty(int(n_pick) + int(n_uniform), 3, device=self.device, dtype=torch.float32)
+        fdsdf_sample(self.ctx, pool, n_pick, box_half, n_uniform, seed, iteration, out, stream)
+        return out
+
+    def adam(self, params, grad, m, v, t, lr=5e-5, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+        """In-place Adam update of the device tensor params (m, v: device moment buffers)."""
+        fdsdf_adam(self.ctx, params, grad, m, v, t, lr, beta1, beta2, eps, stream)
+
     def comm_init(self, uid: bytes, rank: int, world: int):
         fdsdf_comm_init(self.ctx, uid, rank, world)
 
@@ -350,3 +378,46 @@ def fdsdf_selftest_mma(W, B, nprod=6, mn_major=0, stream=None):
 
 def version() -> str:
     return lib().fdsdf_version().decode()
+
+
+class Trainer:
+    """The full training iteration of PAPER.md §4 on one device: per
+    iteration fdsdf_sample (n_pick of the surface pool + n_uniform box points) ->
+    fdsdf_step (+ NCCL allreduce when data-parallel) -> fdsdf_adam, all enqueued on one
+    stream with no host synchronisation.  Host-side orchestration only."""
+
+    def __init__(self, model: FDSDF, params, pool, n_pick, n_uniform, box_half, h, loss_cfg, seed=0,
+                 lr=5e-5, betas=(0.9, 0.999), eps=1e-8, counts=None, index_offset=0, allreduce=False):
+        import torch
+        self.m = model
+        self.params = model._dev(params, torch.float32).clone()
+        self.pool = model._dev(pool, torch.float32).reshape(-1, 3)
+        self.n_pick, self.n_uniform, self.box_half, self.h = int(n_pick), int(n_uniform), float(box_half), float(h)
+        self.loss_cfg, self.seed, self.lr, self.betas, self.eps = loss_cfg, int(seed), lr, betas, eps
+        n = self.n_pick + self.n_uniform
+        self.counts = counts if counts is not None else (self.n_pick, self.n_uniform, n)
+        self.index_offset, self.allreduce = int(index_offset), bool(allreduce)
+        self.x = torch.empty(n, 3, device=model.device, dtype=torch.float32)
+        self.grad = torch.zeros(model.P, device=model.device, dtype=torch.float32)
+        self.loss = torch.zeros(8, device=model.device, dtype=torch.float64)
+        self.mom1 = torch.zeros_like(self.grad)
+        self.mom2 = torch.zeros_like(self.grad)
+        self.t = 0
+
+    def frame_seed(self, it):
+        """Per-iteration frame seed: frames are redrawn every iteration; the same
+        convention as harness.frame_seed (high 32 bits: base seed, low 32 bits: iteration)."""
+        return ((self.seed & 0xFFFFFFFF) << 32 | (int(it) & 0xFFFFFFFF)) & ((1 << 64) - 1)
+
+    def iterate(self, stream=None):
+        """One iteration; returns the device loss tensor [8] (of the batch before the update)."""
+        it = self.t
+        self.m.sample(self.pool, self.n_pick, self.box_half, self.n_uniform, self.seed, it, out=self.x,
+                      stream=stream)
+        self.m.step(self.params, self.x, self.n_pick, self.h, self.loss_cfg, counts=self.counts,
+                    frame_seed=self.frame_seed(it), index_offset=self.index_offset, grad=self.grad,
+                    loss=self.loss, allreduce=self.allreduce, stream=stream)
+        self.t += 1
+        self.m.adam(self.params, self.grad, self.mom1, self.mom2, self.t, self.lr, self.betas[0], self.betas[1],
+                    self.eps, stream=stream)
+        return self.loss
