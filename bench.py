@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--config", choices=("c2", "c5"), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the train-iteration and eval measurements")
+    ap.add_argument("--eval-sweep", action="store_true",
+                    help="C5e: fdsdf_eval throughput for 1e4 .. 1e7 centres (rank 0, adds 'eval_sweep')")
     ap.add_argument("--path", choices=("default", "ffma", "tensor"), default="default",
                     help="contraction path of the library (default: the library's choice)")
     return ap.parse_args()
@@ -206,6 +209,81 @@ def workload(name, rank, world):
 # ----------------------------------------------------------------------------- our arm
 
 
+def _event_ms(stream, fn, steps, flush):
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        fn(i)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev) / steps
+
+
+def measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank, dev):
+    """(1) the full training iteration of PAPER.md §4: fdsdf_sample (20k of a
+    30k CSG surface pool + 20k box points) -> fdsdf_step (+ allreduce) -> fdsdf_adam
+    (lr 5e-5); (2) fdsdf_eval throughput (f, grad f, FD Hessian, D, K, frames, mask) on
+    the same batch; (3) optionally the C5e eval sweep.  All CUDA-event timed on the stream."""
+    import torch
+    from harness import csg_surface
+    from paper_2511_08980_b200 import FDSDF
+    from paper_2511_08980_b200.fdsdf import Trainer
+    out = {}
+    n = len(cfg["x"])
+    ns = cfg["n_surface"]
+    pool = csg_surface(int(ns * 1.5), 3, 100 + rank).astype(np.float32)
+    lc = cfg["loss"]
+    tr = Trainer(model, params, pool, ns, n - ns, 1.1, cfg["h"], lc, seed=4 + 1000 * rank,
+                 counts=cfg["counts"], index_offset=cfg["index_offset"], allreduce=world > 1)
+    for _ in range(args.warmup):
+        tr.iterate(stream)
+    barrier()
+    ms = _event_ms(stream, lambda i: tr.iterate(stream), args.steps, flush)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    out["train_iteration"] = {
+        "ms": ms, "iterations_per_s": 1e3 / ms, "stencil_points_per_s": 9.0 * n * world / (ms * 1e-3),
+        "includes": "fdsdf_sample (20k of a 30k CSG pool + 20k box points, fresh per iteration) + "
+                    "fdsdf_step" + (" + NCCL allreduce" if world > 1 else "") + " + fdsdf_adam (lr 5e-5)",
+        "paper_context": "NCR-FD per-iteration time on H100, P:L399-403: 6.03 (caption unit ms) or 60.3 ms "
+                         "(10-ms reading), BASELINE.md §1"}
+    # eval throughput on this batch
+    x = torch.from_numpy(cfg["x"]).to(dev)
+    pdev = torch.from_numpy(cfg["params"]).to(dev)
+    outs = model.eval(pdev, x, ns, cfg["h"], frame_seed=1, stream=stream)
+    for i in range(args.warmup):
+        model.eval(pdev, x, ns, cfg["h"], frame_seed=i, stream=stream, outputs=outs)
+    ms_e = _event_ms(stream, lambda i: model.eval(pdev, x, ns, cfg["h"], frame_seed=i, stream=stream, outputs=outs),
+                     args.steps, flush)
+    out["eval"] = {"ms": ms_e, "centres": n, "stencil_points_per_s": 9.0 * n / (ms_e * 1e-3),
+                   "outputs": "f, grad f, (f_uu, f_uv, f_vv), D, K, frames, mask"}
+    if args.eval_sweep and rank == 0:
+        from harness import csg_surface as cs, uniform_box
+        sweep = []
+        nmax = 10_000_000
+        em = FDSDF(cfg["spec"], dev.index, max_centers=nmax, eval_only=True,
+                   path=None if args.path == "default" else args.path)
+        xs = np.concatenate([cs(nmax // 2, 3, 7), uniform_box(nmax - nmax // 2, 1.1, 8)]).astype(np.float32)
+        xall = torch.from_numpy(xs).to(dev)
+        for nn in (10_000, 30_000, 100_000, 300_000, 1_000_000, 3_000_000, 10_000_000):
+            xi = xall[:nn]
+            o = em.eval(pdev, xi, nn // 2, cfg["h"], frame_seed=0, stream=stream)
+            for i in range(2):
+                em.eval(pdev, xi, nn // 2, cfg["h"], frame_seed=i, stream=stream, outputs=o)
+            reps = 5 if nn <= 1_000_000 else 2
+            ms_s = _event_ms(stream, lambda i: em.eval(pdev, xi, nn // 2, cfg["h"], frame_seed=i, stream=stream,
+                                                      outputs=o), reps, flush)
+            sweep.append({"centres": nn, "ms": ms_s, "stencil_points_per_s": 9.0 * nn / (ms_s * 1e-3)})
+        em.close()
+        out["eval_sweep"] = sweep
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -323,6 +401,11 @@ def main():
         e2e = {"value": 9.0 * n * world / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(P * 4 + 8 * 8)}
 
+    # ------------------------------------------------------------------ full training iteration + eval
+    extras = {}
+    if not args.no_extras:
+        extras = measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank, dev)
+
     # ------------------------------------------------------------------ roofline of the dominant kernel
     P_mm, P_gemm = p_mm(spec)
     path = model.path
@@ -389,7 +472,7 @@ def main():
             "kernel_ms": kernel_ms, "path": path,
             "precision": ("bf16x6: fp32 operands split exactly into 3 bf16 pieces, 6 tcgen05 products, fp32 "
                           "accumulation" if path == "tensor" else "fp32 FFMA"), "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches_per_step * args.steps), "clocks": clocks,
+            "gpu_launches": int(launches_per_step * args.steps), "clocks": clocks, **extras,
             "wall_s_timed_region": wall,
         }
         print(json.dumps(line), flush=True)
