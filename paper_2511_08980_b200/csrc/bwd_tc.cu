@@ -16,6 +16,9 @@
 
 namespace fdsdf {
 
+#ifndef BWD_TC_PREFETCH
+#define BWD_TC_PREFETCH 0
+#endif
 #ifndef BWD_TC_NEPI
 #define BWD_TC_NEPI 16
 #endif
@@ -75,11 +78,28 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     float* acc_dWL = bacc + (size_t)(L - 1) * MPAD;
     float* acc_dbL = acc_dWL + MPAD;
     float* acc_dW0 = acc_dbL + 1;
-    for (int64_t i = (ew % (4 * MH)) * 32 + lane; i < a.nacc; i += 32 * 4 * MH) bacc[i] = 0.f;  // own slot
+    // this thread's accumulators (its neuron m), summed over its tiles in tile order and
+    // written once at the end: db per hidden layer, dW_last[m], dW_0[m][:], db_last (m == 0)
+    float r_db[MAXL];
+#pragma unroll
+    for (int l = 0; l < MAXL; ++l) r_db[l] = 0.f;
+    float r_dWL = 0.f, r_dbL = 0.f, r_dW0[3] = {0.f, 0.f, 0.f};
     uint32_t nd = 0;
+    // the stored forward pre-activations of a tile are one contiguous block of zf
+    auto prefetch_tile = [&](int64_t tile) {
+      if (et == 0 && tile < a.ntiles) {
+        const int64_t cb = tile * CT, ce = min(cb + CT, a.n);
+        const size_t per = (size_t)nh * NCOLF * MPAD * sizeof(float);
+        const char* p0 = reinterpret_cast<const char*>(a.zf) + (size_t)cb * per;
+        for (size_t off = 0; off < (size_t)(ce - cb) * per; off += 65536)
+          prefetch_l2_bulk(p0 + off, (uint32_t)min((size_t)65536, (size_t)(ce - cb) * per - off));
+      }
+    };
+    if (BWD_TC_PREFETCH) prefetch_tile(blockIdx.x);
 
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       const int64_t c0 = tile * CT;
+      if (BWD_TC_PREFETCH) prefetch_tile(tile + gridDim.x);
       bar_named(1, C::NEPI * 32);  // previous tile's seed reads are done
       for (int i = et; i < CT * 20; i += C::NEPI * 32) {
         const int cl = i / 20, q = i % 20;
@@ -227,22 +247,27 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         } else if (!top) {
           tc::fence_before();
         }
-        if (mok) {
-          acc_db[(size_t)l * MPAD + m] += s_db;
-          if (top) acc_dWL[m] += s_vL;
-          if (l == 0) {
-            acc_dW0[m * 3 + 0] += s_w0[0];
-            acc_dW0[m * 3 + 1] += s_w0[1];
-            acc_dW0[m * 3 + 2] += s_w0[2];
-          }
+        r_db[l] += s_db;
+        if (top) r_dWL += s_vL;
+        if (l == 0) {
+          r_dW0[0] += s_w0[0];
+          r_dW0[1] += s_w0[1];
+          r_dW0[2] += s_w0[2];
         }
       }
       if (m == 0) {  // bias of the last layer: sum of the centre seeds (fbar) of this group
         float v = 0.f;
         for (int i = 0; i < CPE; ++i) v += sds[(eg + EG * i) * 20 + 0];
-        acc_dbL[0] += v;
+        r_dbL += v;
       }
     }
+    // write this thread's slots (every element of the slot is owned by exactly one thread)
+    for (int l = 0; l <= L - 2; ++l) acc_db[(size_t)l * MPAD + m] = r_db[l];
+    acc_dWL[m] = r_dWL;
+    acc_dW0[m * 3 + 0] = r_dW0[0];
+    acc_dW0[m * 3 + 1] = r_dW0[1];
+    acc_dW0[m * 3 + 2] = r_dW0[2];
+    if (m == 0) acc_dbL[0] = r_dbL;
   }
   tc_teardown<C>(tbase);
 }
