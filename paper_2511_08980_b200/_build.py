@@ -13,6 +13,7 @@ BUILD = os.path.join(ROOT, "build")
 SOURCES = ["api.cu", "fwd.cu", "bwd.cu", "wgrad.cu", "tcprobe.cu", "fwd_tc.cu", "bwd_tc.cu", "wgrad_tc.cu", "train.cu"]
 HEADERS = ["common.cuh", "act.cuh", "tile.cuh", "kernels.cuh", "tc.cuh", "fdepi.cuh", "tcmlp.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("FDSDF_NVCC_EXTRA", "").split()  # debug builds only (e.g. -DFDSDF_PHASE_TIMING)
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-diag-suppress", "177"]
 
@@ -32,7 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *EXTRA, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log = os.path.join(BUILD, src.replace(".cu", ".ptxas.log"))
         with open(log, "w") as fh:

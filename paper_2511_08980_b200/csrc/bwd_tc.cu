@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     for (int l = 0; l < MAXL; ++l) r_db[l] = 0.f;
     float r_dWL = 0.f, r_dbL = 0.f, r_dW0[3] = {0.f, 0.f, 0.f};
     uint32_t nd = 0;
+    PhaseTimer ptimer;
+    ptimer.start();
     // the stored forward pre-activations of a tile are one contiguous block of zf
     auto prefetch_tile = [&](int64_t tile) {
       if (et == 0 && tile < a.ntiles) {
@@ -141,7 +143,9 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         };
         Zq qn = ldq(0);
         if (!top) {
+          ptimer.before_wait();
           mbar_wait(bars.dfull, nd & 1u);
+          ptimer.after_wait();
           ++nd;
           tc::fence_after();
         }
@@ -268,6 +272,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     acc_dW0[m * 3 + 1] = r_dW0[1];
     acc_dW0[m * 3 + 2] = r_dW0[2];
     if (m == 0) acc_dbL[0] = r_dbL;
+    ptimer.report("bwd_tc", et == 0);
   }
   tc_teardown<C>(tbase);
 }

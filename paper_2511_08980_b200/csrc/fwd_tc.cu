@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
     const float h = a.h;
     const bool step = a.step != 0;
     uint32_t nd = 0;
+    PhaseTimer ptimer;
+    ptimer.start();
     double lacc[NLOSS];
 #pragma unroll
     for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
@@ -177,7 +179,9 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
         };
         float z0n = ldz(0);
         if (l > 0) {
+          ptimer.before_wait();
           mbar_wait(bars.dfull, nd & 1u);
+          ptimer.after_wait();
           ++nd;
           tc::fence_after();
         }
@@ -336,6 +340,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
 #pragma unroll
       for (int q = 0; q < NLOSS; ++q) a.lossp[(size_t)blockIdx.x * NLOSS + q] = lacc[q];
     }
+    ptimer.report(MODE == 1 ? "fwd_tc centre" : "fwd_tc pairs", et == 0);
   }
 
   tc_teardown<C>(tbase);

@@ -14,6 +14,8 @@
 // Hand-offs: wfull/wempty (producer <-> MMA), bfull (8 epilogue warps -> MMA: B written and
 // the previous D fully read), dfull (MMA -> epilogue).
 #pragma once
+#include <cstdio>
+
 #include "tc.cuh"
 
 namespace fdsdf {
@@ -156,6 +158,39 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
       tc::mma_commit(b.dfull);
     }
 }
+
+// Debug-build phase timer (-DFDSDF_PHASE_TIMING): epilogue thread 0 of CTA 0 accumulates the
+// cycles it spends waiting for "D full" (the MMA phase as seen by the epilogue) and the cycles
+// between D full and its next hand-over (the epilogue phase), and prints them at kernel end.
+struct PhaseTimer {
+#ifdef FDSDF_PHASE_TIMING
+  long long t_mark = 0, wait = 0, work = 0, first = 0;
+  int n = 0;
+  __device__ __forceinline__ void start() { t_mark = first = clock64(); }
+  __device__ __forceinline__ void before_wait() {
+    const long long t = clock64();
+    work += t - t_mark;
+    t_mark = t;
+  }
+  __device__ __forceinline__ void after_wait() {
+    const long long t = clock64();
+    wait += t - t_mark;
+    t_mark = t;
+    ++n;
+  }
+  __device__ __forceinline__ void report(const char* name, bool who) {
+    if (who && blockIdx.x == 0)
+      printf("[phase] %s: total %lld cyc, waiting for D %lld (%.1f%%), epilogue %lld, %d waits, %.0f cyc/wait\n",
+             name, clock64() - first, wait, 100.0 * wait / (double)(clock64() - first), work, n,
+             n ? (double)wait / n : 0.0);
+  }
+#else
+  __device__ __forceinline__ void start() {}
+  __device__ __forceinline__ void before_wait() {}
+  __device__ __forceinline__ void after_wait() {}
+  __device__ __forceinline__ void report(const char*, bool) {}
+#endif
+};
 
 // epilogue warp: the B operand of the next GEMM is complete (this warp's rows), and its
 // reads of the previous D are finished -> hand over to the MMA thread
