@@ -116,11 +116,16 @@ __device__ __forceinline__ void sincos_acc(float x, float* s, float* c) {
   *c = cv;
 }
 
-// sincos_acc for the small arguments of the pair maps (A/2, S/4): |x| <= pi/4 needs no range
-// reduction (k = 0, r = x), so the polynomial alone gives bit-identical results; larger |x|
-// (rare) take the full path.
+// sincos for the small arguments of the pair maps (A/2, S/4): most are below 2^-4, where a
+// short Taylor polynomial is exact to fp32 rounding; |x| <= pi/4 needs no range reduction
+// (k = 0, r = x: the sincos_acc polynomial alone); larger |x| (rare) take the full path.
 __device__ __forceinline__ void sincos_small(float x, float* s, float* c) {
-  if (fabsf(x) <= 0.78539816339744831f) {
+  if (fabsf(x) <= 0.0625f) {
+    // |x| <= 2^-4: Taylor to x^5 / x^6; truncation <= x^7/5040 < 1e-12 |x|, below fp32 rounding
+    const float z = x * x;
+    *s = fmaf(-x * z, fmaf(z, -8.3333333333e-3f, 1.6666666667e-1f), x);
+    *c = fmaf(z, fmaf(z, fmaf(z, -1.3888888889e-3f, 4.1666666667e-2f), -0.5f), 1.0f);
+  } else if (fabsf(x) <= 0.78539816339744831f) {
     const float z = x * x;
     float ps = fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f);
     ps = fmaf(ps * z, x, x);
