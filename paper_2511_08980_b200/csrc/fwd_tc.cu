@@ -34,9 +34,13 @@ template <int MPAD>
 struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI> {
   using B = TcCfg<MPAD, 64, FWD_TC_NEPI>;
   static constexpr int MAXC = 16;                                   // max centres per tile
-  static constexpr int OFF_RED = B::OFF_X;                          // float [NEPI][MAXC][4]
-  static constexpr int OFF_CI = OFF_RED + B::NEPI * MAXC * 4 * 4;   // float [MAXC][16]
-  static constexpr int OFF_LV = OFF_CI + MAXC * NCINFO * 4;         // double [MAXC][NLOSS]
+  // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
+  // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
+  static constexpr int RED_N = B::NEPI * MAXC * 4;                  // floats per buffer
+  static constexpr int CI_N = MAXC * NCINFO;                        // floats per buffer
+  static constexpr int OFF_RED = B::OFF_X;                          // float [2][NEPI][MAXC][4]
+  static constexpr int OFF_CI = OFF_RED + 2 * RED_N * 4;            // float [2][MAXC][16]
+  static constexpr int OFF_LV = OFF_CI + 2 * CI_N * 4;              // double [MAXC][NLOSS]
   static constexpr int OFF_BAR = OFF_LV + MAXC * NLOSS * 8;         // mbarriers + TMEM slot
   static constexpr int BYTES = OFF_BAR + tc_bars_bytes<B>() + 1024; // + alignment slack
 };
@@ -101,8 +105,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
   sm += (1024 - (smem_u32(sm) & 1023)) & 1023;
   unsigned char* Ws = sm + C::OFF_W;
   unsigned char* Bs = sm + C::OFF_B;
-  float* red = reinterpret_cast<float*>(sm + C::OFF_RED);
-  float* cis = reinterpret_cast<float*>(sm + C::OFF_CI);
+  float* red0 = reinterpret_cast<float*>(sm + C::OFF_RED);
+  float* cis0 = reinterpret_cast<float*>(sm + C::OFF_CI);
   double* lvs = reinterpret_cast<double*>(sm + C::OFF_LV);
   const TcBars bars = tc_bars<C>(sm + C::OFF_BAR);
 
@@ -142,8 +146,53 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
     };
     auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
 
-    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    // per-centre epilogue of a finished tile (warp 2 only: et < CT <= 16): mode 1 -> f, g, mask,
+    // frame, cinfo; mode 2 -> FD entries, D, K, Eq. (1) terms, seeds, and the fixed-order
+    // fp64 accumulation of the tile's loss terms
+    auto finish = [&](int64_t fc0, const float* red, float* cis) {
+      if (et < CT) {
+        const int cl = et;
+        const int64_t c = fc0 + cl;
+        const bool valid = c < a.n;
+        float tot[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float v = 0.f;
+          for (int w = 0; w < C::NEPI; ++w)
+            if ((w / (4 * MH)) == (cl % C::EG)) v += red[(w * C::MAXC + cl) * 4 + j];
+          tot[j] = v;
+        }
+        if (MODE == 1) {
+          float* ci = cis + cl * NCINFO;
+          centre_frame(a, c, valid, tot[0] + net.b[L - 1][0], tot[1], tot[2], tot[3], ci);
+          if (valid) {
+#pragma unroll
+            for (int q = 0; q < NCINFO; ++q) a.cinfo[c * NCINFO + q] = ci[q];
+          }
+        } else {
+          double lv[NLOSS];
+          fd_centre(a, c, valid, tot, cis + cl * NCINFO, lv);
+#pragma unroll
+          for (int q = 0; q < NLOSS; ++q) lvs[cl * NLOSS + q] = lv[q];
+        }
+      }
+      __syncwarp();
+      if (MODE == 2 && et == 0) {  // fixed-order tile reduction of the loss terms
+        for (int s2 = 0; s2 < CT; ++s2)
+#pragma unroll
+          for (int q = 0; q < NLOSS; ++q) lacc[q] += lvs[s2 * NLOSS + q];
+      }
+    };
+    bool pending = false;
+    int64_t pend_c0 = 0;
+    const float* pend_red = nullptr;
+    float* pend_cis = nullptr;
+    uint32_t tpar = 0;
+
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, tpar ^= 1u) {
       const int64_t c0 = tile * CT;
+      float* red = red0 + tpar * C::RED_N;
+      float* cis = cis0 + tpar * C::CI_N;
       if (MODE == 2) {  // the tile's centre info (f, g, frame, mask) from mode 1
         for (int i = et; i < CT * NCINFO; i += C::NEPI * 32) {
           const int64_t c = c0 + i / NCINFO;
@@ -300,42 +349,19 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
         } else if (l > 0) {
           tc::fence_before();
         }
+        if (l == 0 && pending) {  // the previous tile's per-centre work, overlapping the MMA phase
+          if (ew == 0) finish(pend_c0, pend_red, pend_cis);
+          pending = false;
+        }
       }
 
-      bar_named(1, C::NEPI * 32);
-      if (et < CT) {
-        const int cl = et;
-        const int64_t c = c0 + cl;
-        const bool valid = c < a.n;
-        float tot[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float v = 0.f;
-          for (int w = 0; w < C::NEPI; ++w)
-            if ((w / (4 * MH)) == (cl % C::EG)) v += red[(w * C::MAXC + cl) * 4 + j];
-          tot[j] = v;
-        }
-        if (MODE == 1) {
-          float* ci = cis + cl * NCINFO;
-          centre_frame(a, c, valid, tot[0] + net.b[L - 1][0], tot[1], tot[2], tot[3], ci);
-          if (valid) {
-#pragma unroll
-            for (int q = 0; q < NCINFO; ++q) a.cinfo[c * NCINFO + q] = ci[q];
-          }
-        } else {
-          double lv[NLOSS];
-          fd_centre(a, c, valid, tot, cis + cl * NCINFO, lv);
-#pragma unroll
-          for (int q = 0; q < NLOSS; ++q) lvs[cl * NLOSS + q] = lv[q];
-        }
-      }
-      bar_named(1, C::NEPI * 32);
-      if (MODE == 2 && et == 0) {  // fixed-order tile reduction of the loss terms
-        for (int s2 = 0; s2 < CT; ++s2)
-#pragma unroll
-          for (int q = 0; q < NLOSS; ++q) lacc[q] += lvs[s2 * NLOSS + q];
-      }
+      bar_named(1, C::NEPI * 32);  // this tile's last-layer partial sums are complete
+      pending = true;
+      pend_c0 = c0;
+      pend_red = red;
+      pend_cis = cis;
     }
+    if (pending && ew == 0) finish(pend_c0, pend_red, pend_cis);
     if (MODE == 2 && et == 0) {
 #pragma unroll
       for (int q = 0; q < NLOSS; ++q) a.lossp[(size_t)blockIdx.x * NLOSS + q] = lacc[q];
