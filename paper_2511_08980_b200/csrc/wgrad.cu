@@ -148,6 +148,21 @@ cudaError_t launch_wgrad(const WgradArgs& a, int nglayers, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------------------------- finalize
+// sum_{s < n} p[s * stride] in the fixed order s = 0, 1, ..., with 8 loads in flight
+__device__ __forceinline__ float sum_strided(const float* __restrict__ p, int64_t stride, int n) {
+  float v = 0.f;
+  int s = 0;
+  for (; s + 8 <= n; s += 8) {
+    float t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = __ldg(p + (size_t)(s + q) * stride);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += t[q];
+  }
+  for (; s < n; ++s) v += __ldg(p + (size_t)s * stride);
+  return v;
+}
+
 // grid.y = layer (0..L-1), plus one extra block row for the loss.
 __global__ void finalize_kernel(const FinArgs a) {
   const Net& net = a.net;
@@ -196,21 +211,21 @@ __global__ void finalize_kernel(const FinArgs a) {
     if (idx < nW) {
       const int m = (int)(idx / K), k = (int)(idx % K);
       if (l == L - 1) {
-        for (int c = 0; c < a.nbcta; ++c) v += a.bacc[(size_t)c * a.nacc + oWL + k];
+        v = sum_strided(a.bacc + oWL + k, a.nacc, a.nbcta);
       } else if (l == 0) {
-        for (int c = 0; c < a.nbcta; ++c) v += a.bacc[(size_t)c * a.nacc + oW0 + m * 3 + k];
+        v = sum_strided(a.bacc + oW0 + m * 3 + k, a.nacc, a.nbcta);
       } else {
         const float* p = a.part + (size_t)(l - 1) * a.nsplit * mp * mp + (size_t)m * mp + k;
-        for (int s = 0; s < a.nsplit; ++s) v += p[(size_t)s * mp * mp];
+        v = sum_strided(p, (int64_t)mp * mp, a.nsplit);
       }
       if (a.accumulate) v += gW[idx];
       gW[idx] = v;
     } else {
       const int m = (int)(idx - nW);
       if (l == L - 1) {
-        for (int c = 0; c < a.nbcta; ++c) v += a.bacc[(size_t)c * a.nacc + obL];
+        v = sum_strided(a.bacc + obL, a.nacc, a.nbcta);
       } else {
-        for (int c = 0; c < a.nbcta; ++c) v += a.bacc[(size_t)c * a.nacc + (size_t)l * mp + m];
+        v = sum_strided(a.bacc + (size_t)l * mp + m, a.nacc, a.nbcta);
       }
       if (a.accumulate) v += gb[m];
       gb[m] = v;
@@ -219,7 +234,8 @@ __global__ void finalize_kernel(const FinArgs a) {
 }
 
 cudaError_t launch_finalize(const FinArgs& a, cudaStream_t st) {
-  dim3 grid(64, a.net.L + 1);
+  const int mp = a.net.mpad;
+  dim3 grid(std::max(64, (mp * mp + mp + 255) / 256), a.net.L + 1);
   finalize_kernel<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }

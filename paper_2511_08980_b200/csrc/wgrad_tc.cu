@@ -10,7 +10,7 @@
 //   warp 0      TMEM owner + MMA issuer (one thread): per 32-wide j chunk, 2 K-steps x
 //               M-halves x 6 piece products, tcgen05.mma kind::f16 with BOTH operands
 //               MN-major (delta and a are stored j-major, m / k contiguous);
-//   warps 1..8  stagers: read the fp32 chunk of delta_l and a_{l-1} (float4, coalesced), split
+//   warps 1..16 stagers: read the fp32 chunk of delta_l and a_{l-1} (float4, coalesced), split
 //               every value into 3 bf16 pieces and store them in the MN-major SWIZZLE_128B
 //               layout of a 2-deep ring (8-byte st.shared per piece); after the last chunk of
 //               a layer they read the accumulator back (tcgen05.ld) and write the partial.
@@ -28,7 +28,7 @@ struct WtcCfg {
   static constexpr int STAGE = 2 * OPER;            // delta chunk + a chunk
   static constexpr int NST = 2;
   static constexpr int KSTRIDE = (MPAD / 64) * 1024;  // byte stride between swizzle atoms along K
-  static constexpr int NSTG = 8;                    // stager warps
+  static constexpr int NSTG = 16;                   // stager warps
   static constexpr int NTHR = (1 + NSTG) * 32;
   static constexpr int OFF_BAR = NST * STAGE;
   static constexpr int BYTES = OFF_BAR + 64 + 1024;
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
     }
   } else {
     // ------------------------------------------------------------------ stagers + readback
-    const int sw = warp - 1;        // 0..7
+    const int sw = warp - 1;        // 0 .. NSTG-1
     const int st = tid - 32;        // 0..255
     uint32_t it = 0;
     constexpr int QUADS = MPAD / 4;  // float4 per j row
@@ -156,11 +156,11 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
         __syncwarp();
         if (lane == 0) mbar_arrive(&sfull[s]);
       }
-      // readback of this layer's partial: warp sw -> lane quarter sw % 4, halves (sw / 4) + 2i
+      // readback of this layer's partial: warp sw -> lane quarter (warp % 4), halves (sw / 4) + 4i
       mbar_wait(dfull, 0u);
       tc::fence_after();
       float* out = a.part + ((size_t)li * a.nsplit + split) * MPAD * MPAD;
-      for (int h = sw >> 2; h < MH; h += 2) {
+      for (int h = sw >> 2; h < MH; h += C::NSTG / 4) {
         const int q4 = (warp & 3);
         const int m = h * 128 + 32 * q4 + lane;
         const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + h * MPAD;
