@@ -276,6 +276,10 @@ const char* fdsdf_version(void);
  * launch failure -> FDSDF_E_CUDA.  Test/diagnostic use only (not on the hot path). */
 fdsdf_status fdsdf_selftest_mma(const float* d_W, const float* d_B, float* d_D, int M, int N, int K,
                                 int nprod, int mn_major, void* stream);
+/* The same bf16x6 GEMM on a CTA pair (cluster of 2, tcgen05 cta_group::2, M = 256): D [256][N]
+ * = d_W [256][K] . d_B [N][K]^T; N a multiple of 32 in [32, 256], K a multiple of 64.
+ * Errors as fdsdf_selftest_mma.  Test/diagnostic use only. */
+fdsdf_status fdsdf_selftest_mma_pair(const float* d_W, const float* d_B, float* d_D, int N, int K, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,481 @@
+// fwd_tc2.cu -- the tensor-core forward on CTA pairs (tcgen05 cta_group::2) with two half-tile
+// slots in flight (tcpair.cuh).  Same arithmetic as fwd_tc.cu (modes 1 and 2, bf16x6, the
+// cancellation-free pair maps, fdepi.cuh epilogues); what changes is the schedule:
+//   * a pair tile = 2 slots of CPS centres (mode 1: 16 centres x 4 columns, mode 2: 8 centres
+//     x 8 pair columns); each slot is a 64-column GEMM on the pair (M = 256 over 2 SMs);
+//   * per layer the leader issues slot 0's MMAs, then slot 1's, while the 16 epilogue warps of
+//     each CTA process the other slot -- the MMA phase of one slot overlaps the epilogue of the
+//     other (the single-CTA kernels serialise them);
+//   * each CTA streams only its 128 weight rows: 192 KB per slot-layer instead of 384 KB;
+//   * the last-layer sums over the 256 neurons are reduced across the pair through distributed
+//     shared memory into the CTA that owns the centre, whose first epilogue warp runs the
+//     per-centre epilogue (frame / FD, Eq. (1) terms, seeds) during the next tile's first MMA
+//     phase.
+// Used for 256-padded widths (C2, C4, C5); the single-CTA kernels keep C1.
+#include "act.cuh"
+#include "fdepi.cuh"
+#include "tcmlp.cuh"
+#include "tcpair.cuh"
+
+namespace fdsdf {
+
+template <int MODE>
+struct F2Cfg {
+  static constexpr int MPAD = 256;
+  static constexpr int KC = 4;                          // K chunks of 64
+  static constexpr int NS = 64;                         // columns per slot (pair-wide)
+  static constexpr int NH = 32;                         // columns per slot per CTA
+  static constexpr int CPC = MODE == 1 ? 4 : 8;         // columns per centre
+  static constexpr int CPS = NS / CPC;                  // centres per slot (16 / 8)
+  static constexpr int COWN = NH / CPC;                 // centres per slot owned by one CTA
+  static constexpr int STAGE = 3 * 128 * 128;           // weight stage: this CTA's 128 rows
+  static constexpr int NST = 2;
+  static constexpr int BSLOT = KC * 3 * NH * 128;       // B block of one slot in one CTA
+  static constexpr int NEPI = 16;
+  static constexpr int NTHR = (2 + NEPI) * 32;
+  static constexpr int CPT = CPS / 4;                   // centres per epilogue thread per slot
+  static constexpr int NRED = 8 * CPS * 4;              // floats per (parity, slot) reduction block
+  static constexpr int OFF_W = 0;
+  static constexpr int OFF_B = NST * STAGE;
+  static constexpr int OFF_RED = OFF_B + 2 * BSLOT;     // float [2 par][2 slot][8 grp][CPS][4]
+  static constexpr int OFF_CI = OFF_RED + 4 * NRED * 4; // float [2 par][2 slot][CPS][16]
+  static constexpr int OFF_LV = OFF_CI + 4 * CPS * NCINFO * 4;
+  static constexpr int OFF_BAR = OFF_LV + 2 * CPS * NLOSS * 8;
+  static constexpr int NBAR = 2 * NST + NST + 2 + 2 + 4;  // wfull, wempty, wpeer, bfull, dfull, rfull
+  static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;
+  static constexpr uint32_t TCOLS = 2 * NS <= 128 ? 128 : 256;
+};
+
+int fwd_tc2_tile_centres(int mode) { return mode == 1 ? 32 : 16; }
+
+template <int ACT, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1)
+    fwd_tc2_kernel(const FwdArgs a) {
+  using C = F2Cfg<MODE>;
+  using AF = Act<ACT>;
+  constexpr int MPAD = C::MPAD, NS = C::NS, NH = C::NH, CPS = C::CPS, CPC = C::CPC, CPT = C::CPT;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = smem_raw;
+  sm += (1024 - (smem_u32(sm) & 1023)) & 1023;
+  unsigned char* Ws = sm + C::OFF_W;
+  unsigned char* Bs = sm + C::OFF_B;
+  float* red0 = reinterpret_cast<float*>(sm + C::OFF_RED);
+  float* cis0 = reinterpret_cast<float*>(sm + C::OFF_CI);
+  double* lvs = reinterpret_cast<double*>(sm + C::OFF_LV);
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* wempty = wfull + C::NST;
+  uint64_t* wpeer = wempty + C::NST;
+  uint64_t* bfull = wpeer + C::NST;
+  uint64_t* dfull = bfull + 2;
+  uint64_t* rfull = dfull + 2;  // [par][slot]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rfull + 4);
+
+  const Net& net = a.net;
+  const int L = net.L;
+  const int nh = L - 1;
+  const int ngemm = L - 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tp::ctarank();
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
+      mbar_init(&wpeer[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bfull[s], 2 * C::NEPI);
+      mbar_init(&dfull[s], 1);
+    }
+    for (int s = 0; s < 4; ++s) mbar_init(&rfull[s], 2 * C::NEPI);
+    fence_mbar_init();
+  }
+  if (warp == 1) tp::tmem_alloc2(tslot, C::TCOLS);
+  tc::fence_before();
+  tp::cluster_sync();
+  tc::fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ weight producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t tile = cid; tile < a.ntiles; tile += ncl)
+        for (int g = 0; g < ngemm; ++g)
+          for (int slot = 0; slot < 2; ++slot)
+            for (int kc = 0; kc < C::KC; ++kc, ++it) {
+              const int s = (int)(it % C::NST);
+              mbar_wait(&wempty[s], ((it / C::NST) & 1u) ^ 1u);
+              mbar_arrive_expect_tx(&wfull[s], C::STAGE);
+              bulk_g2s(Ws + s * C::STAGE, a.wimg + (((size_t)g * C::KC + kc) * 2 + rank) * C::STAGE, C::STAGE,
+                       &wfull[s]);
+            }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------------------------------------------------------- MMA issuer (leader)
+      constexpr uint32_t idesc = tc::idesc_bf16(256, NS);
+      uint32_t it = 0, nb[2] = {0u, 0u};
+      for (int64_t tile = cid; tile < a.ntiles; tile += ncl)
+        for (int g = 0; g < ngemm; ++g)
+          for (int slot = 0; slot < 2; ++slot) {
+            tp::wait_cluster(&bfull[slot], nb[slot] & 1u);
+            ++nb[slot];
+            tc::fence_after();
+            const uint32_t bslot = smem_u32(Bs + slot * C::BSLOT);
+            for (int kc = 0; kc < C::KC; ++kc, ++it) {
+              const int s = (int)(it % C::NST);
+              const uint32_t ph = (it / C::NST) & 1u;
+              mbar_wait(&wfull[s], ph);
+              tp::wait_cluster(&wpeer[s], ph);
+              tc::fence_after();
+              const uint32_t wa = smem_u32(Ws + s * C::STAGE);
+              const uint32_t ba = bslot + kc * (3 * NH * 128);
+#pragma unroll
+              for (int sub = 0; sub < 4; ++sub)
+#pragma unroll
+                for (int q = 0; q < 6; ++q)
+                  tp::mma2(tbase + slot * NS, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
+                           tc::sdesc_sw128(ba + tc::prod_b(q) * NH * 128 + sub * 32), idesc,
+                           (kc | sub | q) != 0 ? 1u : 0u);
+              tp::commit2(&wempty[s]);
+            }
+            tp::commit2(&dfull[slot]);
+          }
+    } else if (lane == 0 && rank == 1) {
+      // ---------------------------------------------------------------- stage forwarder (peer)
+      uint32_t it = 0;
+      const uint32_t wpeer_leader = tp::mapa(smem_u32(wpeer), 0);
+      for (int64_t tile = cid; tile < a.ntiles; tile += ncl)
+        for (int g = 0; g < ngemm; ++g)
+          for (int slot = 0; slot < 2; ++slot)
+            for (int kc = 0; kc < C::KC; ++kc, ++it) {
+              const int s = (int)(it % C::NST);
+              mbar_wait(&wfull[s], (it / C::NST) & 1u);
+              tp::arrive_cluster(wpeer_leader + s * 8);
+            }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue warps
+    const int ew = warp - 2;                          // 0..15
+    const int et = tid - 64;                          // 0..511
+    const int q4 = warp & 3;                          // TMEM lane quarter
+    const int eg = ew >> 2;                           // centre group 0..3
+    const int ml = 32 * q4 + lane;                    // neuron within this CTA's half
+    const int m = 128 * (int)rank + ml;               // output neuron (= next layer's K index)
+    const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
+    const float beta = net.beta;
+    const float h = a.h;
+    const bool step = a.step != 0;
+    const uint32_t bs_c[2] = {tp::mapa(smem_u32(Bs), 0), tp::mapa(smem_u32(Bs), 1)};
+    const uint32_t red_c[2] = {tp::mapa(smem_u32(red0), 0), tp::mapa(smem_u32(red0), 1)};
+    const uint32_t rfull_c[2] = {tp::mapa(smem_u32(rfull), 0), tp::mapa(smem_u32(rfull), 1)};
+    const uint32_t bfull_leader = tp::mapa(smem_u32(bfull), 0);
+    uint32_t nd[2] = {0u, 0u}, rph[4] = {0u, 0u, 0u, 0u};
+    PhaseTimer ptimer;
+    ptimer.start();
+    double lacc[NLOSS];
+#pragma unroll
+    for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
+
+    auto zp = [&](int64_t c, int l, int col) -> float* {
+      return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
+    };
+
+    // per-centre epilogue of the centres this CTA owns in (tile base c0, parity par)
+    auto finish = [&](int64_t c0, int par) {
+      if (ew == 0) {
+        for (int slot = 0; slot < 2; ++slot) {
+          tp::wait_cluster(&rfull[par * 2 + slot], rph[par * 2 + slot] & 1u);
+          ++rph[par * 2 + slot];
+        }
+        if (et < 2 * C::COWN) {
+          const int slot = et / C::COWN;
+          const int cl = (int)rank * C::COWN + et % C::COWN;  // centre within the slot
+          const int64_t c = c0 + slot * CPS + cl;
+          const bool valid = c < a.n;
+          const float* red = red0 + (par * 2 + slot) * C::NRED;
+          float tot[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float v = 0.f;
+            for (int grp = 0; grp < 8; ++grp) v += red[(grp * CPS + cl) * 4 + j];
+            tot[j] = v;
+          }
+          float* ci = cis0 + ((par * 2 + slot) * CPS + cl) * NCINFO;
+          if (MODE == 1) {
+            centre_frame(a, c, valid, tot[0] + net.b[L - 1][0], tot[1], tot[2], tot[3], ci);
+            if (valid) {
+#pragma unroll
+              for (int q = 0; q < NCINFO; ++q) a.cinfo[c * NCINFO + q] = ci[q];
+            }
+          } else {
+            double lv[NLOSS];
+            fd_centre(a, c, valid, tot, ci, lv);
+#pragma unroll
+            for (int q = 0; q < NLOSS; ++q) lvs[et * NLOSS + q] = lv[q];
+          }
+        }
+        __syncwarp();
+        if (MODE == 2 && et == 0) {  // fixed order: slot 0 centres, then slot 1
+          for (int s2 = 0; s2 < 2 * C::COWN; ++s2)
+#pragma unroll
+            for (int q = 0; q < NLOSS; ++q) lacc[q] += lvs[s2 * NLOSS + q];
+        }
+      }
+    };
+
+    bool pending = false;
+    int64_t pend_c0 = 0;
+    int pend_par = 0, par = 0;
+    for (int64_t tile = cid; tile < a.ntiles; tile += ncl, par ^= 1) {
+      const int64_t c0 = tile * 2 * CPS;
+      float* cisp = cis0 + par * 2 * CPS * NCINFO;
+      if (MODE == 2) {  // both slots' centre info (frames) from the centre kernel
+        for (int i = et; i < 2 * CPS * NCINFO; i += C::NEPI * 32) {
+          const int64_t c = c0 + i / NCINFO;
+          cisp[i] = c < a.n ? a.cinfo[c * NCINFO + (i % NCINFO)] : 0.f;
+        }
+      }
+      bar_named(1, C::NEPI * 32);
+
+      for (int l = 0; l <= L - 2; ++l) {
+        const bool last = (l == L - 2);
+        const int M = net.width[l + 1];
+        const float om = net.omega[l];
+        const bool mok = m < M;
+        const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
+        for (int slot = 0; slot < 2; ++slot) {
+          const int64_t cs = c0 + slot * CPS;
+          const uint32_t bslot_off = slot * C::BSLOT;
+          // the pre-activations the backward needs, stored AFTER the hand-off below: the proxy
+          // fence before it (MEMBAR at cluster scope) would otherwise wait for these stores
+          float zst[CPT][8];
+          float z0n[CPT];
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const int64_t c = cs + eg + 4 * i;
+            z0n[i] = (MODE == 2 && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
+          }
+          if (l > 0) {
+            ptimer.before_wait();
+            mbar_wait(&dfull[slot], nd[slot] & 1u);
+            ptimer.after_wait();
+            ++nd[slot];
+            tc::fence_after();
+          }
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const int cl = eg + 4 * i;           // centre within the slot
+            const int64_t c = cs + cl;
+            const bool valid = c < a.n;
+            const int owner = (cl * CPC) / NH;  // CTA holding this centre's columns
+            const int nl0 = (cl * CPC) % NH;    // its first local column there
+            float outv[8];
+            int nout;
+            if (MODE == 1) {
+              float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
+              if (l == 0) {
+                float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+                if (valid) {
+                  x0 = a.x[c * 3 + 0];
+                  x1 = a.x[c * 3 + 1];
+                  x2 = a.x[c * 3 + 2];
+                  if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
+                }
+                if (mok) {
+                  const float* W0 = net.W[0];
+                  const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+                  z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + net.b[0][m]);
+                  t0 = om * w0;
+                  t1 = om * w1;
+                  t2 = om * w2;
+                }
+              } else {
+                float v[8];
+                tc::tmem_ld8(tl + slot * NS + (uint32_t)((cl >> 1) * 8), v);
+                const int o = (cl & 1) * 4;
+                if (mok) {
+                  z = om * (v[o] + net.b[l][m]);
+                  t0 = om * v[o + 1];
+                  t1 = om * v[o + 2];
+                  t2 = om * v[o + 3];
+                }
+              }
+              zst[i][0] = z;
+              zst[i][1] = t0;
+              zst[i][2] = t1;
+              zst[i][3] = t2;
+              float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+              if (mok) {
+                const typename AF::C cc = AF::centre(z, beta);
+                const float s1 = AF::d1(cc, beta);
+                o0 = AF::value(cc, beta);
+                o1 = s1 * t0;
+                o2 = s1 * t1;
+                o3 = s1 * t2;
+              }
+              outv[0] = o0;
+              outv[1] = o1;
+              outv[2] = o2;
+              outv[3] = o3;
+              nout = 4;
+            } else {
+              const float* ci = cisp + (slot * CPS + cl) * NCINFO;
+              float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
+              if (l == 0) {
+                if (mok) {
+                  const float* W0 = net.W[0];
+                  const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+                  const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
+                  const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
+                  const float hs = om * h;
+                  Av[0] = hs * du;
+                  Av[1] = hs * dv;
+                  Av[2] = hs * (du + dv);
+                  Av[3] = hs * (du - dv);
+                }
+              } else {
+                float v[8];
+                tc::tmem_ld8(tl + slot * NS + (uint32_t)(cl * 8), v);
+                if (mok) {
+#pragma unroll
+                  for (int p = 0; p < 4; ++p) {
+                    Av[p] = om * v[2 * p];
+                    Sv[p] = om * v[2 * p + 1];
+                  }
+                }
+              }
+              const float z0 = z0n[i];
+#pragma unroll
+              for (int p = 0; p < 4; ++p) {
+                zst[i][2 * p] = Av[p];
+                zst[i][2 * p + 1] = Sv[p];
+              }
+#pragma unroll
+              for (int p = 0; p < 8; ++p) outv[p] = 0.f;
+              if (mok) {
+                const typename AF::C cc = AF::centre(z0, beta);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &outv[2 * p], &outv[2 * p + 1]);
+              }
+              nout = 8;
+            }
+            if (!last) {
+              if (owner == (int)rank) {
+                unsigned char* bsl = Bs + bslot_off;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if (j < nout) tp::put_b_local<NH>(bsl, nl0 + j, m, outv[j]);
+              } else {
+                const uint32_t bsl = bs_c[owner] + bslot_off;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if (j < nout) tp::put_b<NH>(bsl, nl0 + j, m, outv[j]);
+              }
+            } else {
+              // last layer: this warp's 32-neuron sums of w_L * (values), into the owner's block
+              float pv[4];
+              if (MODE == 1) {
+                pv[0] = wl * outv[0];
+                pv[1] = wl * outv[1];
+                pv[2] = wl * outv[2];
+                pv[3] = wl * outv[3];
+              } else {
+                pv[0] = wl * outv[1];
+                pv[1] = wl * outv[3];
+                pv[2] = wl * outv[5];
+                pv[3] = wl * outv[7];
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                float v = pv[j];
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                if (lane == 0) {
+                  const int grp = (int)rank * 4 + q4;
+                  tp::st_f32(red_c[owner] + (uint32_t)((((par * 2 + slot) * 8 + grp) * CPS + cl) * 4 + j) * 4, v);
+                }
+              }
+            }
+          }
+          if (!last) {  // B of (slot, l+1) written (this warp's part): hand over to the leader's MMA
+            tc::fence_before();
+            tp::fence_proxy_async_cluster();
+            __syncwarp();
+            if (lane == 0) tp::arrive_cluster(bfull_leader + slot * 8);
+          } else {
+            if (l > 0) tc::fence_before();
+            __syncwarp();
+            if (lane == 0) {  // partial sums in place (both owners)
+              tp::arrive_cluster(rfull_c[0] + (par * 2 + slot) * 8);
+              tp::arrive_cluster(rfull_c[1] + (par * 2 + slot) * 8);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {  // the deferred pre-activation stores
+            const int64_t c = cs + eg + 4 * i;
+            if (c < a.n) {
+              if (MODE == 1) {
+                *zp(c, l, 0) = zst[i][0];
+                if (step) {
+                  *zp(c, l, 1) = zst[i][1];
+                  *zp(c, l, 2) = zst[i][2];
+                  *zp(c, l, 3) = zst[i][3];
+                }
+              } else if (step) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) *zp(c, l, 4 + q) = zst[i][q];
+              }
+            }
+          }
+          if (l == 0 && slot == 1 && pending) {  // previous tile's per-centre work, during this MMA phase
+            finish(pend_c0, pend_par);
+            pending = false;
+          }
+        }
+      }
+      pending = true;
+      pend_c0 = c0;
+      pend_par = par;
+    }
+    if (pending) finish(pend_c0, pend_par);
+    ptimer.report(MODE == 1 ? "fwd_tc2 centre" : "fwd_tc2 pairs", et == 0 && rank == 0);
+    if (MODE == 2 && et == 0) {
+#pragma unroll
+      for (int q = 0; q < NLOSS; ++q) a.lossp[(size_t)blockIdx.x * NLOSS + q] = lacc[q];
+    }
+  }
+
+  tc::fence_before();
+  tp::cluster_sync();
+  if (warp == 1) tp::tmem_dealloc2(tbase, C::TCOLS);
+}
+
+template <int ACT, int MODE>
+static cudaError_t launch_fwd_tc2_t(const FwdArgs& a, int grid, cudaStream_t st) {
+  using C = F2Cfg<MODE>;
+  auto k = fwd_tc2_kernel<ACT, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  if (e != cudaSuccess) return e;
+  k<<<grid, C::NTHR, C::BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
+// grid: an even number of CTAs (clusters of 2)
+cudaError_t launch_fwd_tc2(const FwdArgs& a, int mode, int grid, cudaStream_t st) {
+  const int act = a.net.act;
+  if (a.net.mpad != 256 || a.net.L < 3) return cudaErrorInvalidValue;
+  if (act == ACT_SINE && mode == 1) return launch_fwd_tc2_t<ACT_SINE, 1>(a, grid, st);
+  if (act == ACT_SINE && mode == 2) return launch_fwd_tc2_t<ACT_SINE, 2>(a, grid, st);
+  if (act == ACT_SOFTPLUS && mode == 1) return launch_fwd_tc2_t<ACT_SOFTPLUS, 1>(a, grid, st);
+  if (act == ACT_SOFTPLUS && mode == 2) return launch_fwd_tc2_t<ACT_SOFTPLUS, 2>(a, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fdsdf

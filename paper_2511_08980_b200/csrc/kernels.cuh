@@ -129,6 +129,9 @@ size_t tc_wimg_bytes(int mpad, int ngemm);          // one packed weight image (
 cudaError_t launch_pack_tc(const Net& net, unsigned char* fwd_img, unsigned char* bwd_img, cudaStream_t st);
 cudaError_t launch_fwd_tc(const FwdArgs& a, int mode, int grid, cudaStream_t st);
 int fwd_tc_tile_centres(int mode);                  // 16 (mode 1) / 8 (mode 2)
+// CTA-pair variants (fwd_tc2.cu): mpad 256, L >= 3; grid = 2 x clusters
+cudaError_t launch_fwd_tc2(const FwdArgs& a, int mode, int grid, cudaStream_t st);
+int fwd_tc2_tile_centres(int mode);                 // 32 (mode 1) / 16 (mode 2) per pair tile
 cudaError_t launch_bwd_tc(const BwdArgs& a, int grid, cudaStream_t st);
 int bwd_tc_tile_centres();                          // 8
 int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA

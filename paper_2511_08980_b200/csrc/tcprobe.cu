@@ -117,3 +117,117 @@ extern "C" fdsdf_status fdsdf_selftest_mma(const float* d_W, const float* d_B, f
   tcprobe_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(d_W, d_B, d_D, M, N, K, nprod, mn_major);
   return cudaGetLastError() == cudaSuccess ? FDSDF_OK : FDSDF_E_CUDA;
 }
+
+// ----------------------------------------------------------------------------- CTA-pair probe
+// D[256][N] = W[256][K] . B[N][K]^T on a CTA pair (cluster of 2, tcgen05 cta_group::2):
+// CTA r stages W rows [128 r, 128 r + 128) and B rows [N/2 r, N/2 (r + 1)) (bf16x3 pieces,
+// K-major SW128) at the SAME shared-memory offsets; the leader (rank 0) issues M = 256 MMAs
+// that read both CTAs' operands; the commit is multicast to both CTAs' mbarriers; each CTA
+// reads its own 128 TMEM lanes (rows 128 r ..) back.  Validates the pair mechanics used by the
+// pair-tiled kernels.
+namespace fdsdf {
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    tcprobe2_kernel(const float* __restrict__ W, const float* __restrict__ B, float* __restrict__ D, int N, int K) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw;
+  base += (1024 - (smem_u32(base) & 1023)) & 1023;
+  const int NH = N / 2;
+  unsigned char* As = base;                 // [3][128 rows x 128 B]
+  unsigned char* Bs = As + 3 * 128 * 128;   // [3][NH rows x 128 B]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + 3 * NH * 128);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t rank = cluster_ctarank();
+  uint32_t ncols = 32;
+  while (ncols < (uint32_t)N) ncols <<= 1;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before();
+  cluster_sync_all();
+  tc::fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t idesc = tc::idesc_bf16(256, N);
+  for (int kc = 0; kc < K / 64; ++kc) {
+    for (int i = tid; i < 128 * 64; i += 256) {
+      const int r = i >> 6, k = i & 63;
+      const tc::Bf3 s = tc::split3(W[(size_t)(128 * rank + r) * K + kc * 64 + k]);
+      const uint32_t o = tc::sw128_off(r, k, 128);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(As + p * 128 * 128 + o) = s.p[p];
+    }
+    for (int i = tid; i < NH * 64; i += 256) {
+      const int r = i >> 6, k = i & 63;
+      const tc::Bf3 s = tc::split3(B[(size_t)(NH * rank + r) * K + kc * 64 + k]);
+      const uint32_t o = tc::sw128_off(r, k, NH);
+#pragma unroll
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * NH * 128 + o) = s.p[p];
+    }
+    fence_proxy_async();
+    tc::fence_before();
+    cluster_sync_all();  // both CTAs' operands of this chunk are in place
+    if (rank == 0 && tid == 0) {
+      tc::fence_after();
+      for (int s = 0; s < 4; ++s)
+        for (int q = 0; q < 6; ++q) {
+          const uint64_t ad = tc::sdesc_sw128(smem_u32(As + tc::prod_a(q) * 128 * 128 + s * 32));
+          const uint64_t bd = tc::sdesc_sw128(smem_u32(Bs + tc::prod_b(q) * NH * 128 + s * 32));
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tbase),
+              "l"(ad), "l"(bd), "r"(idesc), "r"((kc | s | q) != 0 ? 1u : 0u)
+              : "memory");
+        }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(bar)),
+          "h"((uint16_t)3)
+          : "memory");
+    }
+    mbar_wait(bar, kc & 1);
+    tc::fence_after();
+  }
+  if (warp < 4) {
+    const int m = 128 * (int)rank + 32 * warp + (tid & 31);
+    for (int n0 = 0; n0 < N; n0 += 8) {
+      float v[8];
+      tc::tmem_ld8(tbase + tc::tmem_lane_base(warp) + n0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) D[(size_t)m * N + n0 + j] = v[j];
+    }
+  }
+  tc::fence_before();
+  cluster_sync_all();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols) : "memory");
+}
+
+}  // namespace fdsdf
+
+extern "C" fdsdf_status fdsdf_selftest_mma_pair(const float* d_W, const float* d_B, float* d_D, int N, int K,
+                                                void* stream) {
+  using namespace fdsdf;
+  if (!d_W || !d_B || !d_D) return FDSDF_E_INVALID;
+  if (N < 32 || N > 256 || N % 32 || K < 64 || K % 64) return FDSDF_E_INVALID;
+  const size_t smem = 3 * (size_t)(128 + N / 2) * 128 + 64 + 1024;
+  cudaError_t e = cudaFuncSetAttribute(tcprobe2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return FDSDF_E_CUDA;
+  tcprobe2_kernel<<<2, 256, smem, (cudaStream_t)stream>>>(d_W, d_B, d_D, N, K);
+  return cudaGetLastError() == cudaSuccess ? FDSDF_OK : FDSDF_E_CUDA;
+}

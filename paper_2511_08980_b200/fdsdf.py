@@ -111,6 +111,8 @@ def lib():
         L.fdsdf_kernel_times.restype = C.c_int
         L.fdsdf_selftest_mma.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp]
         L.fdsdf_selftest_mma.restype = C.c_int
+        L.fdsdf_selftest_mma_pair.argtypes = [vp, vp, vp, C.c_int, C.c_int, vp]
+        L.fdsdf_selftest_mma_pair.restype = C.c_int
         L.fdsdf_version.argtypes = []
         L.fdsdf_version.restype = C.c_char_p
         _lib = L
@@ -373,6 +375,16 @@ def fdsdf_selftest_mma(W, B, nprod=6, mn_major=0, stream=None):
     D = torch.empty(M, N, device=W.device, dtype=torch.float32)
     _check(lib().fdsdf_selftest_mma(_ptr(W.contiguous()), _ptr(B.contiguous()), _ptr(D), M, N, K, int(nprod),
                                     int(mn_major), _stream(stream)))
+    return D
+
+
+def fdsdf_selftest_mma_pair(W, B, stream=None):
+    """D = W @ B.T on a tcgen05 CTA pair (W [256,K], B [N,K] fp32 CUDA tensors)."""
+    import torch
+    N, K = B.shape
+    D = torch.empty(256, N, device=W.device, dtype=torch.float32)
+    _check(lib().fdsdf_selftest_mma_pair(_ptr(W.contiguous()), _ptr(B.contiguous()), _ptr(D), N, K,
+                                         _stream(stream)))
     return D
 
 

@@ -74,3 +74,20 @@ def test_mma_mn_major(M, N, K):
     assert err <= 24.0
     Ds, refs, _ = _run(M, N, K, 6, structured=True, mn=1)
     assert np.max(np.abs(Ds - refs)) < 1e-3
+
+
+@pytest.mark.parametrize("N,K", [(64, 128), (128, 256), (256, 64), (96, 192)])
+def test_mma_cta_pair(N, K):
+    """cta_group::2 (M = 256 over a CTA pair, B split by columns between the pair)."""
+    from paper_2511_08980_b200.fdsdf import fdsdf_selftest_mma_pair
+    rng = np.random.default_rng(N + K)
+    W = rng.standard_normal((256, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    D = fdsdf_selftest_mma_pair(torch.from_numpy(W).cuda(), torch.from_numpy(B).cuda())
+    torch.cuda.synchronize()
+    D = D.cpu().numpy().astype(np.float64)
+    ref = W.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.abs(W.astype(np.float64)) @ np.abs(B.astype(np.float64)).T
+    err = np.max(np.abs(D - ref) / (scale * 2.0 ** -24))
+    print("pair", N, K, "err ulps", err)
+    assert err <= 24.0
