@@ -23,8 +23,10 @@ namespace fdsdf {
 #define BWD_TC_NEPI 16
 #endif
 template <int MPAD>
-struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI> {
-  using B = TcCfg<MPAD, 80, BWD_TC_NEPI>;
+struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20> {
+  // one accumulator range (6 MMAs per K step) leaves TMEM for the phase-A stash:
+  // (MH x EG thread groups) x (centres per thread) x 20 values
+  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20>;
   static constexpr int CT = 8;                                      // centres per tile
   static constexpr int OFF_SD = B::OFF_X;                           // float [CT][20]: seeds + x
   static constexpr int OFF_BAR = OFF_SD + CT * 20 * 4;
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     const int eg = ew / (4 * MH);
     const int m = hh * 128 + 32 * q4 + lane;
     const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * C::DH;
+    // this thread group's stash columns (after both halves' accumulators)
+    const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + C::MH * C::DH + (hh * EG + eg) * CPE * 20;
     const float beta = net.beta;
     const float h = a.h;
     const int64_t nrows = a.n * NCOLB;
@@ -119,8 +123,9 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         const bool mok = m < M;
         const float wl = (top && mok) ? net.W[L - 1][m] : 0.f;
         float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
-        // the 12 stored forward pre-activations of (centre i, layer l, this neuron), loaded one
-        // centre ahead so the global-load latency hides behind the previous centre's math
+        // ---- phase A (X-independent, overlaps this layer's MMA): the pair maps of every
+        // centre of this thread -- A_a, S_a and the derivative factors P, Dd, Z -- from the
+        // stored forward pre-activations, stashed in this thread's TMEM lane
         struct Zq {
           float z, t0, t1, t2, A[4], S[4];
         };
@@ -141,7 +146,47 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           }
           return q;
         };
-        Zq qn = ldq(0);
+        {
+          Zq qn = ldq(0);
+#pragma unroll 1
+          for (int i = 0; i < CPE; ++i) {
+            const Zq q = qn;
+            qn = ldq(i + 1);
+            float v16[16], v4[4];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v16[j] = 0.f;
+            v4[0] = v4[1] = v4[2] = v4[3] = 0.f;
+            if (mok && c0 + eg + EG * i < a.n) {
+              const typename AF::C cc = AF::centre(q.z, beta);
+              float t[20];
+#pragma unroll
+              for (int p = 0; p < 4; ++p)
+                AF::pair_bwd(cc, q.A[p], q.S[p], beta, &t[5 * p], &t[5 * p + 1], &t[5 * p + 2], &t[5 * p + 3],
+                             &t[5 * p + 4]);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v16[j] = t[j];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v4[j] = t[16 + j];
+            }
+            tc::tmem_st16(tstash + i * 20, v16);
+            tc::tmem_st4(tstash + i * 20 + 16, v4);
+          }
+          tc::tmem_wait_st();
+        }
+        // ---- phase B (after the MMA): combine with the adjoint X
+        auto ldz = [&](int i, float (&z4)[4]) {
+          const int64_t c = c0 + eg + EG * i;
+          z4[0] = z4[1] = z4[2] = z4[3] = 0.f;
+          if (i < CPE && c < a.n && mok) {
+            const float* zq = a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + m;
+            z4[0] = __ldg(zq);
+            z4[1] = __ldg(zq + 1 * MPAD);
+            z4[2] = __ldg(zq + 2 * MPAD);
+            z4[3] = __ldg(zq + 3 * MPAD);
+          }
+        };
+        float zn[4];
+        ldz(0, zn);
         if (!top) {
           ptimer.before_wait();
           mbar_wait(bars.dfull, nd & 1u);
@@ -154,8 +199,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           const int cl = eg + EG * i;
           const int64_t c = c0 + cl;
           const bool valid = c < a.n;
-          const Zq q = qn;
-          qn = ldq(i + 1);
+          const float zc[4] = {zn[0], zn[1], zn[2], zn[3]};
+          ldz(i + 1, zn);
           const float* sd = sds + cl * 20;
           float X[NCOLB];
           if (top) {
@@ -171,6 +216,16 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             X[8] = v2[0];
             X[9] = v2[1];
           }
+          float t[20];
+          {
+            float v16[16], v4[4];
+            tc::tmem_ld16(tstash + i * 20, v16);
+            tc::tmem_ld4(tstash + i * 20 + 16, v4);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) t[j] = v16[j];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) t[16 + j] = v4[j];
+          }
           const float r0 = sd[5], r1 = sd[6], r2 = sd[7];
           const float u0 = sd[8], u1 = sd[9], u2 = sd[10], v0 = sd[11], v1 = sd[12], v2_ = sd[13];
           float dl[NCOLB], pv[NCOLB];
@@ -178,15 +233,13 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           for (int j = 0; j < NCOLB; ++j) dl[j] = pv[j] = 0.f;
           float w0p[3] = {0.f, 0.f, 0.f};
           if (mok && valid) {
-            const float tr = fmaf(r0, q.t0, fmaf(r1, q.t1, r2 * q.t2));
-            const typename AF::C cc = AF::centre(q.z, beta);
+            const float tr = fmaf(r0, zc[1], fmaf(r1, zc[2], r2 * zc[3]));
+            const typename AF::C cc = AF::centre(zc[0], beta);
             float zbar = 0.f;
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
-              const float A = q.A[p], S = q.S[p];
+              const float Aa = t[5 * p], Sa = t[5 * p + 1], P = t[5 * p + 2], Dd = t[5 * p + 3], Z = t[5 * p + 4];
               const float XA = X[2 + 2 * p], XS = X[3 + 2 * p];
-              float Aa, Sa, P, Dd, Z;
-              AF::pair_bwd(cc, A, S, beta, &Aa, &Sa, &P, &Dd, &Z);
               const float dA = om * fmaf(XA, P, 2.0f * XS * Dd);
               const float dS = om * fmaf(0.5f * XA, Dd, XS * P);
               zbar = fmaf(XA, Dd, fmaf(XS, Z, zbar));

@@ -20,7 +20,7 @@
 
 namespace fdsdf {
 
-template <int MPAD_, int N_, int NEPI_ = 8>
+template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
@@ -36,12 +36,16 @@ struct TcCfg {
   static constexpr int OFF_W = 0;
   static constexpr int OFF_B = NST * STAGE;
   static constexpr int OFF_X = OFF_B + 3 * BPIECE;  // kernel-specific scratch starts here
-  // TMEM: per M-half three accumulator ranges of N columns (see tc_mma)
-  static constexpr int DH = 3 * N;
-  static constexpr uint32_t TCOLS = (MH * DH) <= 32 ? 32 : (MH * DH) <= 64 ? 64 : (MH * DH) <= 128 ? 128
-                                    : (MH * DH) <= 256 ? 256 : 512;
-  static_assert(N % 16 == 0 && N >= 16 && 3 * N <= 256, "tcgen05 M=128 needs N % 16 == 0 and 3N <= 256");
-  static_assert(MH * DH <= 512, "TMEM has 512 columns");
+  // TMEM: per M-half RANGES accumulator ranges of N columns (see tc_mma), then STASH extra
+  // columns of kernel scratch
+  static constexpr int RANGES = RANGES_;
+  static constexpr int DH = RANGES * N;
+  static constexpr int STASH = STASH_;
+  static constexpr int TUSE = MH * DH + STASH;
+  static constexpr uint32_t TCOLS = TUSE <= 32 ? 32 : TUSE <= 64 ? 64 : TUSE <= 128 ? 128 : TUSE <= 256 ? 256 : 512;
+  static_assert(RANGES == 1 || RANGES == 3, "one accumulator range (6 MMAs) or three (3 MMAs)");
+  static_assert(N % 16 == 0 && N >= 16 && RANGES * N <= 256, "tcgen05 M=128 needs N % 16 == 0, <= 256");
+  static_assert(TUSE <= 512, "TMEM has 512 columns");
   static_assert(NEPI % (4 * MH) == 0, "every (lane quarter, M-half) needs the same number of epilogue warps");
 };
 
@@ -146,12 +150,22 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
           const uint32_t wa = smem_u32(Ws + s * C::STAGE);
           const uint32_t ba = smem_u32(Bs + kc * C::BKC);
           const uint32_t d = tbase + h * C::DH;
+          if (C::RANGES == 3) {
 #pragma unroll
-          for (int sub = 0; sub < 4; ++sub) {
-            const uint64_t bd = tc::sdesc_sw128(ba + sub * 32);
-            tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
-            tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
-            tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+            for (int sub = 0; sub < 4; ++sub) {
+              const uint64_t bd = tc::sdesc_sw128(ba + sub * 32);
+              tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
+              tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
+              tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+            }
+          } else {  // the six piece products into one range
+#pragma unroll
+            for (int sub = 0; sub < 4; ++sub)
+#pragma unroll
+              for (int q = 0; q < 6; ++q)
+                tc::mma_bf16(d, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
+                             tc::sdesc_sw128(ba + tc::prod_b(q) * C::N * 128 + sub * 32), id1,
+                             (kc | sub | q) != 0 ? 1u : 0u);
           }
           tc::mma_commit(&b.wempty[s]);
         }
@@ -215,6 +229,10 @@ __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float 
 // TMEM ranges (range 0 + (range 1 + range 2), smallest terms first)
 template <class C>
 __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8]) {
+  if (C::RANGES == 1) {
+    tc::tmem_ld8(taddr + col, v);
+    return;
+  }
   float r1[8], r2[8];
   tc::tmem_ld8(taddr + col, v);
   tc::tmem_ld8(taddr + C::N + col, r1);
@@ -224,6 +242,10 @@ __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8
 }
 template <class C>
 __device__ __forceinline__ void tc_ld_sum2(uint32_t taddr, int col, float (&v)[2]) {
+  if (C::RANGES == 1) {
+    tc::tmem_ld2(taddr + col, v);
+    return;
+  }
   float r1[2], r2[2];
   tc::tmem_ld2(taddr + col, v);
   tc::tmem_ld2(taddr + C::N + col, r1);
