@@ -27,12 +27,15 @@
 
 namespace fdsdf {
 
+#ifndef FWD_TC_NSPLIT
+#define FWD_TC_NSPLIT 1
+#endif
 #ifndef FWD_TC_NEPI
 #define FWD_TC_NEPI 16
 #endif
 template <int MPAD>
-struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI> {
-  using B = TcCfg<MPAD, 64, FWD_TC_NEPI>;
+struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT> {
+  using B = TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
@@ -221,22 +224,27 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
             if (lane == 0) red[(ew * C::MAXC + cl) * 4 + j] = v;
           }
         };
+        // the tile's centres are processed split by split (C::NSPLIT column splits): as soon as
+        // this split's part of the next B operand is written, its MMA pass for layer l+1 runs
+        // while the epilogue continues with the next split of layer l
+        constexpr int CPSPL = CT / C::NSPLIT;   // centres per split
+        constexpr int CPEs = CPE / C::NSPLIT;   // centres per thread per split
+        for (int sp = 0; sp < C::NSPLIT; ++sp) {
         // mode 2: the centre pre-activation of this neuron, prefetched one centre ahead
         auto ldz = [&](int i) -> float {
-          const int64_t c = c0 + eg + C::EG * i;
-          return (MODE == 2 && i < CPE && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
+          const int64_t c = c0 + sp * CPSPL + eg + C::EG * i;
+          return (MODE == 2 && i < CPEs && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
         };
         float z0n = ldz(0);
         if (l > 0) {
           ptimer.before_wait();
-          mbar_wait(bars.dfull, nd & 1u);
+          mbar_wait(&bars.dfull[sp], nd & 1u);
           ptimer.after_wait();
-          ++nd;
           tc::fence_after();
         }
 #pragma unroll 1
-        for (int i = 0; i < CPE; ++i) {
-          const int cl = eg + C::EG * i;  // centre slot in the tile
+        for (int i = 0; i < CPEs; ++i) {
+          const int cl = sp * CPSPL + eg + C::EG * i;  // centre slot in the tile
           const int64_t c = c0 + cl;
           const bool valid = c < a.n;
           const float z0 = z0n;
@@ -344,11 +352,13 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
             }
           }
         }
-        if (!last) {  // B operand of layer l+1 complete (this warp's part): hand to the MMA thread
-          tc_epi_arrive(bars);
+        if (!last) {  // this split's B operand of layer l+1 (this warp's part): hand to the MMA thread
+          tc_epi_arrive(bars, sp);
         } else if (l > 0) {
           tc::fence_before();
         }
+        }  // split
+        if (l > 0) ++nd;
         if (l == 0 && pending) {  // the previous tile's per-centre work, overlapping the MMA phase
           if (ew == 0) finish(pend_c0, pend_red, pend_cis);
           pending = false;

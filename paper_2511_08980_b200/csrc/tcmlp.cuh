@@ -20,7 +20,7 @@
 
 namespace fdsdf {
 
-template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0>
+template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
@@ -29,7 +29,13 @@ struct TcCfg {
   static constexpr int STAGE = 3 * 128 * 128;   // weight stage (kc, h): 3 pieces x 128 rows x 128 B
   static constexpr int NST = 2;                 // weight ring depth
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
-  static constexpr int BKC = 3 * N * 128;       // one K chunk of B: the 3 pieces as consecutive row blocks
+  static constexpr int BKC = 3 * N * 128;       // one K chunk of B
+  // column splits: the tile's N columns are NSPLIT independent MMA passes of NS columns each,
+  // so the MMA of split s (layer l+1) can run while the epilogue still works on split s+1
+  // (layer l).  Within a K chunk split s holds its 3 pieces as consecutive row blocks
+  // [b0 | b1 | b2] of NS rows.
+  static constexpr int NSPLIT = NSPLIT_;
+  static constexpr int NS = N / NSPLIT;
   static constexpr int NEPI = NEPI_;            // epilogue warps (a multiple of 4 * MH)
   static constexpr int NTHR = (2 + NEPI) * 32;
   static constexpr int EG = NEPI / (4 * MH);    // epilogue warps per (lane quarter, M-half)
@@ -39,12 +45,13 @@ struct TcCfg {
   // TMEM: per M-half RANGES accumulator ranges of N columns (see tc_mma), then STASH extra
   // columns of kernel scratch
   static constexpr int RANGES = RANGES_;
-  static constexpr int DH = RANGES * N;
+  static constexpr int DH = RANGES * N;          // per M-half: splits x ranges x NS
   static constexpr int STASH = STASH_;
   static constexpr int TUSE = MH * DH + STASH;
   static constexpr uint32_t TCOLS = TUSE <= 32 ? 32 : TUSE <= 64 ? 64 : TUSE <= 128 ? 128 : TUSE <= 256 ? 256 : 512;
   static_assert(RANGES == 1 || RANGES == 3, "one accumulator range (6 MMAs) or three (3 MMAs)");
-  static_assert(N % 16 == 0 && N >= 16 && RANGES * N <= 256, "tcgen05 M=128 needs N % 16 == 0, <= 256");
+  static_assert(NS % 16 == 0 && NS >= 16 && RANGES * NS <= 256, "tcgen05 M=128 needs N % 16 == 0, <= 256");
+  static_assert(NSPLIT == 1 || NSPLIT == 2, "one or two column splits");
   static_assert(TUSE <= 512, "TMEM has 512 columns");
   static_assert(NEPI % (4 * MH) == 0, "every (lane quarter, M-half) needs the same number of epilogue warps");
 };
@@ -52,8 +59,8 @@ struct TcCfg {
 struct TcBars {
   uint64_t* wfull;
   uint64_t* wempty;
-  uint64_t* bfull;
-  uint64_t* dfull;
+  uint64_t* bfull;  // [NSPLIT]
+  uint64_t* dfull;  // [NSPLIT]
   uint32_t* tslot;
 };
 
@@ -64,13 +71,13 @@ __device__ __forceinline__ TcBars tc_bars(unsigned char* p) {
   b.wfull = reinterpret_cast<uint64_t*>(p);
   b.wempty = b.wfull + C::NST;
   b.bfull = b.wempty + C::NST;
-  b.dfull = b.bfull + 1;
-  b.tslot = reinterpret_cast<uint32_t*>(b.dfull + 1);
+  b.dfull = b.bfull + C::NSPLIT;
+  b.tslot = reinterpret_cast<uint32_t*>(b.dfull + C::NSPLIT);
   return b;
 }
 template <class C>
 constexpr int tc_bars_bytes() {
-  return (2 * C::NST + 2) * 8 + 16;
+  return (2 * C::NST + 2 * C::NSPLIT) * 8 + 16;
 }
 
 // CTA prologue: barrier init (thread 0), TMEM allocation (warp 1); returns the TMEM base.
@@ -82,8 +89,10 @@ __device__ __forceinline__ uint32_t tc_setup(const TcBars& b) {
       mbar_init(&b.wfull[s], 1);
       mbar_init(&b.wempty[s], 1);
     }
-    mbar_init(b.bfull, C::NEPI);
-    mbar_init(b.dfull, 1);
+    for (int s = 0; s < C::NSPLIT; ++s) {
+      mbar_init(&b.bfull[s], C::NEPI);
+      mbar_init(&b.dfull[s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(b.tslot, C::TCOLS);
@@ -107,8 +116,8 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
                                             unsigned char* Ws, const TcBars& b) {
   uint32_t it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-    for (int gi = 0; gi < ngemm; ++gi) {
-      const int g = reverse ? ngemm - 1 - gi : gi;
+    for (int gi = 0; gi < ngemm * C::NSPLIT; ++gi) {  // each layer once per column split
+      const int g = reverse ? ngemm - 1 - gi / C::NSPLIT : gi / C::NSPLIT;
       for (int kc = 0; kc < C::KC; ++kc)
         for (int h = 0; h < C::MH; ++h, ++it) {
           const int s = (int)(it % C::NST);
@@ -133,13 +142,13 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
 template <class C>
 __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned char* Ws,
                                        const unsigned char* Bs, uint32_t tbase, const TcBars& b) {
-  constexpr uint32_t id3 = tc::idesc_bf16(128, 3 * C::N), id2 = tc::idesc_bf16(128, 2 * C::N),
-                     id1 = tc::idesc_bf16(128, C::N);
+  constexpr uint32_t id3 = tc::idesc_bf16(128, 3 * C::NS), id2 = tc::idesc_bf16(128, 2 * C::NS),
+                     id1 = tc::idesc_bf16(128, C::NS);
   uint32_t it = 0, nb = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-    for (int g = 0; g < ngemm; ++g) {
-      mbar_wait(b.bfull, nb & 1u);
-      ++nb;
+    for (int gs = 0; gs < ngemm * C::NSPLIT; ++gs, ++nb) {
+      const int sp = gs % C::NSPLIT;  // column split of this pass
+      mbar_wait(&b.bfull[sp], (nb / C::NSPLIT) & 1u);
       tc::fence_after();
       for (int kc = 0; kc < C::KC; ++kc)
         for (int h = 0; h < C::MH; ++h, ++it) {
@@ -148,8 +157,8 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
           mbar_wait(&b.wfull[s], ph);
           tc::fence_after();
           const uint32_t wa = smem_u32(Ws + s * C::STAGE);
-          const uint32_t ba = smem_u32(Bs + kc * C::BKC);
-          const uint32_t d = tbase + h * C::DH;
+          const uint32_t ba = smem_u32(Bs + kc * C::BKC + sp * 3 * C::NS * 128);
+          const uint32_t d = tbase + h * C::DH + sp * C::RANGES * C::NS;
           if (C::RANGES == 3) {
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
@@ -164,12 +173,12 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
 #pragma unroll
               for (int q = 0; q < 6; ++q)
                 tc::mma_bf16(d, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
-                             tc::sdesc_sw128(ba + tc::prod_b(q) * C::N * 128 + sub * 32), id1,
+                             tc::sdesc_sw128(ba + tc::prod_b(q) * C::NS * 128 + sub * 32), id1,
                              (kc | sub | q) != 0 ? 1u : 0u);
           }
           tc::mma_commit(&b.wempty[s]);
         }
-      tc::mma_commit(b.dfull);
+      tc::mma_commit(&b.dfull[sp]);
     }
 }
 
@@ -208,11 +217,11 @@ struct PhaseTimer {
 
 // epilogue warp: the B operand of the next GEMM is complete (this warp's rows), and its
 // reads of the previous D are finished -> hand over to the MMA thread
-__device__ __forceinline__ void tc_epi_arrive(const TcBars& b) {
+__device__ __forceinline__ void tc_epi_arrive(const TcBars& b, int sp = 0) {
   tc::fence_before();
   fence_proxy_async();
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(b.bfull);
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&b.bfull[sp]);
 }
 
 // write v (split into 3 bf16 pieces) at B operand element (column n, K index k): K chunk
@@ -220,9 +229,10 @@ __device__ __forceinline__ void tc_epi_arrive(const TcBars& b) {
 template <class C>
 __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float v) {
   const tc::Bf3 s = tc::split3(v);
-  const uint32_t off = (uint32_t)((k >> 6) * C::BKC) + tc::sw128_off(n, k & 63, C::N);
+  const int sp = n / C::NS, nl = n % C::NS;
+  const uint32_t off = (uint32_t)((k >> 6) * C::BKC + sp * 3 * C::NS * 128) + tc::sw128_off(nl, k & 63, C::NS);
 #pragma unroll
-  for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::N * 128 + off) = s.p[p];
+  for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::NS * 128 + off) = s.p[p];
 }
 
 // accumulator of columns [col, col + W) of this warp's lane quarter: the sum of the three
@@ -234,9 +244,11 @@ __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8
     return;
   }
   float r1[8], r2[8];
-  tc::tmem_ld8(taddr + col, v);
-  tc::tmem_ld8(taddr + C::N + col, r1);
-  tc::tmem_ld8(taddr + 2 * C::N + col, r2);
+  const int sp = col / C::NS, nl = col % C::NS;  // 8 columns never straddle a split
+  const uint32_t t0 = taddr + sp * 3 * C::NS + nl;
+  tc::tmem_ld8(t0, v);
+  tc::tmem_ld8(t0 + C::NS, r1);
+  tc::tmem_ld8(t0 + 2 * C::NS, r2);
 #pragma unroll
   for (int j = 0; j < 8; ++j) v[j] += r1[j] + r2[j];
 }
@@ -247,9 +259,11 @@ __device__ __forceinline__ void tc_ld_sum2(uint32_t taddr, int col, float (&v)[2
     return;
   }
   float r1[2], r2[2];
-  tc::tmem_ld2(taddr + col, v);
-  tc::tmem_ld2(taddr + C::N + col, r1);
-  tc::tmem_ld2(taddr + 2 * C::N + col, r2);
+  const int sp = col / C::NS, nl = col % C::NS;
+  const uint32_t t0 = taddr + sp * 3 * C::NS + nl;
+  tc::tmem_ld2(t0, v);
+  tc::tmem_ld2(t0 + C::NS, r1);
+  tc::tmem_ld2(t0 + 2 * C::NS, r2);
 #pragma unroll
   for (int j = 0; j < 2; ++j) v[j] += r1[j] + r2[j];
 }
