@@ -19,14 +19,19 @@ namespace fdsdf {
 #ifndef BWD_TC_PREFETCH
 #define BWD_TC_PREFETCH 0
 #endif
+#ifndef BWD_TC_WPK
+#define BWD_TC_WPK 3
+#endif
 #ifndef BWD_TC_NEPI
 #define BWD_TC_NEPI 16
 #endif
 template <int MPAD>
-struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20> {
+struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20, 1,
+                      BWD_TC_WPK> {
   // one accumulator range (6 MMAs per K step) leaves TMEM for the phase-A stash:
   // (MH x EG thread groups) x (centres per thread) x 20 values
-  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20>;
+  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20, 1,
+                  BWD_TC_WPK>;
   static constexpr int CT = 8;                                      // centres per tile
   static constexpr int OFF_SD = B::OFF_X;                           // float [CT][20]: seeds + x
   static constexpr int OFF_BAR = OFF_SD + CT * 20 * 4;

@@ -33,9 +33,14 @@ namespace fdsdf {
 #ifndef FWD_TC_NEPI
 #define FWD_TC_NEPI 16
 #endif
-template <int MPAD>
-struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT> {
-  using B = TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT>;
+#ifndef FWD_TC_PAIR_WPK
+#define FWD_TC_PAIR_WPK 3
+#endif
+// mode 1 (centre + tangents: they set g, the frames and the |g|^p denominators) streams all
+// three weight pieces; mode 2 (the stencil-pair differences) streams FWD_TC_PAIR_WPK
+template <int MPAD, int MODE>
+struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT, MODE == 1 ? 3 : FWD_TC_PAIR_WPK> {
+  using B = TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT, MODE == 1 ? 3 : FWD_TC_PAIR_WPK>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
@@ -50,12 +55,12 @@ struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT> {
 
 bool tc_supported(int mpad, int skip) { return (mpad == 128 || mpad == 256) && skip < 0; }
 
-size_t tc_wimg_bytes(int mpad, int ngemm) { return (size_t)(ngemm > 0 ? ngemm : 0) * mpad * mpad * 6; }
+size_t tc_wimg_bytes(int mpad, int ngemm) { return (size_t)(ngemm > 0 ? ngemm : 0) * mpad * mpad * 2 * tc::WP; }
 
 int fwd_tc_tile_centres(int mode) { return mode == 1 ? 16 : 8; }
 
 // ----------------------------------------------------------------------------- weight images
-// image[g][kc][h][piece][sw128 128 rows x 64 k]: forward A operand = W_l (rows = output
+// image[g][kc][h][piece < WP][sw128 128 rows x 64 k]: forward A operand = W_l (rows = output
 // neuron m, K = input neuron k); backward A operand = W_l^T (rows = k, K = m).
 __global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char* bimg) {
   const int mp = net.mpad;
@@ -65,22 +70,22 @@ __global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char
   const int M = net.width[l + 1];
   const int K = net.width[l];
   const float* W = net.W[l];
-  const size_t per_layer = (size_t)mp * mp * 6;
+  const size_t per_layer = (size_t)mp * mp * 2 * tc::WP;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < mp * mp; idx += gridDim.x * blockDim.x) {
     const int r = idx / mp, k = idx % mp;  // A-operand row r, K index k
     const int h = r >> 7, rr = r & 127, kc = k >> 6, kk = k & 63;
-    const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * TcCfg<128, 64, 8>::STAGE + tc::sw128_off(rr, kk, 128);
+    const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * (tc::WP * 16384) + tc::sw128_off(rr, kk, 128);
     {
       const float v = (r < M && k < K) ? W[(size_t)r * K + k] : 0.f;  // forward: W[m = r][k]
       const tc::Bf3 s = tc::split3(v);
 #pragma unroll
-      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(fimg + off + p * 16384) = s.p[p];
+      for (int p = 0; p < tc::WP; ++p) *reinterpret_cast<__nv_bfloat16*>(fimg + off + p * 16384) = s.p[p];
     }
     if (bimg) {
       const float v = (k < M && r < K) ? W[(size_t)k * K + r] : 0.f;  // backward: W^T[k = r][m = k]
       const tc::Bf3 s = tc::split3(v);
 #pragma unroll
-      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(bimg + off + p * 16384) = s.p[p];
+      for (int p = 0; p < tc::WP; ++p) *reinterpret_cast<__nv_bfloat16*>(bimg + off + p * 16384) = s.p[p];
     }
   }
   (void)KC;
@@ -95,8 +100,8 @@ cudaError_t launch_pack_tc(const Net& net, unsigned char* fimg, unsigned char* b
 
 // ----------------------------------------------------------------------------- the kernel
 template <int ACT, int MPAD, int MODE>
-__global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const FwdArgs a) {
-  using C = FtcCfg<MPAD>;
+__global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(const FwdArgs a) {
+  using C = FtcCfg<MPAD, MODE>;
   using AF = Act<ACT>;
   constexpr int N = C::N, MH = C::MH;
   constexpr int CPC = MODE == 1 ? 4 : 8;  // columns per centre
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD>::NTHR, 1) fwd_tc_kernel(const Fwd
 // ----------------------------------------------------------------------------- host launch
 template <int ACT, int MPAD, int MODE>
 static cudaError_t launch_fwd_tc_t(const FwdArgs& a, int grid, cudaStream_t st) {
-  using C = FtcCfg<MPAD>;
+  using C = FtcCfg<MPAD, MODE>;
   auto k = fwd_tc_kernel<ACT, MPAD, MODE>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
   if (e != cudaSuccess) return e;

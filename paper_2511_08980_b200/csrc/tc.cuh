@@ -208,6 +208,9 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
 
 __device__ __forceinline__ uint32_t tmem_lane_base(int warp) { return (uint32_t)(32 * (warp & 3)) << 16; }
 
+// the packed weight images hold WP = 3 exact bf16 pieces per weight (48 KB per (K chunk,
+// M-half) stage); a kernel may stream only the first WPK of them (see TcCfg::WPK)
+constexpr int WP = 3;
 // the six piece products (i, j), i + j <= 2, smallest first
 __host__ __device__ constexpr int prod_a(int q) { return q == 0 ? 2 : (q == 1 || q == 3) ? 1 : 0; }
 __host__ __device__ constexpr int prod_b(int q) { return q == 2 ? 2 : (q == 1 || q == 4) ? 1 : 0; }

@@ -20,14 +20,20 @@
 
 namespace fdsdf {
 
-template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1>
+template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1, int WPK_ = 3>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
   static constexpr int MH = MPAD / 128;         // tcgen05 M-halves (M = 128 each)
   static constexpr int KC = MPAD / 64;          // K chunks (one 128-byte swizzle row each)
-  static constexpr int STAGE = 3 * 128 * 128;   // weight stage (kc, h): 3 pieces x 128 rows x 128 B
-  static constexpr int NST = 2;                 // weight ring depth
+  // weight pieces streamed: 3 = the fp32-accurate bf16x6 products; 2 = W' = w0 + w1
+  // (|W' - W| <= 2^-18 |W|) with all three activation pieces: products a0 b0, a0 b1, a0 b2,
+  // a1 b0, a1 b1 ("bf16x5"), for kernels whose gates tolerate that fixed perturbation of
+  // the hidden weights (the stencil-pair columns and the backward)
+  static constexpr int WPK = WPK_;
+  static constexpr int IMGSTAGE = tc::WP * 128 * 128;  // stage stride in the packed image
+  static constexpr int STAGE = WPK * 128 * 128;        // weight stage (kc, h) in shared memory
+  static constexpr int NST = WPK == 3 ? 2 : 3;         // weight ring depth (96 KB either way)
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
   static constexpr int BKC = 3 * N * 128;       // one K chunk of B
   // column splits: the tile's N columns are NSPLIT independent MMA passes of NS columns each,
@@ -124,7 +130,7 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
           const uint32_t ph = (it / C::NST) & 1u;
           mbar_wait(&b.wempty[s], ph ^ 1u);
           mbar_arrive_expect_tx(&b.wfull[s], C::STAGE);
-          bulk_g2s(Ws + s * C::STAGE, img + (((size_t)g * C::KC + kc) * C::MH + h) * C::STAGE, C::STAGE,
+          bulk_g2s(Ws + s * C::STAGE, img + (((size_t)g * C::KC + kc) * C::MH + h) * C::IMGSTAGE, C::STAGE,
                    &b.wfull[s]);
         }
     }
@@ -165,16 +171,16 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
               const uint64_t bd = tc::sdesc_sw128(ba + sub * 32);
               tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
               tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
-              tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+              if (C::WPK == 3) tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
             }
           } else {  // the six piece products into one range
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub)
 #pragma unroll
-              for (int q = 0; q < 6; ++q)
+              for (int q = 3 - C::WPK; q < 6; ++q)  // WPK = 2: skip (a2, b0)
                 tc::mma_bf16(d, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
                              tc::sdesc_sw128(ba + tc::prod_b(q) * C::NS * 128 + sub * 32), id1,
-                             (kc | sub | q) != 0 ? 1u : 0u);
+                             (kc == 0 && sub == 0 && q == 3 - C::WPK) ? 0u : 1u);
           }
           tc::mma_commit(&b.wempty[s]);
         }
