@@ -33,8 +33,8 @@ struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC
   using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20, 1,
                   BWD_TC_WPK>;
   static constexpr int CT = 8;                                      // centres per tile
-  static constexpr int OFF_SD = B::OFF_X;                           // float [CT][20]: seeds + x
-  static constexpr int OFF_BAR = OFF_SD + CT * 20 * 4;
+  static constexpr int OFF_SD = B::OFF_X;                           // float [2][CT][20]: seeds + x
+  static constexpr int OFF_BAR = OFF_SD + 2 * CT * 20 * 4;
   static constexpr int BYTES = OFF_BAR + tc_bars_bytes<B>() + 1024;
 };
 
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
   sm += (1024 - (smem_u32(sm) & 1023)) & 1023;
   unsigned char* Ws = sm + C::OFF_W;
   unsigned char* Bs = sm + C::OFF_B;
-  float* sds = reinterpret_cast<float*>(sm + C::OFF_SD);
+  float* sds0 = reinterpret_cast<float*>(sm + C::OFF_SD);
   const TcBars bars = tc_bars<C>(sm + C::OFF_BAR);
 
   const Net& net = a.net;
@@ -108,18 +108,28 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     };
     if (BWD_TC_PREFETCH) prefetch_tile(blockIdx.x);
 
-    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-      const int64_t c0 = tile * CT;
-      if (BWD_TC_PREFETCH) prefetch_tile(tile + gridDim.x);
-      bar_named(1, C::NEPI * 32);  // previous tile's seed reads are done
+    // per-tile seeds + coordinates, double-buffered: the next tile's are copied asynchronously
+    // (cp.async) while this tile runs
+    auto load_seeds = [&](int64_t tile, float* dst) {
+      const int64_t cb = tile * CT;
       for (int i = et; i < CT * 20; i += C::NEPI * 32) {
         const int cl = i / 20, q = i % 20;
-        const int64_t c = c0 + cl;
-        float v = 0.f;
-        if (c < a.n) v = q < NSEED ? a.seed[c * NSEED + q] : (q < NSEED + 3 ? a.x[c * 3 + (q - NSEED)] : 0.f);
-        sds[i] = v;
+        const int64_t c = cb + cl;
+        if (tile < a.ntiles && c < a.n && q < NSEED + 3)
+          cp_async4(dst + i, q < NSEED ? (const void*)(a.seed + c * NSEED + q) : (const void*)(a.x + c * 3 + (q - NSEED)));
+        else
+          dst[i] = 0.f;
       }
-      bar_named(1, C::NEPI * 32);
+    };
+    load_seeds(blockIdx.x, sds0);
+    uint32_t spar = 0;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, spar ^= 1u) {
+      const int64_t c0 = tile * CT;
+      if (BWD_TC_PREFETCH) prefetch_tile(tile + gridDim.x);
+      cp_async_wait_all();
+      bar_named(1, C::NEPI * 32);  // this tile's seeds are in; every thread is done with the other buffer
+      const float* sds = sds0 + spar * CT * 20;
+      load_seeds(tile + gridDim.x, sds0 + (spar ^ 1u) * CT * 20);
 
       for (int l = L - 2; l >= 0; --l) {
         const bool top = (l == L - 2);

@@ -197,15 +197,26 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
     float* pend_cis = nullptr;
     uint32_t tpar = 0;
 
+    // mode 2: the tile's centre info (f, g, frame, mask) from mode 1.  The first tile's is
+    // loaded here; every later one is copied asynchronously (cp.async, warp 2) into the other
+    // buffer right after that buffer's deferred per-centre epilogue
+    auto load_cinfo = [&](int64_t tile, float* dst, int t0, int nt) {
+      const int64_t cb = tile * CT;
+      for (int i = t0; i < CT * NCINFO; i += nt) {
+        const int64_t c = cb + i / NCINFO;
+        if (tile < a.ntiles && c < a.n)
+          cp_async4(dst + i, a.cinfo + c * NCINFO + (i % NCINFO));
+        else
+          dst[i] = 0.f;
+      }
+    };
+    if (MODE == 2) load_cinfo(blockIdx.x, cis0, et, C::NEPI * 32);
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, tpar ^= 1u) {
       const int64_t c0 = tile * CT;
       float* red = red0 + tpar * C::RED_N;
       float* cis = cis0 + tpar * C::CI_N;
-      if (MODE == 2) {  // the tile's centre info (f, g, frame, mask) from mode 1
-        for (int i = et; i < CT * NCINFO; i += C::NEPI * 32) {
-          const int64_t c = c0 + i / NCINFO;
-          cis[i] = c < a.n ? a.cinfo[c * NCINFO + (i % NCINFO)] : 0.f;
-        }
+      if (MODE == 2) {
+        cp_async_wait_all();
         bar_named(1, C::NEPI * 32);
       }
 
@@ -368,6 +379,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           if (ew == 0) finish(pend_c0, pend_red, pend_cis);
           pending = false;
         }
+        if (l == 0 && MODE == 2 && ew == 0)  // next tile's centre info into the buffer just freed
+          load_cinfo(tile + gridDim.x, cis0 + (tpar ^ 1u) * C::CI_N, lane, 32);
       }
 
       bar_named(1, C::NEPI * 32);  // this tile's last-layer partial sums are complete
