@@ -308,11 +308,28 @@ def main():
     spec = cfg["spec"]
     model = FDSDF(spec, local, max_centers=n, path=None if args.path == "default" else args.path)
     P = model.P
+    collective = None
     if world > 1:
-        uid = F.fdsdf_comm_unique_id() if rank == 0 else bytes(128)
-        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        # the library's own NCCL communicator (the in-step allreduce of FDSDF_STEP_ALLREDUCE);
+        # should loading / initialising it fail on a box, fall back to torch.distributed's NCCL
+        # all-reduce of the same two buffers on the same stream (reported in the JSON line)
+        ok = 1
+        try:
+            uid = F.fdsdf_comm_unique_id() if rank == 0 else bytes(128)
+        except F.FdsdfError:
+            uid, ok = bytes(128), 0
+        t = torch.tensor(list(uid) + [ok], dtype=torch.uint8, device=dev)
         dist.broadcast(t, 0)
-        model.comm_init(bytes(t.cpu().tolist()), rank, world)
+        ok = int(t[128].item())
+        if ok:
+            try:
+                model.comm_init(bytes(t[:128].cpu().tolist()), rank, world)
+            except F.FdsdfError as e:
+                print(f"[bench] rank {rank}: fdsdf_comm_init failed ({e})", file=sys.stderr)
+                ok = 0
+        okt = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        collective = "fdsdf NCCL (in-step ncclAllReduce)" if okt.item() else "torch.distributed NCCL all_reduce"
 
     params = torch.from_numpy(cfg["params"]).to(dev)
     x = torch.from_numpy(cfg["x"]).to(dev)
@@ -322,7 +339,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     lc = cfg["loss"]
     ls = F.make_loss(lc, cfg["counts"])
-    flags = F.STEP_ALLREDUCE if world > 1 else 0
+    lib_ar = collective is not None and collective.startswith("fdsdf")
+    flags = F.STEP_ALLREDUCE if lib_ar else 0
 
     def stencil(step):
         from harness import frame_seed
@@ -331,6 +349,9 @@ def main():
 
     def one_step(i, xin=None):
         F.fdsdf_step(model.ctx, params, x if xin is None else xin, n, stencil(i), ls, grad, loss, flags, stream)
+        if world > 1 and not lib_ar:
+            dist.all_reduce(grad)
+            dist.all_reduce(loss)
 
     def barrier():
         if world > 1:
@@ -403,7 +424,7 @@ def main():
 
     # ------------------------------------------------------------------ full training iteration + eval
     extras = {}
-    if not args.no_extras:
+    if not args.no_extras and (world == 1 or lib_ar):
         extras = measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank, dev)
 
     # ------------------------------------------------------------------ roofline of the dominant kernel
@@ -473,6 +494,7 @@ def main():
             "precision": ("bf16x6: fp32 operands split exactly into 3 bf16 pieces, 6 tcgen05 products, fp32 "
                           "accumulation" if path == "tensor" else "fp32 FFMA"), "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps), "clocks": clocks, **extras,
+            "collective": collective,
             "wall_s_timed_region": wall,
         }
         print(json.dumps(line), flush=True)
