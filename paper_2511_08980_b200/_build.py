@@ -25,8 +25,10 @@ def _newest_input():
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every .cu for sm_100a and link libfdsdf.so; returns its path."""
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, build_dir: str = BUILD) -> str:
+    """Compile every .cu for sm_100a and link libfdsdf.so; returns its path.  `lib` / `build_dir`
+    redirect the output (compile-time variants for A/B timing, see scripts/build_variant.py)."""
+    LIB, BUILD = lib, build_dir
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_input():
         return LIB
     os.makedirs(BUILD, exist_ok=True)

@@ -25,13 +25,29 @@ namespace fdsdf {
 #ifndef BWD_TC_NEPI
 #define BWD_TC_NEPI 16
 #endif
+// B / D column of (centre cl, adjoint column j): 8 j + cl (1) or 10 cl + j (0).  With 8 j + cl
+// the SW128 row group of column j is j itself, so each thread writes a centre's ten B columns
+// at one base offset plus compile-time offsets j * 1024 (no per-element swizzle arithmetic).
+#ifndef BWD_TC_COLPERM
+#define BWD_TC_COLPERM 1
+#endif
+// 1: the top layer of tile t+1 (adjoint seeds -> delta_{L-2}; needs no MMA) is computed during
+// tile t's MMA phases and parked in the delta buffer, so a tile starts with a reload + split
+// instead of a full epilogue pass with the tensor cores idle.
+#ifndef BWD_TC_PIPE_TOP
+#define BWD_TC_PIPE_TOP 1
+#endif
+// accumulator ranges of the X GEMM: 2 (a0.[b0|b1], a1.[b0|b1], a0.b2, a2.b0: four A reads per
+// K step, stash of the 12 derivative factors) or 1 (six MMAs, stash of 20 values)
+#ifndef BWD_TC_RANGES
+#define BWD_TC_RANGES 2
+#endif
+constexpr int BWD_SV = BWD_TC_RANGES == 2 ? 12 : 20;  // stashed values per centre
+// TMEM stash: (MH x EG thread groups) x (centres per thread) x BWD_SV values
+#define BWD_TC_STASH(MPAD) ((BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * ((MPAD) / 128)))) * BWD_SV)
 template <int MPAD>
-struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20, 1,
-                      BWD_TC_WPK> {
-  // one accumulator range (6 MMAs per K step) leaves TMEM for the phase-A stash:
-  // (MH x EG thread groups) x (centres per thread) x 20 values
-  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 1, (BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * (MPAD / 128)))) * 20, 1,
-                  BWD_TC_WPK>;
+struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, BWD_TC_RANGES, BWD_TC_STASH(MPAD), 1, BWD_TC_WPK> {
+  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, BWD_TC_RANGES, BWD_TC_STASH(MPAD), 1, BWD_TC_WPK>;
   static constexpr int CT = 8;                                      // centres per tile
   static constexpr int OFF_SD = B::OFF_X;                           // float [2][CT][20]: seeds + x
   static constexpr int OFF_BAR = OFF_SD + 2 * CT * 20 * 4;
@@ -47,6 +63,10 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
   using AF = Act<ACT>;
   constexpr int N = C::N, MH = C::MH, CT = C::CT, EG = C::EG;
   constexpr int CPE = CT / EG;
+  static_assert(!BWD_TC_COLPERM || (CT == 8 && NCOLB == 10 && C::NSPLIT == 1 && C::RANGES <= 2),
+                "column permutation 8 j + cl assumes 8 centres x 10 columns, one or two accumulator ranges");
+  static_assert(C::RANGES == 1 || BWD_TC_COLPERM, "two ranges are read with the permuted column loads");
+  constexpr int SV = BWD_SV;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = smem_raw;
@@ -76,7 +96,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     const int m = hh * 128 + 32 * q4 + lane;
     const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * C::DH;
     // this thread group's stash columns (after both halves' accumulators)
-    const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + C::MH * C::DH + (hh * EG + eg) * CPE * 20;
+    const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + C::MH * C::DH + (hh * EG + eg) * CPE * SV;
     const float beta = net.beta;
     const float h = a.h;
     const int64_t nrows = a.n * NCOLB;
@@ -122,7 +142,73 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       }
     };
     load_seeds(blockIdx.x, sds0);
+
+    // write delta (10 columns of centre slot cl, neuron m) as the next GEMM's B operand
+    auto put_b10 = [&](int cl, const float (&dl)[NCOLB]) {
+      if (BWD_TC_COLPERM) {
+        // sw128_off(8 j + cl, m) = (m / 64) BKC + 1024 j + 128 cl + (((m % 64) / 8 ^ cl) << 4) + 2 (m % 8)
+        unsigned char* bp = Bs + (m >> 6) * C::BKC + cl * 128 + ((((m & 63) >> 3) ^ cl) << 4) + ((m & 7) << 1);
+#pragma unroll
+        for (int j = 0; j < NCOLB; ++j) {
+          const tc::Bf3 sp3 = tc::split3(dl[j]);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(bp + j * 1024 + p * C::NS * 128) = sp3.p[p];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NCOLB; ++j) tc_put_b<C>(Bs, cl * NCOLB + j, m, dl[j]);
+      }
+    };
+    // the top layer l = L-2 for centre i of tile tl (seeds sdsT): X = W_{L-1}^T fbar-seeds, so
+    // delta_{L-2} needs no MMA.  Writes delta to a.del and accumulates db_{L-2} and dW_{L-1}.
+    const int ltop = L - 2;
+    const bool pipe_top = BWD_TC_PIPE_TOP && ngemm > 0;
+    auto top_centre = [&](int64_t tl, int i, const float* sdsT) {
+      const int cl = eg + EG * i;
+      const int64_t c = tl * CT + cl;
+      if (tl >= a.ntiles || c >= a.n || m >= net.width[ltop + 1]) return;
+      const float omt = net.omega[ltop];
+      const float wlt = net.W[L - 1][m];
+      const float* zq = a.zf + ((size_t)c * nh + ltop) * NCOLF * MPAD + m;
+      float zv[NCOLF];
+#pragma unroll
+      for (int j = 0; j < NCOLF; ++j) zv[j] = __ldg(zq + j * MPAD);
+      const float* sd = sdsT + cl * 20;
+      const float dL[NCOLB] = {sd[0], 1.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
+      const typename AF::C cc = AF::centre(zv[0], beta);
+      float dl[NCOLB], pv[NCOLB];
+      float zbar = 0.f;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        float Aa, Sa, P, Dd, Z;
+        AF::pair_bwd(cc, zv[4 + 2 * p], zv[5 + 2 * p], beta, &Aa, &Sa, &P, &Dd, &Z);
+        const float XA = wlt * dL[2 + 2 * p], XS = wlt * dL[3 + 2 * p];
+        dl[2 + 2 * p] = omt * fmaf(XA, P, 2.0f * XS * Dd);
+        dl[3 + 2 * p] = omt * fmaf(0.5f * XA, Dd, XS * P);
+        zbar = fmaf(XA, Dd, fmaf(XS, Z, zbar));
+        pv[2 + 2 * p] = Aa;
+        pv[3 + 2 * p] = Sa;
+      }
+      const float tr = fmaf(sd[5], zv[1], fmaf(sd[6], zv[2], sd[7] * zv[3]));
+      const float s1 = AF::d1(cc, beta), s2 = AF::d2(cc, beta);
+      const float Xc = wlt * dL[0], Xt = wlt * dL[1];
+      dl[0] = omt * fmaf(Xc, s1, fmaf(s2 * tr, Xt, zbar));
+      dl[1] = omt * s1 * Xt;
+      pv[0] = AF::value(cc, beta);
+      pv[1] = s1 * tr;
+      float* dp = a.del + ((size_t)ltop * nrows + (size_t)c * NCOLB) * MPAD + m;
+#pragma unroll
+      for (int j = 0; j < NCOLB; ++j) dp[j * MPAD] = dl[j];
+      float v = 0.f;
+#pragma unroll
+      for (int j = 0; j < NCOLB; ++j) v = fmaf(dL[j], pv[j], v);
+      r_db[ltop] += dl[0];
+      r_dWL += v;
+    };
     uint32_t spar = 0;
+#ifdef FDSDF_PHASE_TIMING
+    long long t_tstart = 0, t_tstart_n = 0, t_top = 0, t_pa = 0;
+#endif
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, spar ^= 1u) {
       const int64_t c0 = tile * CT;
       if (BWD_TC_PREFETCH) prefetch_tile(tile + gridDim.x);
@@ -130,8 +216,42 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       bar_named(1, C::NEPI * 32);  // this tile's seeds are in; every thread is done with the other buffer
       const float* sds = sds0 + spar * CT * 20;
       load_seeds(tile + gridDim.x, sds0 + (spar ^ 1u) * CT * 20);
+      const float* sds_next = sds0 + (spar ^ 1u) * CT * 20;
 
-      for (int l = L - 2; l >= 0; --l) {
+#ifdef FDSDF_PHASE_TIMING
+      const long long t_ts0 = clock64();
+#endif
+      if (pipe_top) {
+        // the first GEMM's B operand: delta_{L-2} of this tile, computed during the previous
+        // tile (here only for the CTA's first tile) and reloaded from a.del (this thread's writes)
+        if (tile == blockIdx.x)
+          for (int i = 0; i < CPE; ++i) top_centre(tile, i, sds);
+        const bool mt = m < net.width[ltop + 1];
+        float dn[NCOLB];
+        auto ldd = [&](int i, float (&d)[NCOLB]) {
+          const int64_t c = c0 + eg + EG * i;
+          const bool ok = i < CPE && c < a.n && mt;
+          const float* dp = a.del + ((size_t)ltop * nrows + (size_t)c * NCOLB) * MPAD + m;
+#pragma unroll
+          for (int j = 0; j < NCOLB; ++j) d[j] = ok ? dp[j * MPAD] : 0.f;
+        };
+        ldd(0, dn);
+#pragma unroll 1
+        for (int i = 0; i < CPE; ++i) {
+          float dl[NCOLB];
+#pragma unroll
+          for (int j = 0; j < NCOLB; ++j) dl[j] = dn[j];
+          ldd(i + 1, dn);
+          put_b10(eg + EG * i, dl);
+        }
+        tc_epi_arrive(bars);
+      }
+#ifdef FDSDF_PHASE_TIMING
+      t_tstart += clock64() - t_ts0;
+      t_tstart_n += 1;
+#endif
+
+      for (int l = pipe_top ? L - 3 : L - 2; l >= 0; --l) {
         const bool top = (l == L - 2);
         const int M = net.width[l + 1];
         const float om = net.omega[l];
@@ -167,27 +287,85 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           for (int i = 0; i < CPE; ++i) {
             const Zq q = qn;
             qn = ldq(i + 1);
-            float v16[16], v4[4];
+            const int cl = eg + EG * i;
+            const int64_t c = c0 + cl;
+            const bool valid = c < a.n;
+            float t[20];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v16[j] = 0.f;
-            v4[0] = v4[1] = v4[2] = v4[3] = 0.f;
-            if (mok && c0 + eg + EG * i < a.n) {
+            for (int j = 0; j < 20; ++j) t[j] = 0.f;
+            float pv[NCOLB];
+#pragma unroll
+            for (int j = 0; j < NCOLB; ++j) pv[j] = 0.f;
+            if (mok && valid) {
               const typename AF::C cc = AF::centre(q.z, beta);
-              float t[20];
 #pragma unroll
               for (int p = 0; p < 4; ++p)
                 AF::pair_bwd(cc, q.A[p], q.S[p], beta, &t[5 * p], &t[5 * p + 1], &t[5 * p + 2], &t[5 * p + 3],
                              &t[5 * p + 4]);
+              if (SV == 12) {  // the layer's activations (wgrad operand) are X-independent: stored here
+                const float* sd = sds + cl * 20;
+                const float tr = fmaf(sd[5], q.t0, fmaf(sd[6], q.t1, sd[7] * q.t2));
+                pv[0] = AF::value(cc, beta);
+                pv[1] = AF::d1(cc, beta) * tr;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                  pv[2 + 2 * p] = t[5 * p];
+                  pv[3 + 2 * p] = t[5 * p + 1];
+                }
+              }
+            }
+            if (SV == 12) {
+              if (valid && l <= L - 3) {
+                float* ap = a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
+#pragma unroll
+                for (int j = 0; j < NCOLB; ++j) ap[j * MPAD] = pv[j];
+              }
+              if (top) {
+                const float* sd = sds + cl * 20;
+                const float dL[NCOLB] = {sd[0], valid ? 1.f : 0.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
+                float v = 0.f;
+#pragma unroll
+                for (int j = 0; j < NCOLB; ++j) v = fmaf(dL[j], pv[j], v);
+                s_vL += v;
+              }
+              // stash P, Dd, Z of the four pairs
+              float v4[4];
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const int e = 4 * k + j;  // (pair e / 3, factor e % 3)
+                  v4[j] = t[5 * (e / 3) + 2 + e % 3];
+                }
+                tc::tmem_st4(tstash + i * SV + 4 * k, v4);
+              }
+            } else {
+              float v16[16], v4[4];
 #pragma unroll
               for (int j = 0; j < 16; ++j) v16[j] = t[j];
 #pragma unroll
               for (int j = 0; j < 4; ++j) v4[j] = t[16 + j];
+              tc::tmem_st16(tstash + i * SV, v16);
+              tc::tmem_st4(tstash + i * SV + 16, v4);
             }
-            tc::tmem_st16(tstash + i * 20, v16);
-            tc::tmem_st4(tstash + i * 20 + 16, v4);
           }
           tc::tmem_wait_st();
         }
+#ifdef FDSDF_PHASE_TIMING
+        const long long t_pa1 = clock64();
+#endif
+        if (pipe_top) {  // the next tile's top layer, its centres spread over this tile's MMA phases
+          const int g = L - 3 - l;
+          if (g == 0) {
+            cp_async_wait_all();
+            bar_named(1, C::NEPI * 32);  // the next tile's seeds are in
+          }
+#pragma unroll 1
+          for (int i = g; i < CPE; i += ngemm) top_centre(tile + gridDim.x, i, sds_next);
+        }
+#ifdef FDSDF_PHASE_TIMING
+        t_top += clock64() - t_pa1;
+#endif
         // ---- phase B (after the MMA): combine with the adjoint X
         auto ldz = [&](int i, float (&z4)[4]) {
           const int64_t c = c0 + eg + EG * i;
@@ -222,6 +400,10 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             const float dL[NCOLB] = {sd[0], valid ? 1.f : 0.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
 #pragma unroll
             for (int j = 0; j < NCOLB; ++j) X[j] = wl * dL[j];
+          } else if constexpr (C::RANGES == 2) {
+            tc::tmem_ld10x2_stride8(taddr + cl, taddr + C::NS + cl, X);
+          } else if constexpr (BWD_TC_COLPERM) {
+            tc::tmem_ld10_stride8(taddr + cl, X);
           } else {
             float v8[8], v2[2];
             tc_ld_sum8<C>(taddr, cl * NCOLB, v8);
@@ -231,11 +413,24 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             X[8] = v2[0];
             X[9] = v2[1];
           }
-          float t[20];
-          {
+          float t[20];  // per pair: A_a, S_a, P, Dd, Z (SV == 12: only P, Dd, Z are stashed)
+          if (SV == 12) {
+            float v4[4];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              tc::tmem_ld4(tstash + i * SV + 4 * k, v4);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int e = 4 * k + j;
+                t[5 * (e / 3) + 2 + e % 3] = v4[j];
+              }
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p) t[5 * p] = t[5 * p + 1] = 0.f;
+          } else {
             float v16[16], v4[4];
-            tc::tmem_ld16(tstash + i * 20, v16);
-            tc::tmem_ld4(tstash + i * 20 + 16, v4);
+            tc::tmem_ld16(tstash + i * SV, v16);
+            tc::tmem_ld4(tstash + i * SV + 16, v4);
 #pragma unroll
             for (int j = 0; j < 16; ++j) t[j] = v16[j];
 #pragma unroll
@@ -290,18 +485,15 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
 #pragma unroll
               for (int j = 0; j < NCOLB; ++j) dp[j * MPAD] = dl[j];
             }
-            if (l <= L - 3) {
+            if (SV == 20 && l <= L - 3) {
               float* ap = a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
               for (int j = 0; j < NCOLB; ++j) ap[j * MPAD] = pv[j];
             }
           }
-          if (l >= 1) {
-#pragma unroll
-            for (int j = 0; j < NCOLB; ++j) tc_put_b<C>(Bs, cl * NCOLB + j, m, dl[j]);
-          }
+          if (l >= 1) put_b10(cl, dl);
           s_db += dl[0];
-          if (top) {
+          if (SV == 20 && top) {
             const float dL[NCOLB] = {sd[0], valid ? 1.f : 0.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
             float v = 0.f;
 #pragma unroll
@@ -314,6 +506,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             s_w0[2] += w0p[2];
           }
         }
+        if (!top) ptimer.end_b();
         if (l >= 1) {
           tc_epi_arrive(bars);
         } else if (!top) {
@@ -340,7 +533,12 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     acc_dW0[m * 3 + 1] = r_dW0[1];
     acc_dW0[m * 3 + 2] = r_dW0[2];
     if (m == 0) acc_dbL[0] = r_dbL;
-    ptimer.report("bwd_tc", et == 0);
+#ifdef FDSDF_PHASE_TIMING
+    if (blockIdx.x == 0 && (et == 0 || et == C::NEPI * 32 - 32))
+      printf("[phase] bwd_tc (thread %d): tile-start phase %.0f cyc/tile, next-tile top work %.0f cyc/tile\n", (int)threadIdx.x,
+             (double)t_tstart / t_tstart_n, (double)t_top / t_tstart_n);
+#endif
+    ptimer.report("bwd_tc", et == 0 || et == C::NEPI * 32 - 32);
   }
   tc_teardown<C>(tbase);
 }

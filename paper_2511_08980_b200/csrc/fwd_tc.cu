@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
             }
           }
         }
+        if (l > 0) ptimer.end_b();
         if (!last) {  // this split's B operand of layer l+1 (this warp's part): hand to the MMA thread
           tc_epi_arrive(bars, sp);
         } else if (l > 0) {
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
 #pragma unroll
       for (int q = 0; q < NLOSS; ++q) a.lossp[(size_t)blockIdx.x * NLOSS + q] = lacc[q];
     }
-    ptimer.report(MODE == 1 ? "fwd_tc centre" : "fwd_tc pairs", et == 0);
+    ptimer.report(MODE == 1 ? "fwd_tc centre" : "fwd_tc pairs", et == 0 || et == C::NEPI * 32 - 32);
   }
 
   tc_teardown<C>(tbase);

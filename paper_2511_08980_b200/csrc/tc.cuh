@@ -160,6 +160,51 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, float (&v)[2]) {
   v[1] = __uint_as_float(r1);
 }
 
+// columns taddr + 8 j, j = 0..9 (one 32-bit column each, a single wait)
+__device__ __forceinline__ void tmem_ld10_stride8(uint32_t taddr, float (&v)[10]) {
+  uint32_t r[10];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%10];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%1}, [%11];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%2}, [%12];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%3}, [%13];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%4}, [%14];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%5}, [%15];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%6}, [%16];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%7}, [%17];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%8}, [%18];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%9}, [%19];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9])
+      : "r"(taddr), "r"(taddr + 8), "r"(taddr + 16), "r"(taddr + 24), "r"(taddr + 32), "r"(taddr + 40),
+        "r"(taddr + 48), "r"(taddr + 56), "r"(taddr + 64), "r"(taddr + 72)
+      : "memory");
+#pragma unroll
+  for (int j = 0; j < 10; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// columns ta + 8 j and tb + 8 j, j = 0..9, summed pairwise (two accumulator ranges), one wait
+__device__ __forceinline__ void tmem_ld10x2_stride8(uint32_t ta, uint32_t tb, float (&v)[10]) {
+  uint32_t r[20];
+#define FDSDF_LD1(i, t) "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%" #i "}, [%" #t "];\n\t"
+  asm volatile(FDSDF_LD1(0, 20) FDSDF_LD1(1, 21) FDSDF_LD1(2, 22) FDSDF_LD1(3, 23) FDSDF_LD1(4, 24)
+                   FDSDF_LD1(5, 25) FDSDF_LD1(6, 26) FDSDF_LD1(7, 27) FDSDF_LD1(8, 28) FDSDF_LD1(9, 29)
+                       FDSDF_LD1(10, 30) FDSDF_LD1(11, 31) FDSDF_LD1(12, 32) FDSDF_LD1(13, 33) FDSDF_LD1(14, 34)
+                           FDSDF_LD1(15, 35) FDSDF_LD1(16, 36) FDSDF_LD1(17, 37) FDSDF_LD1(18, 38)
+                               FDSDF_LD1(19, 39) "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                 "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19])
+               : "r"(ta), "r"(ta + 8), "r"(ta + 16), "r"(ta + 24), "r"(ta + 32), "r"(ta + 40), "r"(ta + 48),
+                 "r"(ta + 56), "r"(ta + 64), "r"(ta + 72), "r"(tb), "r"(tb + 8), "r"(tb + 16), "r"(tb + 24),
+                 "r"(tb + 32), "r"(tb + 40), "r"(tb + 48), "r"(tb + 56), "r"(tb + 64), "r"(tb + 72)
+               : "memory");
+#undef FDSDF_LD1
+#pragma unroll
+  for (int j = 0; j < 10; ++j) v[j] = __uint_as_float(r[j]) + __uint_as_float(r[10 + j]);
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(

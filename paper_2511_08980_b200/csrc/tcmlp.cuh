@@ -55,7 +55,7 @@ struct TcCfg {
   static constexpr int STASH = STASH_;
   static constexpr int TUSE = MH * DH + STASH;
   static constexpr uint32_t TCOLS = TUSE <= 32 ? 32 : TUSE <= 64 ? 64 : TUSE <= 128 ? 128 : TUSE <= 256 ? 256 : 512;
-  static_assert(RANGES == 1 || RANGES == 3, "one accumulator range (6 MMAs) or three (3 MMAs)");
+  static_assert(RANGES >= 1 && RANGES <= 3, "one accumulator range (6 MMAs), two (4 MMAs) or three (3 MMAs)");
   static_assert(NS % 16 == 0 && NS >= 16 && RANGES * NS <= 256, "tcgen05 M=128 needs N % 16 == 0, <= 256");
   static_assert(NSPLIT == 1 || NSPLIT == 2, "one or two column splits");
   static_assert(TUSE <= 512, "TMEM has 512 columns");
@@ -151,16 +151,28 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
   constexpr uint32_t id3 = tc::idesc_bf16(128, 3 * C::NS), id2 = tc::idesc_bf16(128, 2 * C::NS),
                      id1 = tc::idesc_bf16(128, C::NS);
   uint32_t it = 0, nb = 0;
+#ifdef FDSDF_PHASE_TIMING
+  long long t0 = clock64(), tb = 0, tw = 0, tspan = 0, tm;
+#define TC_MMA_T(acc, stmt) \
+  tm = clock64();           \
+  stmt;                     \
+  acc += clock64() - tm;
+#else
+#define TC_MMA_T(acc, stmt) stmt;
+#endif
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
     for (int gs = 0; gs < ngemm * C::NSPLIT; ++gs, ++nb) {
       const int sp = gs % C::NSPLIT;  // column split of this pass
-      mbar_wait(&b.bfull[sp], (nb / C::NSPLIT) & 1u);
+      TC_MMA_T(tb, mbar_wait(&b.bfull[sp], (nb / C::NSPLIT) & 1u));
+#ifdef FDSDF_PHASE_TIMING
+      const long long tstart = clock64();
+#endif
       tc::fence_after();
       for (int kc = 0; kc < C::KC; ++kc)
         for (int h = 0; h < C::MH; ++h, ++it) {
           const int s = (int)(it % C::NST);
           const uint32_t ph = (it / C::NST) & 1u;
-          mbar_wait(&b.wfull[s], ph);
+          TC_MMA_T(tw, mbar_wait(&b.wfull[s], ph));
           tc::fence_after();
           const uint32_t wa = smem_u32(Ws + s * C::STAGE);
           const uint32_t ba = smem_u32(Bs + kc * C::BKC + sp * 3 * C::NS * 128);
@@ -172,6 +184,18 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
               tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
               tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
               if (C::WPK == 3) tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+            }
+          } else if (C::RANGES == 2) {
+            // a0 . [b0|b1] and a1 . [b0|b1] (N = 2N: ranges 0, 1), then a0 . b2 and a2 . b0
+            // (N = N: range 0) -- the six products, four A reads per K step instead of six
+#pragma unroll
+            for (int sub = 0; sub < 4; ++sub) {
+              const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);
+              const uint64_t b2 = tc::sdesc_sw128(ba + 2 * C::NS * 128 + sub * 32);
+              tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b01, id2, (kc | sub) != 0 ? 1u : 0u);
+              tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), b01, id2, 1u);
+              tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b2, id1, 1u);
+              tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), b01, id1, 1u);
             }
           } else {  // the six piece products into one range
 #pragma unroll
@@ -185,7 +209,18 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
           tc::mma_commit(&b.wempty[s]);
         }
       tc::mma_commit(&b.dfull[sp]);
+#ifdef FDSDF_PHASE_TIMING
+      tspan += clock64() - tstart;
+#endif
     }
+#ifdef FDSDF_PHASE_TIMING
+  if (blockIdx.x == 0)
+    printf("[phase] mma thread: total %lld cyc, %u passes, waiting for B %lld (%.0f/pass), issue span %lld (%.0f/pass) "
+           "of which waiting for W stages %lld (%.0f/pass)\n",
+           clock64() - t0, nb, tb, nb ? (double)tb / nb : 0.0, tspan, nb ? (double)tspan / nb : 0.0, tw,
+           nb ? (double)tw / nb : 0.0);
+#endif
+#undef TC_MMA_T
 }
 
 // Debug-build phase timer (-DFDSDF_PHASE_TIMING): epilogue thread 0 of CTA 0 accumulates the
@@ -193,7 +228,7 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
 // between D full and its next hand-over (the epilogue phase), and prints them at kernel end.
 struct PhaseTimer {
 #ifdef FDSDF_PHASE_TIMING
-  long long t_mark = 0, wait = 0, work = 0, first = 0;
+  long long t_mark = 0, wait = 0, work = 0, first = 0, t_b = 0, bwork = 0;
   int n = 0;
   __device__ __forceinline__ void start() { t_mark = first = clock64(); }
   __device__ __forceinline__ void before_wait() {
@@ -204,19 +239,23 @@ struct PhaseTimer {
   __device__ __forceinline__ void after_wait() {
     const long long t = clock64();
     wait += t - t_mark;
-    t_mark = t;
+    t_mark = t_b = t;
     ++n;
   }
+  // end of the post-wait part of the epilogue (phase B)
+  __device__ __forceinline__ void end_b() { bwork += clock64() - t_b; }
   __device__ __forceinline__ void report(const char* name, bool who) {
     if (who && blockIdx.x == 0)
-      printf("[phase] %s: total %lld cyc, waiting for D %lld (%.1f%%), epilogue %lld, %d waits, %.0f cyc/wait\n",
-             name, clock64() - first, wait, 100.0 * wait / (double)(clock64() - first), work, n,
-             n ? (double)wait / n : 0.0);
+      printf("[phase] %s (thread %d): total %lld cyc, waiting for D %lld (%.1f%%), epilogue %lld (post-wait %lld), "
+             "%d waits, %.0f cyc/wait, %.0f post-wait cyc/wait\n",
+             name, (int)threadIdx.x, clock64() - first, wait, 100.0 * wait / (double)(clock64() - first), work, bwork,
+             n, n ? (double)wait / n : 0.0, n ? (double)bwork / n : 0.0);
   }
 #else
   __device__ __forceinline__ void start() {}
   __device__ __forceinline__ void before_wait() {}
   __device__ __forceinline__ void after_wait() {}
+  __device__ __forceinline__ void end_b() {}
   __device__ __forceinline__ void report(const char*, bool) {}
 #endif
 };
@@ -245,6 +284,7 @@ __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float 
 // TMEM ranges (range 0 + (range 1 + range 2), smallest terms first)
 template <class C>
 __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8]) {
+  static_assert(C::RANGES != 2, "two-range accumulators: sum the ranges at the call site");
   if (C::RANGES == 1) {
     tc::tmem_ld8(taddr + col, v);
     return;
@@ -275,6 +315,7 @@ __device__ __forceinline__ void tc_ld_sum_frag(uint32_t taddr, int col, float (&
 
 template <class C>
 __device__ __forceinline__ void tc_ld_sum2(uint32_t taddr, int col, float (&v)[2]) {
+  static_assert(C::RANGES != 2, "two-range accumulators: sum the ranges at the call site");
   if (C::RANGES == 1) {
     tc::tmem_ld2(taddr + col, v);
     return;

@@ -231,3 +231,76 @@ extern "C" fdsdf_status fdsdf_selftest_mma_pair(const float* d_W, const float* d
   tcprobe2_kernel<<<2, 256, smem, (cudaStream_t)stream>>>(d_W, d_B, d_D, N, K);
   return cudaGetLastError() == cudaSuccess ? FDSDF_OK : FDSDF_E_CUDA;
 }
+
+// ----------------------------------------------------------------------------- MMA issue rate
+// Diagnostic (not part of include/fdsdf.h; called by scripts/mma_rate.py): cycles per 16-wide
+// K step of one CTA issuing the six bf16x6 piece products back to back in different shapes,
+//   mode 0: six MMAs a_i . b_j, N = n each, one accumulator range
+//   mode 1: a0 . [b0|b1|b2] (3n), a1 . [b0|b1] (2n), a2 . b0 (n)      -> three ranges
+//   mode 2: a0 . [b0|b1] (2n), a1 . [b0|b1] (2n), a0 . b2 (n), a2 . b0 (n) -> two ranges
+//   mode 3: one MMA a0 . b0 (N = n) per K step (reference rate)
+// Operands are zero; the timing does not depend on the values.
+namespace fdsdf {
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int mode, int n, int iters, long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw;
+  base += (1024 - (smem_u32(base) & 1023)) & 1023;
+  unsigned char* As = base;                    // 3 pieces x [128 rows x 128 B]
+  unsigned char* Bs = As + 3 * 16384;          // 3 pieces x [n rows x 128 B]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + 3 * n * 128 + 1024);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (3 * 16384 + 3 * n * 128) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(As)[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, 512);
+  fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t d = *tslot;
+  if (tid == 32) {
+    const uint32_t a = smem_u32(As), b = smem_u32(Bs);
+    const uint32_t i1 = tc::idesc_bf16(128, n), i2 = tc::idesc_bf16(128, 2 * n), i3 = tc::idesc_bf16(128, 3 * n);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int sub = 0; sub < 4; ++sub) {
+        auto A = [&](int p) { return tc::sdesc_sw128(a + p * 16384 + sub * 32); };
+        auto B = [&](int p) { return tc::sdesc_sw128(b + p * n * 128 + sub * 32); };
+        if (mode == 0) {
+#pragma unroll
+          for (int q = 0; q < 6; ++q) tc::mma_bf16(d, A(tc::prod_a(q)), B(tc::prod_b(q)), i1, 1u);
+        } else if (mode == 1) {
+          tc::mma_bf16(d, A(0), B(0), i3, 1u);
+          tc::mma_bf16(d, A(1), B(0), i2, 1u);
+          tc::mma_bf16(d, A(2), B(0), i1, 1u);
+        } else if (mode == 2) {
+          tc::mma_bf16(d, A(0), B(0), i2, 1u);
+          tc::mma_bf16(d, A(1), B(0), i2, 1u);
+          tc::mma_bf16(d, A(0), B(2), i1, 1u);
+          tc::mma_bf16(d, A(2), B(0), i1, 1u);
+        } else {
+          tc::mma_bf16(d, A(0), B(0), i1, 1u);
+        }
+      }
+    tc::mma_commit(bar);
+    mbar_wait(bar, 0);
+    out[0] = clock64() - t0;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(d, 512);
+}
+}  // namespace fdsdf
+
+extern "C" int fdsdf_probe_mma_rate(int mode, int n, int iters, long long* d_out) {
+  const int bytes = 3 * 16384 + 3 * n * 128 + 2048 + 64;
+  auto k = fdsdf::mma_rate_kernel;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 1;
+  k<<<1, 128, bytes>>>(mode, n, iters, d_out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 2;
+}

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfdsdf.so")
+# FDSDF_LIB: an alternative build of the same library (A/B timing of compile-time variants)
+LIB_PATH = os.environ.get("FDSDF_LIB") or os.path.join(_PKG, "libfdsdf.so")
 
 MAX_LINEAR = 16
 ACT = {"softplus": 0, "sine": 1}

@@ -1,0 +1,22 @@
+"""Cycles per 16-wide K step of the bf16x6 product shapes (tcprobe.cu fdsdf_probe_mma_rate)."""
+import ctypes as C
+import sys
+import torch
+sys.path.insert(0, ".")
+from paper_2511_08980_b200 import fdsdf
+
+L = fdsdf.lib()
+L.fdsdf_probe_mma_rate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+out = torch.zeros(1, dtype=torch.int64, device="cuda")
+names = {0: "1-range 6 x N", 1: "3-range 3N,2N,N", 2: "2-range 2N,2N,N,N", 3: "single N"}
+for n in (32, 48, 64, 80):
+    for mode in (3, 0, 1, 2):
+        if mode == 1 and 3 * n > 256:
+            continue
+        iters = 400
+        assert L.fdsdf_probe_mma_rate(mode, n, iters, out.data_ptr()) == 0
+        assert L.fdsdf_probe_mma_rate(mode, n, iters, out.data_ptr()) == 0
+        cyc = out.item() / (iters * 4)
+        nsum = {0: 6 * n, 1: 6 * n, 2: 6 * n, 3: n}[mode]
+        floor = 128 * nsum / 256
+        print(f"N={n:3d} {names[mode]:20s} {cyc:7.1f} cyc/kstep  floor {floor:6.1f}  ratio {cyc / floor:4.2f}")
