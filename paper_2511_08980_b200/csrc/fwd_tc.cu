@@ -41,11 +41,22 @@ namespace fdsdf {
 #ifndef FWD_TC_PAIR_WPK
 #define FWD_TC_PAIR_WPK 3
 #endif
+// 1: layer 0 of tile t+1 (fan-in 3, no MMA) is computed in tile t's MMA phases and parked in
+// spare TMEM columns, so a tile starts with a split of the parked outputs into the B operand
+// instead of a full epilogue pass with the tensor cores idle
+#ifndef FWD_TC_PIPE0
+#define FWD_TC_PIPE0 1
+#endif
+constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && !FWD_TC_FRAG && FWD_TC_NSPLIT == 1;
 // mode 1 (centre + tangents: they set g, the frames and the |g|^p denominators) streams all
 // three weight pieces; mode 2 (the stencil-pair differences) streams FWD_TC_PAIR_WPK
 template <int MPAD, int MODE>
-struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT, MODE == 1 ? 3 : FWD_TC_PAIR_WPK> {
-  using B = TcCfg<MPAD, 64, FWD_TC_NEPI, 3, 0, FWD_TC_NSPLIT, MODE == 1 ? 3 : FWD_TC_PAIR_WPK>;
+struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI, 3, FWD_PIPE0 ? 64 * (MPAD / 128) : 0, FWD_TC_NSPLIT,
+                      MODE == 1 ? 3 : FWD_TC_PAIR_WPK> {
+  // TMEM stash (FWD_PIPE0): the next tile's layer-0 outputs, (MH x EG thread groups) x CPE x
+  // columns per centre = MH x 64 columns
+  using B = TcCfg<MPAD, 64, FWD_TC_NEPI, 3, FWD_PIPE0 ? 64 * (MPAD / 128) : 0, FWD_TC_NSPLIT,
+                  MODE == 1 ? 3 : FWD_TC_PAIR_WPK>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
@@ -170,6 +181,95 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
       return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
     };
     auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
+    // this thread's stash columns: CPE centres x CPC values (FWD_PIPE0)
+    const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + MH * C::DH + (hh * C::EG + eg) * CPE * CPC;
+    const bool pipe0 = FWD_PIPE0 && ngemm > 0;
+    // layer 0 of centre i of tile tl (centre info cis_t): pre-activations -> zf, activations ->
+    // this thread's stash columns (exactly the l == 0 arithmetic of the epilogue below)
+    auto layer0_centre = [&](int64_t tl, int i, const float* cis_t) {
+      if (tl >= a.ntiles) return;
+      const int cl = eg + C::EG * i;
+      const int64_t c = tl * CT + cl;
+      const bool valid = c < a.n;
+      const float om = net.omega[0];
+      const bool mok = m < net.width[1];
+      if (MODE == 1) {
+        float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+        if (valid) {
+          x0 = a.x[c * 3 + 0];
+          x1 = a.x[c * 3 + 1];
+          x2 = a.x[c * 3 + 2];
+          if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
+        }
+        if (mok) {
+          const float* W0 = net.W[0];
+          const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+          z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + net.b[0][m]);
+          t0 = om * w0;
+          t1 = om * w1;
+          t2 = om * w2;
+        }
+        if (valid) {
+          *zp(c, 0, 0) = z;
+          if (step) {
+            *zp(c, 0, 1) = t0;
+            *zp(c, 0, 2) = t1;
+            *zp(c, 0, 3) = t2;
+          }
+        }
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        if (mok) {
+          const typename AF::C cc = AF::centre(z, beta);
+          const float s1 = AF::d1(cc, beta);
+          o[0] = AF::value(cc, beta);
+          o[1] = s1 * t0;
+          o[2] = s1 * t1;
+          o[3] = s1 * t2;
+        }
+        tc::tmem_st4(tstash + i * CPC, o);
+      } else {
+        const float* ci = cis_t + cl * NCINFO;
+        const float z0 = valid ? __ldg(zp(c, 0, 0)) : 0.f;
+        float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
+        if (mok) {
+          const float* W0 = net.W[0];
+          const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+          const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
+          const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
+          const float hs = om * h;
+          Av[0] = hs * du;
+          Av[1] = hs * dv;
+          Av[2] = hs * (du + dv);
+          Av[3] = hs * (du - dv);
+        }
+        if (step && valid) {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            *zp(c, 0, 4 + 2 * p) = Av[p];
+            *zp(c, 0, 5 + 2 * p) = Sv[p];
+          }
+        }
+        float o[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) o[p] = 0.f;
+        if (mok) {
+          const typename AF::C cc = AF::centre(z0, beta);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &o[2 * p], &o[2 * p + 1]);
+        }
+        float o4[4] = {o[0], o[1], o[2], o[3]};
+        tc::tmem_st4(tstash + i * CPC, o4);
+        o4[0] = o[4];
+        o4[1] = o[5];
+        o4[2] = o[6];
+        o4[3] = o[7];
+        tc::tmem_st4(tstash + i * CPC + 4, o4);
+      }
+    };
+    // the MMA phases of a tile that also run the next tile's layer 0 (mode 2: from layer 2 on,
+    // once warp 2's copy of the next tile's centre info has landed)
+    const int l0first = (MODE == 2 && ngemm >= 2) ? 2 : 1;
 
     // per-centre epilogue of a finished tile (warp 2 only: et < CT <= 16): mode 1 -> f, g, mask,
     // frame, cinfo; mode 2 -> FD entries, D, K, Eq. (1) terms, seeds, and the fixed-order
@@ -262,6 +362,28 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         // while the epilogue continues with the next split of layer l
         constexpr int CPSPL = CT / C::NSPLIT;   // centres per split
         constexpr int CPEs = CPE / C::NSPLIT;   // centres per thread per split
+        if (l == 0 && pipe0) {
+          // B operand of layer 1 from the parked layer-0 outputs (computed here only for the
+          // CTA's first tile)
+          if (tile == blockIdx.x) {
+            for (int i = 0; i < CPE; ++i) layer0_centre(tile, i, cis);
+            tc::tmem_wait_st();
+          }
+#pragma unroll 1
+          for (int i = 0; i < CPE; ++i) {
+            const int cl = eg + C::EG * i;
+            float o4[4];
+            tc::tmem_ld4(tstash + i * CPC, o4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) put_b(cl * CPC + j, o4[j]);
+            if (CPC == 8) {
+              tc::tmem_ld4(tstash + i * CPC + 4, o4);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) put_b(cl * CPC + 4 + j, o4[j]);
+            }
+          }
+          tc_epi_arrive(bars, 0);
+        } else
         for (int sp = 0; sp < C::NSPLIT; ++sp) {
         // mode 2: the centre pre-activation of this neuron, prefetched one centre ahead
         auto ldz = [&](int i) -> float {
@@ -269,6 +391,16 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           return (MODE == 2 && i < CPEs && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
         };
         float z0n = ldz(0);
+        if (pipe0 && l >= l0first) {  // the next tile's layer 0, spread over this tile's MMA phases
+          if (MODE == 2 && l == l0first) {
+            if (ew == 0) cp_async_wait_all();
+            bar_named(1, C::NEPI * 32);  // the next tile's centre info is in
+          }
+#pragma unroll 1
+          for (int i = l - l0first; i < CPE; i += L - 1 - l0first)
+            layer0_centre(tile + gridDim.x, i, cis0 + (tpar ^ 1u) * C::CI_N);
+          tc::tmem_wait_st();
+        }
         if (l > 0) {
           ptimer.before_wait();
           mbar_wait(&bars.dfull[sp], nd & 1u);
