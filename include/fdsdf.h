@@ -155,6 +155,9 @@ enum {
                                 /* Neither flag: the tensor path where supported, else FFMA.  */
                                 /* Both flags -> FDSDF_E_INVALID.                             */
 };
+/* Environment read at create time: FDSDF_MAX_SM=k (k >= 2) caps the persistent grids at k
+ * SMs (GPU sharing; the tests use it to run many tiles per CTA at oracle-sized inputs);
+ * FDSDF_PAIR=1 selects the CTA-pair forward kernels.                        */
 fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_centers,
                           uint32_t flags, fdsdf_ctx** out);
 

@@ -279,6 +279,10 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
   c->max_centers = max_centers;
   c->eval_only = (flags & FDSDF_CREATE_EVAL_ONLY) != 0;
   c->nsm = prop.multiProcessorCount;
+  if (const char* ev = getenv("FDSDF_MAX_SM")) {  // cap the persistent grids (fdsdf.h)
+    const int k = atoi(ev);
+    if (k >= 2 && k < c->nsm) c->nsm = k;
+  }
   c->ftile = fwd_tile_centres(c->mpad);
   c->btile = bwd_tile_centres(c->mpad);
 
