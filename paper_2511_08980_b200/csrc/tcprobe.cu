@@ -304,3 +304,49 @@ extern "C" int fdsdf_probe_mma_rate(int mode, int n, int iters, long long* d_out
   k<<<1, 128, bytes>>>(mode, n, iters, d_out);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 2;
 }
+
+// ----------------------------------------------------------------------------- TMEM load rate
+// Diagnostic: `nw` warps each issue `iters` x (tcgen05.ld 32x32b.x`W` + wait::ld) on their lane
+// quarter; returns the CTA's cycles.  Bytes moved = nw * iters * 32 lanes * W * 4.
+namespace fdsdf {
+template <int W>
+__global__ void tmem_rate_kernel(int iters, long long* out, float* sink) {
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tc::tmem_alloc(&tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t t = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (warp >> 2) * 32;
+  float acc = 0.f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float v[8];
+    if (W == 8) {
+      tc::tmem_ld8(t + (it & 7) * 8, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    } else {
+      float w[16];
+      tc::tmem_ld16(t + (it & 1) * 16, w);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc += w[j];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[0] = clock64() - t0;
+  if (acc == 12345.f) sink[0] = acc;
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tslot, 512);
+}
+}  // namespace fdsdf
+
+extern "C" int fdsdf_probe_tmem_rate(int width, int nwarps, int iters, long long* d_out, float* d_sink) {
+  if (width == 8)
+    fdsdf::tmem_rate_kernel<8><<<1, nwarps * 32>>>(iters, d_out, d_sink);
+  else
+    fdsdf::tmem_rate_kernel<16><<<1, nwarps * 32>>>(iters, d_out, d_sink);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 2;
+}

@@ -20,3 +20,15 @@ for n in (32, 48, 64, 80):
         nsum = {0: 6 * n, 1: 6 * n, 2: 6 * n, 3: n}[mode]
         floor = 128 * nsum / 256
         print(f"N={n:3d} {names[mode]:20s} {cyc:7.1f} cyc/kstep  floor {floor:6.1f}  ratio {cyc / floor:4.2f}")
+
+# TMEM load throughput (tcprobe.cu fdsdf_probe_tmem_rate)
+L.fdsdf_probe_tmem_rate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+sink = torch.zeros(1, device="cuda")
+for width in (8, 16):
+    for nw in (4, 8, 16):
+        iters = 2000
+        assert L.fdsdf_probe_tmem_rate(width, nw, iters, out.data_ptr(), sink.data_ptr()) == 0
+        assert L.fdsdf_probe_tmem_rate(width, nw, iters, out.data_ptr(), sink.data_ptr()) == 0
+        cyc = out.item()
+        byts = nw * iters * 32 * width * 4
+        print(f"tcgen05.ld x{width:2d} {nw:2d} warps: {byts / cyc:6.1f} B/cycle  ({cyc / iters:6.1f} cyc per warp-load round)")
