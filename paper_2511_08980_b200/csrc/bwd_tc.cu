@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
   if (warp == 0) {
     if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 1, a.ntiles, Ws, bars);
   } else if (warp == 1) {
-    if (lane == 0 && ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
+    if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
   } else {
     const int ew = warp - 2;
     const int et = tid - 64;

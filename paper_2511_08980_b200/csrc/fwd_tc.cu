@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
   if (warp == 0) {
     if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 0, a.ntiles, Ws, bars);
   } else if (warp == 1) {
-    if (lane == 0 && ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
+    if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
   } else {
     // ------------------------------------------------------------------ epilogue warps
     const int ew = warp - 2;                 // 0..7

@@ -2,11 +2,26 @@
 // slots in flight (tcpair.cuh).  Same arithmetic as fwd_tc.cu (modes 1 and 2, bf16x6, the
 // cancellation-free pair maps, fdepi.cuh epilogues); what changes is the schedule:
 //   * a pair tile = 2 slots of CPS centres (mode 1: 16 centres x 4 columns, mode 2: 8 centres
-//     x 8 pair columns); each slot is a 64-column GEMM on the pair (M = 256 over 2 SMs);
+//     x 8 pair columns); each slot is a 64-column GEMM on the pair (M = 256 over 2 SMs, each SM
+//     computing its 128 output neurons for all 64 columns);
 //   * per layer the leader issues slot 0's MMAs, then slot 1's, while the 16 epilogue warps of
 //     each CTA process the other slot -- the MMA phase of one slot overlaps the epilogue of the
 //     other (the single-CTA kernels serialise them);
 //   * each CTA streams only its 128 weight rows: 192 KB per slot-layer instead of 384 KB;
+//   * the six bf16x6 products are issued as four M = 256 MMAs per K step into two TMEM
+//     regions, R01 = a0.[b0|b1] + a1.[b0|b1] (N = 128) and R2 = a0.b2 + a2.b0 (N = 64): on a
+//     pair one MMA does twice the work of a single-CTA one for the same issue cost
+//     (scripts/mma_rate.py: 128 cycles per K step and M = 128 half, against 204 for the
+//     single-CTA three-range form);
+//   * operand hand-off: CTA r holds the B columns [32 r, 32 r + 32) of a slot for all 256 K
+//     rows, but its epilogue threads produce K rows [128 r, 128 r + 128) for all 64 columns.
+//     The peer's columns are written into a local 24 KB staging block laid out exactly as the
+//     peer's B rows [128 r, ...), and a dedicated exchanger warp moves it with ONE
+//     cp.async.bulk shared::cta -> shared::cluster per slot-layer (complete_tx on the peer's
+//     mbarrier).  Everything the tensor cores read is then written either by local generic
+//     stores behind fence.proxy.async.shared::cta or by the async proxy -- no cluster-scope
+//     generic-proxy fence (MEMBAR.ALL.GPU) on the path, which is what made the first pair
+//     version (remote st.shared::cluster per element) slower than the single-CTA kernel;
 //   * the last-layer sums over the 256 neurons are reduced across the pair through distributed
 //     shared memory into the CTA that owns the centre, whose first epilogue warp runs the
 //     per-centre epilogue (frame / FD, Eq. (1) terms, seeds) during the next tile's first MMA
@@ -30,20 +45,27 @@ struct F2Cfg {
   static constexpr int COWN = NH / CPC;                 // centres per slot owned by one CTA
   static constexpr int STAGE = 3 * 128 * 128;           // weight stage: this CTA's 128 rows
   static constexpr int NST = 2;
-  static constexpr int BSLOT = KC * 3 * NH * 128;       // B block of one slot in one CTA
+  static constexpr int BSLOT = KC * 3 * NH * 128;       // B block of one slot in one CTA (48 KB)
+  static constexpr int STG = 2 * 3 * NH * 128;          // staging: the peer's columns, 2 K chunks
   static constexpr int NEPI = 16;
-  static constexpr int NTHR = (2 + NEPI) * 32;
+  static constexpr int XW = 2 + NEPI;                   // the exchanger warp
+  static constexpr int NTHR = (3 + NEPI) * 32;
   static constexpr int CPT = CPS / 4;                   // centres per epilogue thread per slot
   static constexpr int NRED = 8 * CPS * 4;              // floats per (parity, slot) reduction block
+  static constexpr int DSL = 3 * NS;                    // TMEM columns per slot: R01 (2 NS), R2 (NS)
   static constexpr int OFF_W = 0;
   static constexpr int OFF_B = NST * STAGE;
-  static constexpr int OFF_RED = OFF_B + 2 * BSLOT;     // float [2 par][2 slot][8 grp][CPS][4]
-  static constexpr int OFF_CI = OFF_RED + 4 * NRED * 4; // float [2 par][2 slot][CPS][16]
-  static constexpr int OFF_LV = OFF_CI + 4 * CPS * NCINFO * 4;
-  static constexpr int OFF_BAR = OFF_LV + 2 * CPS * NLOSS * 8;
-  static constexpr int NBAR = 2 * NST + NST + 2 + 2 + 4;  // wfull, wempty, wpeer, bfull, dfull, rfull
+  static constexpr int OFF_ST = OFF_B + 2 * BSLOT;
+  static constexpr int OFF_RED = OFF_ST + STG;          // float [2 par][2 slot][8 grp][CPS][4]
+  static constexpr int OFF_CI = OFF_RED + 4 * NRED * 4; // mode 2: float [2 par][2 slot][CPS][16]
+  static constexpr int OFF_LV = OFF_CI + (MODE == 2 ? 4 * CPS * NCINFO * 4 : 0);
+  static constexpr int OFF_BAR = OFF_LV + (MODE == 2 ? 2 * CPS * NLOSS * 8 : 0);
+  // wfull, wempty, wpeer [NST]; bfull, dfull [2]; rfull [4]; sready, bin [2]; sfree
+  static constexpr int NBAR = 3 * NST + 2 + 2 + 4 + 2 + 2 + 1;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;
-  static constexpr uint32_t TCOLS = 2 * NS <= 128 ? 128 : 256;
+  static constexpr uint32_t TCOLS = 512;
+  static_assert(2 * DSL <= (int)TCOLS, "two slots of R01 + R2");
+  static_assert(BYTES <= 232448, "shared memory per CTA");
 };
 
 int fwd_tc2_tile_centres(int mode) { return mode == 1 ? 32 : 16; }
@@ -60,6 +82,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
   sm += (1024 - (smem_u32(sm) & 1023)) & 1023;
   unsigned char* Ws = sm + C::OFF_W;
   unsigned char* Bs = sm + C::OFF_B;
+  unsigned char* Stg = sm + C::OFF_ST;
   float* red0 = reinterpret_cast<float*>(sm + C::OFF_RED);
   float* cis0 = reinterpret_cast<float*>(sm + C::OFF_CI);
   double* lvs = reinterpret_cast<double*>(sm + C::OFF_LV);
@@ -69,7 +92,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
   uint64_t* bfull = wpeer + C::NST;
   uint64_t* dfull = bfull + 2;
   uint64_t* rfull = dfull + 2;  // [par][slot]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(rfull + 4);
+  uint64_t* sready = rfull + 4;
+  uint64_t* bin = sready + 2;
+  uint64_t* sfree = bin + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sfree + 1);
 
   const Net& net = a.net;
   const int L = net.L;
@@ -86,10 +112,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
       mbar_init(&wpeer[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&bfull[s], 2 * C::NEPI);
+      mbar_init(&bfull[s], 2);  // one arrival per CTA of the pair: its B half is complete
       mbar_init(&dfull[s], 1);
+      mbar_init(&sready[s], C::NEPI);
+      mbar_init(&bin[s], 1);
     }
     for (int s = 0; s < 4; ++s) mbar_init(&rfull[s], 2 * C::NEPI);
+    mbar_init(sfree, 1);
     fence_mbar_init();
   }
   if (warp == 1) tp::tmem_alloc2(tslot, C::TCOLS);
@@ -114,36 +143,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
             }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
       // ---------------------------------------------------------------- MMA issuer (leader)
-      constexpr uint32_t idesc = tc::idesc_bf16(256, NS);
+      // the whole warp runs the issue loop (warp-uniform descriptors in uniform registers);
+      // one elected lane issues each tcgen05.mma / commit
+      constexpr uint32_t id2 = tc::idesc_bf16(256, 2 * NS), id1 = tc::idesc_bf16(256, NS);
       uint32_t it = 0, nb[2] = {0u, 0u};
+#ifdef FDSDF_PHASE_TIMING
+      long long t0 = clock64(), tb = 0, tw = 0, tspan = 0, tm;
+#endif
       for (int64_t tile = cid; tile < a.ntiles; tile += ncl)
         for (int g = 0; g < ngemm; ++g)
           for (int slot = 0; slot < 2; ++slot) {
+#ifdef FDSDF_PHASE_TIMING
+            tm = clock64();
+#endif
             tp::wait_cluster(&bfull[slot], nb[slot] & 1u);
+#ifdef FDSDF_PHASE_TIMING
+            const long long tstart = clock64();
+            tb += tstart - tm;
+#endif
             ++nb[slot];
             tc::fence_after();
             const uint32_t bslot = smem_u32(Bs + slot * C::BSLOT);
+            const uint32_t d01 = tbase + slot * C::DSL, d2 = d01 + 2 * NS;
             for (int kc = 0; kc < C::KC; ++kc, ++it) {
               const int s = (int)(it % C::NST);
               const uint32_t ph = (it / C::NST) & 1u;
+#ifdef FDSDF_PHASE_TIMING
+              tm = clock64();
+#endif
               mbar_wait(&wfull[s], ph);
               tp::wait_cluster(&wpeer[s], ph);
+#ifdef FDSDF_PHASE_TIMING
+              tw += clock64() - tm;
+#endif
               tc::fence_after();
               const uint32_t wa = smem_u32(Ws + s * C::STAGE);
               const uint32_t ba = bslot + kc * (3 * NH * 128);
 #pragma unroll
-              for (int sub = 0; sub < 4; ++sub)
-#pragma unroll
-                for (int q = 0; q < 6; ++q)
-                  tp::mma2(tbase + slot * NS, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
-                           tc::sdesc_sw128(ba + tc::prod_b(q) * NH * 128 + sub * 32), idesc,
-                           (kc | sub | q) != 0 ? 1u : 0u);
-              tp::commit2(&wempty[s]);
+              for (int sub = 0; sub < 4; ++sub) {
+                const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);            // [b0|b1], NH rows each
+                const uint64_t b2 = tc::sdesc_sw128(ba + 2 * NH * 128 + sub * 32);
+                const uint32_t first = (kc | sub) != 0 ? 1u : 0u;
+                tp::mma2_w(d01, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b01, id2, first);
+                tp::mma2_w(d01, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), b01, id2, 1u);
+                tp::mma2_w(d2, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b2, id1, first);
+                tp::mma2_w(d2, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), b01, id1, 1u);
+              }
+              tp::commit2_w(&wempty[s]);
             }
-            tp::commit2(&dfull[slot]);
+            tp::commit2_w(&dfull[slot]);
+#ifdef FDSDF_PHASE_TIMING
+            tspan += clock64() - tstart;
+#endif
           }
+#ifdef FDSDF_PHASE_TIMING
+      if (blockIdx.x == 0 && lane == 0)
+        printf("[phase] pair mma: total %lld, passes %u, wait B %.0f/pass, issue span %.0f/pass, W waits %.0f/pass\n",
+               clock64() - t0, nb[0] + nb[1], (double)tb / (nb[0] + nb[1]), (double)tspan / (nb[0] + nb[1]),
+               (double)tw / (nb[0] + nb[1]));
+#endif
     } else if (lane == 0 && rank == 1) {
       // ---------------------------------------------------------------- stage forwarder (peer)
       uint32_t it = 0;
@@ -157,6 +217,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
               tp::arrive_cluster(wpeer_leader + s * 8);
             }
     }
+  } else if (warp == C::XW) {
+    // ------------------------------------------------------------------ operand exchanger
+    // per hand-off (tile, layer < L-2, slot), in the epilogue's order: once this CTA's B half
+    // and staging block are written, send the staging block to the peer's B rows
+    // [128 rank, ...), wait for the peer's block to land here, then report this CTA's B half
+    // complete to the leader's MMA thread and the peer's staging block free to the peer
+    if (lane == 0 && ngemm > 0) {
+      const uint32_t peer = rank ^ 1u;
+      const uint32_t peer_b = tp::mapa(smem_u32(Bs), peer) + rank * C::STG;
+      const uint32_t peer_bin = tp::mapa(smem_u32(bin), peer);
+      const uint32_t peer_sfree = tp::mapa(smem_u32(sfree), peer);
+      const uint32_t bfull_leader = tp::mapa(smem_u32(bfull), 0);
+      uint32_t ph[2] = {0u, 0u};
+#ifdef FDSDF_PHASE_TIMING
+      long long t0 = clock64(), tr = 0, ti = 0, tm;
+#endif
+      for (int64_t tile = cid; tile < a.ntiles; tile += ncl)
+        for (int l = 0; l < L - 2; ++l)
+          for (int slot = 0; slot < 2; ++slot) {
+#ifdef FDSDF_PHASE_TIMING
+            tm = clock64();
+#endif
+            mbar_wait(&sready[slot], ph[slot] & 1u);
+#ifdef FDSDF_PHASE_TIMING
+            tr += clock64() - tm;
+            tm = clock64();
+#endif
+            mbar_arrive_expect_tx(&bin[slot], C::STG);
+            tp::bulk_s2peer(peer_b + slot * C::BSLOT, Stg, C::STG, peer_bin + slot * 8);
+            mbar_wait(&bin[slot], ph[slot] & 1u);
+#ifdef FDSDF_PHASE_TIMING
+            ti += clock64() - tm;
+#endif
+            ++ph[slot];
+            tp::arrive_cluster(bfull_leader + slot * 8);
+            tp::arrive_cluster(peer_sfree);
+          }
+#ifdef FDSDF_PHASE_TIMING
+      if (blockIdx.x < 2)
+        printf("[phase] pair exchanger rank %u: total %lld, %u hand-offs, waiting for epilogue %.0f/hand-off, copy "
+               "round trip %.0f/hand-off\n",
+               rank, clock64() - t0, ph[0] + ph[1], (double)tr / (ph[0] + ph[1]), (double)ti / (ph[0] + ph[1]));
+#endif
+    }
   } else {
     // ------------------------------------------------------------------ epilogue warps
     const int ew = warp - 2;                          // 0..15
@@ -169,11 +273,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
     const float beta = net.beta;
     const float h = a.h;
     const bool step = a.step != 0;
-    const uint32_t bs_c[2] = {tp::mapa(smem_u32(Bs), 0), tp::mapa(smem_u32(Bs), 1)};
     const uint32_t red_c[2] = {tp::mapa(smem_u32(red0), 0), tp::mapa(smem_u32(red0), 1)};
     const uint32_t rfull_c[2] = {tp::mapa(smem_u32(rfull), 0), tp::mapa(smem_u32(rfull), 1)};
-    const uint32_t bfull_leader = tp::mapa(smem_u32(bfull), 0);
-    uint32_t nd[2] = {0u, 0u}, rph[4] = {0u, 0u, 0u, 0u};
+    uint32_t nd[2] = {0u, 0u}, rph[4] = {0u, 0u, 0u, 0u}, nhand = 0;
     PhaseTimer ptimer;
     ptimer.start();
     double lacc[NLOSS];
@@ -182,6 +284,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
 
     auto zp = [&](int64_t c, int l, int col) -> float* {
       return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
+    };
+    // 8 accumulator columns [c8, c8 + 8) of a slot (pair-wide column numbers, within one owner
+    // CTA's 32): R01 holds owner o's columns as [o][b0 | b1 products][32], R2 as [o][32]
+    auto ld_x8 = [&](int slot, int c8, float (&v)[8]) {
+      const int o = c8 / NH, lc = c8 % NH;
+      const uint32_t t01 = tl + slot * C::DSL + (uint32_t)(o * 2 * NH + lc);
+      const uint32_t t2 = tl + slot * C::DSL + (uint32_t)(2 * NS + o * NH + lc);
+      float r1[8], r2[8];
+      tc::tmem_ld8(t01, v);
+      tc::tmem_ld8(t01 + NH, r1);
+      tc::tmem_ld8(t2, r2);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += r1[j] + r2[j];
     };
 
     // per-centre epilogue of the centres this CTA owns in (tile base c0, parity par)
@@ -204,14 +319,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
             for (int grp = 0; grp < 8; ++grp) v += red[(grp * CPS + cl) * 4 + j];
             tot[j] = v;
           }
-          float* ci = cis0 + ((par * 2 + slot) * CPS + cl) * NCINFO;
           if (MODE == 1) {
+            float ci[NCINFO];
             centre_frame(a, c, valid, tot[0] + net.b[L - 1][0], tot[1], tot[2], tot[3], ci);
             if (valid) {
 #pragma unroll
               for (int q = 0; q < NCINFO; ++q) a.cinfo[c * NCINFO + q] = ci[q];
             }
           } else {
+            const float* ci = cis0 + ((par * 2 + slot) * CPS + cl) * NCINFO;
             double lv[NLOSS];
             fd_centre(a, c, valid, tot, ci, lv);
 #pragma unroll
@@ -249,9 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
         const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
         for (int slot = 0; slot < 2; ++slot) {
           const int64_t cs = c0 + slot * CPS;
-          const uint32_t bslot_off = slot * C::BSLOT;
-          // the pre-activations the backward needs, stored AFTER the hand-off below: the proxy
-          // fence before it (MEMBAR at cluster scope) would otherwise wait for these stores
+          // the pre-activations the backward needs, stored after the hand-off below
           float zst[CPT][8];
           float z0n[CPT];
 #pragma unroll
@@ -266,15 +380,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
             ++nd[slot];
             tc::fence_after();
           }
+          unsigned char* bsl = Bs + slot * C::BSLOT;
+          if (!last) {
+            // B of (slot, l+1): own columns into this CTA's B block, the peer's into the staging
+            // block, which is free once the peer has received the previous one
+            mbar_wait(sfree, (nhand & 1u) ^ 1u);
+            ++nhand;
+          }
 #pragma unroll
           for (int i = 0; i < CPT; ++i) {
             const int cl = eg + 4 * i;           // centre within the slot
             const int64_t c = cs + cl;
             const bool valid = c < a.n;
-            const int owner = (cl * CPC) / NH;  // CTA holding this centre's columns
-            const int nl0 = (cl * CPC) % NH;    // its first local column there
             float outv[8];
-            int nout;
             if (MODE == 1) {
               float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
               if (l == 0) {
@@ -295,7 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
                 }
               } else {
                 float v[8];
-                tc::tmem_ld8(tl + slot * NS + (uint32_t)((cl >> 1) * 8), v);
+                ld_x8(slot, (cl >> 1) * 8, v);
                 const int o = (cl & 1) * 4;
                 if (mok) {
                   z = om * (v[o] + net.b[l][m]);
@@ -321,7 +439,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
               outv[1] = o1;
               outv[2] = o2;
               outv[3] = o3;
-              nout = 4;
             } else {
               const float* ci = cisp + (slot * CPS + cl) * NCINFO;
               float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
@@ -339,7 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
                 }
               } else {
                 float v[8];
-                tc::tmem_ld8(tl + slot * NS + (uint32_t)(cl * 8), v);
+                ld_x8(slot, cl * 8, v);
                 if (mok) {
 #pragma unroll
                   for (int p = 0; p < 4; ++p) {
@@ -361,19 +478,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
 #pragma unroll
                 for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &outv[2 * p], &outv[2 * p + 1]);
               }
-              nout = 8;
             }
+            const int owner = (cl * CPC) / NH;  // CTA holding this centre's columns
             if (!last) {
+              const int nl0 = (cl * CPC) % NH;
               if (owner == (int)rank) {
-                unsigned char* bsl = Bs + bslot_off;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  if (j < nout) tp::put_b_local<NH>(bsl, nl0 + j, m, outv[j]);
+                for (int j = 0; j < CPC; ++j) tp::put_b_local<NH>(bsl, nl0 + j, m, outv[j]);
               } else {
-                const uint32_t bsl = bs_c[owner] + bslot_off;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  if (j < nout) tp::put_b<NH>(bsl, nl0 + j, m, outv[j]);
+                for (int j = 0; j < CPC; ++j) tp::put_b_local<NH>(Stg, nl0 + j, ml, outv[j]);
               }
             } else {
               // last layer: this warp's 32-neuron sums of w_L * (values), into the owner's block
@@ -404,11 +518,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
               }
             }
           }
-          if (!last) {  // B of (slot, l+1) written (this warp's part): hand over to the leader's MMA
+          if (l > 0) ptimer.end_b();
+          if (!last) {  // this warp's part of (slot, l+1)'s B half and staging block is written
             tc::fence_before();
-            tp::fence_proxy_async_cluster();
+            fence_proxy_async();
             __syncwarp();
-            if (lane == 0) tp::arrive_cluster(bfull_leader + slot * 8);
+            if (lane == 0) mbar_arrive(&sready[slot]);
           } else {
             if (l > 0) tc::fence_before();
             __syncwarp();
@@ -445,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
       pend_par = par;
     }
     if (pending) finish(pend_c0, pend_par);
-    ptimer.report(MODE == 1 ? "fwd_tc2 centre" : "fwd_tc2 pairs", et == 0 && rank == 0);
+    ptimer.report(MODE == 1 ? "fwd_tc2 centre" : "fwd_tc2 pairs", (et == 0 || et == 480) && rank == 0);
     if (MODE == 2 && et == 0) {
 #pragma unroll
       for (int q = 0; q < NLOSS; ++q) a.lossp[(size_t)blockIdx.x * NLOSS + q] = lacc[q];

@@ -6,12 +6,12 @@
 // from global memory, B = the tile's activations / adjoints written by the epilogue warps):
 //   warp 0      TMA producer: one thread bulk-copies 48 KB weight stages (K chunk of 64 x
 //               128 rows x 3 pieces) into an NST-deep ring (cp.async.bulk + mbarrier tx);
-//   warp 1      TMEM owner + MMA issuer: one thread waits for the B operand of a layer,
-//               issues 4 K-steps x 6 piece products tcgen05.mma per stage into the TMEM
+//   warp 1      TMEM owner + MMA issuer: the warp waits for the B operand of a layer, one
+//               elected lane issues the piece-product tcgen05.mma of each stage into the TMEM
 //               accumulator of its M-half, commits the stage back to the producer and, after
 //               the last stage, commits "D full" to the epilogue;
-//   warps 2..9  epilogue (kernel specific): read D rows with tcgen05.ld, write the next B.
-// Hand-offs: wfull/wempty (producer <-> MMA), bfull (8 epilogue warps -> MMA: B written and
+//   warps 2..   epilogue (kernel specific): read D rows with tcgen05.ld, write the next B.
+// Hand-offs: wfull/wempty (producer <-> MMA), bfull (epilogue warps -> MMA: B written and
 // the previous D fully read), dfull (MMA -> epilogue).
 #pragma once
 #include <cstdio>
@@ -136,7 +136,8 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
     }
 }
 
-// MMA issuer (one thread): for every GEMM of every tile and every weight stage (kc, h), per
+// MMA issuer (one whole warp; one elected lane issues -- the descriptors are warp-uniform and
+// stay in uniform registers): for every GEMM of every tile and every weight stage (kc, h), per
 // 16-wide K step three MMAs, one per A piece, against the B pieces stored as consecutive row
 // blocks [b0 | b1 | b2] of the K chunk:
 //     a0 . [b0|b1|b2]  (N = 3N) -> TMEM ranges 0, 1, 2 of half h
@@ -181,9 +182,9 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
               const uint64_t bd = tc::sdesc_sw128(ba + sub * 32);
-              tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
-              tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
-              if (C::WPK == 3) tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
+              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
+              if (C::WPK == 3) tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
             }
           } else if (C::RANGES == 2) {
             // a0 . [b0|b1] and a1 . [b0|b1] (N = 2N: ranges 0, 1), then a0 . b2 and a2 . b0
@@ -192,29 +193,29 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
             for (int sub = 0; sub < 4; ++sub) {
               const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);
               const uint64_t b2 = tc::sdesc_sw128(ba + 2 * C::NS * 128 + sub * 32);
-              tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b01, id2, (kc | sub) != 0 ? 1u : 0u);
-              tc::mma_bf16(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), b01, id2, 1u);
-              tc::mma_bf16(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b2, id1, 1u);
-              tc::mma_bf16(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), b01, id1, 1u);
+              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b01, id2, (kc | sub) != 0 ? 1u : 0u);
+              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), b01, id2, 1u);
+              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b2, id1, 1u);
+              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), b01, id1, 1u);
             }
           } else {  // the six piece products into one range
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub)
 #pragma unroll
               for (int q = 3 - C::WPK; q < 6; ++q)  // WPK = 2: skip (a2, b0)
-                tc::mma_bf16(d, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
+                tc::mma_bf16_w(d, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
                              tc::sdesc_sw128(ba + tc::prod_b(q) * C::NS * 128 + sub * 32), id1,
                              (kc == 0 && sub == 0 && q == 3 - C::WPK) ? 0u : 1u);
           }
-          tc::mma_commit(&b.wempty[s]);
+          tc::mma_commit_w(&b.wempty[s]);
         }
-      tc::mma_commit(&b.dfull[sp]);
+      tc::mma_commit_w(&b.dfull[sp]);
 #ifdef FDSDF_PHASE_TIMING
       tspan += clock64() - tstart;
 #endif
     }
 #ifdef FDSDF_PHASE_TIMING
-  if (blockIdx.x == 0)
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
     printf("[phase] mma thread: total %lld cyc, %u passes, waiting for B %lld (%.0f/pass), issue span %lld (%.0f/pass) "
            "of which waiting for W stages %lld (%.0f/pass)\n",
            clock64() - t0, nb, tb, nb ? (double)tb / nb : 0.0, tspan, nb ? (double)tspan / nb : 0.0, tw,

@@ -62,6 +62,17 @@ __device__ __forceinline__ void fence_proxy_async_cluster() {
   asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
 }
 
+// bulk copy of `bytes` from this CTA's shared memory to shared::cluster address `dst` (a peer
+// CTA), completing `bytes` of transaction count on the mbarrier at shared::cluster `mbar` (in
+// the destination CTA).  Async proxy end to end: the source needs fence.proxy.async.shared::cta
+// after its generic writes, the destination's readers only the mbarrier.
+__device__ __forceinline__ void bulk_s2peer(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst),
+               "r"(smem_u32(src)), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
 __device__ __forceinline__ void mma2(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                      uint32_t accumulate) {
   asm volatile(
@@ -70,6 +81,25 @@ __device__ __forceinline__ void mma2(uint32_t dtmem, uint64_t adesc, uint64_t bd
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// warp-collective forms: the whole warp executes them with warp-uniform operands (kept in
+// uniform registers -- no per-lane waterfall around the issue), one elected lane issues
+__device__ __forceinline__ void mma2_w(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit2_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 // arrive once on the mbarrier at this shared offset in BOTH CTAs when the issued MMAs are done
 __device__ __forceinline__ void commit2(uint64_t* bar) {
   asm volatile(

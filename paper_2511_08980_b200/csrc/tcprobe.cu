@@ -350,3 +350,94 @@ extern "C" int fdsdf_probe_tmem_rate(int width, int nwarps, int iters, long long
     fdsdf::tmem_rate_kernel<16><<<1, nwarps * 32>>>(iters, d_out, d_sink);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 2;
 }
+
+// ----------------------------------------------------------------------------- pair MMA rate
+// Diagnostic: the same issue shapes on a CTA pair (tcgen05 cta_group::2, M = 256): `n` is the
+// pair-wide N of one operand piece (each CTA holds n/2 columns of it).
+//   mode 0: six MMAs a_i . b_j (N = n);  mode 1: three MMAs a_p . [b0|b1|b2] (N = 3n, 9
+//   products);  mode 2: a0.[b0|b1], a1.[b0|b1] (2n), a0.b2, a2.b0 (n);  mode 3: one MMA (N = n)
+namespace fdsdf {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma_rate2_kernel(int mode, int n, int iters, long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = smem_raw;
+  base += (1024 - (smem_u32(base) & 1023)) & 1023;
+  const int nh = n / 2;
+  unsigned char* As = base;
+  unsigned char* Bs = As + 3 * 16384;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + 3 * nh * 128 + 1024);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = tid; i < (3 * 16384 + 3 * nh * 128) / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(As)[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc::fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tc::fence_after();
+  const uint32_t d = *tslot;
+  auto mma2 = [&](uint64_t ad, uint64_t bd, uint32_t id) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(id), "r"(1u)
+        : "memory");
+  };
+  if (tid == 32 && rank == 0) {
+    const uint32_t a = smem_u32(As), b = smem_u32(Bs);
+    const uint32_t i1 = tc::idesc_bf16(256, n), i2 = tc::idesc_bf16(256, 2 * n), i3 = tc::idesc_bf16(256, 3 * n);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+      for (int sub = 0; sub < 4; ++sub) {
+        auto A = [&](int p) { return tc::sdesc_sw128(a + p * 16384 + sub * 32); };
+        auto B = [&](int p) { return tc::sdesc_sw128(b + p * nh * 128 + sub * 32); };
+        if (mode == 0) {
+#pragma unroll
+          for (int q = 0; q < 6; ++q) mma2(A(tc::prod_a(q)), B(tc::prod_b(q)), i1);
+        } else if (mode == 1) {
+          mma2(A(0), B(0), i3);
+          mma2(A(1), B(0), i3);
+          mma2(A(2), B(0), i3);
+        } else if (mode == 2) {
+          mma2(A(0), B(0), i2);
+          mma2(A(1), B(0), i2);
+          mma2(A(0), B(2), i1);
+          mma2(A(2), B(0), i1);
+        } else {
+          mma2(A(0), B(0), i1);
+        }
+      }
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+    mbar_wait(bar, 0);
+    out[0] = clock64() - t0;
+  } else if (tid == 32) {
+    mbar_wait(bar, 0);
+  }
+  tc::fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(d), "r"(512) : "memory");
+}
+}  // namespace fdsdf
+
+extern "C" int fdsdf_probe_mma_rate2(int mode, int n, int iters, long long* d_out) {
+  const int bytes = 3 * 16384 + 3 * (n / 2) * 128 + 2048 + 64;
+  auto k = fdsdf::mma_rate2_kernel;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return 1;
+  k<<<2, 128, bytes>>>(mode, n, iters, d_out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 2;
+}

@@ -32,3 +32,16 @@ for width in (8, 16):
         cyc = out.item()
         byts = nw * iters * 32 * width * 4
         print(f"tcgen05.ld x{width:2d} {nw:2d} warps: {byts / cyc:6.1f} B/cycle  ({cyc / iters:6.1f} cyc per warp-load round)")
+
+# CTA pair (cta_group::2, M = 256): cycles per K step for the whole pair
+L.fdsdf_probe_mma_rate2.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+names2 = {0: "6 x N", 1: "3 x 3N (9 products)", 2: "2N,2N,N,N", 3: "single N"}
+for n in (64, 80):
+    for mode in (3, 0, 2, 1):
+        if mode == 1 and 3 * n > 256:
+            continue
+        iters = 400
+        assert L.fdsdf_probe_mma_rate2(mode, n, iters, out.data_ptr()) == 0
+        assert L.fdsdf_probe_mma_rate2(mode, n, iters, out.data_ptr()) == 0
+        cyc = out.item() / (iters * 4)
+        print(f"pair N={n:3d} {names2[mode]:22s} {cyc:7.1f} cyc/kstep (M=256)  = {cyc / 2:6.1f} per M=128 half")

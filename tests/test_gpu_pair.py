@@ -44,8 +44,13 @@ def _built():
     build()
 
 
-def test_pair_kernels_parity():
+# the full grid (74 clusters, 1-2 pair tiles each), and 2 clusters (tens of tiles per cluster:
+# every slot / parity / staging-block hand-off sequence runs many times, ragged last tile)
+@pytest.mark.parametrize("max_sm", [None, "4"])
+def test_pair_kernels_parity(max_sm):
     env = dict(os.environ, FDSDF_PAIR="1")
+    if max_sm:
+        env["FDSDF_MAX_SM"] = max_sm
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=300)
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0 and "PAIR-OK" in r.stdout
