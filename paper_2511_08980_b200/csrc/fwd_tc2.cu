@@ -48,8 +48,8 @@ struct F2Cfg {
   static constexpr int BSLOT = KC * 3 * NH * 128;       // B block of one slot in one CTA (48 KB)
   static constexpr int STG = 2 * 3 * NH * 128;          // staging: the peer's columns, 2 K chunks
   static constexpr int NEPI = 16;
-  static constexpr int XW = 2 + NEPI;                   // the exchanger warp
-  static constexpr int NTHR = (3 + NEPI) * 32;
+  static constexpr int XW = 2 + NEPI;                   // exchanger warps: sender, receiver
+  static constexpr int NTHR = (4 + NEPI) * 32;
   static constexpr int CPT = CPS / 4;                   // centres per epilogue thread per slot
   static constexpr int NRED = 8 * CPS * 4;              // floats per (parity, slot) reduction block
   static constexpr int DSL = 3 * NS;                    // TMEM columns per slot: R01 (2 NS), R2 (NS)
@@ -218,20 +218,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
             }
     }
   } else if (warp == C::XW) {
-    // ------------------------------------------------------------------ operand exchanger
+    // ------------------------------------------------------------------ operand sender
     // per hand-off (tile, layer < L-2, slot), in the epilogue's order: once this CTA's B half
-    // and staging block are written, send the staging block to the peer's B rows
-    // [128 rank, ...), wait for the peer's block to land here, then report this CTA's B half
-    // complete to the leader's MMA thread and the peer's staging block free to the peer
+    // and staging block are written, send the staging block to the peer's B rows [128 rank, ..)
     if (lane == 0 && ngemm > 0) {
-      const uint32_t peer = rank ^ 1u;
-      const uint32_t peer_b = tp::mapa(smem_u32(Bs), peer) + rank * C::STG;
-      const uint32_t peer_bin = tp::mapa(smem_u32(bin), peer);
-      const uint32_t peer_sfree = tp::mapa(smem_u32(sfree), peer);
+      const uint32_t peer_b = tp::mapa(smem_u32(Bs), rank ^ 1u) + rank * C::STG;
+      const uint32_t peer_bin = tp::mapa(smem_u32(bin), rank ^ 1u);
+      uint32_t ph[2] = {0u, 0u};
+      for (int64_t tile = cid; tile < a.ntiles; tile += ncl)
+        for (int l = 0; l < L - 2; ++l)
+          for (int slot = 0; slot < 2; ++slot) {
+            mbar_wait(&sready[slot], ph[slot] & 1u);
+            ++ph[slot];
+            tp::bulk_s2peer(peer_b + slot * C::BSLOT, Stg, C::STG, peer_bin + slot * 8);
+          }
+    }
+  } else if (warp == C::XW + 1) {
+    // ------------------------------------------------------------------ operand receiver
+    // per hand-off: wait for the peer's block to land here and tell the peer at once that its
+    // staging block is free; then, once this CTA's own half is written too, report this CTA's
+    // B half of the slot complete to the leader's MMA thread
+    if (lane == 0 && ngemm > 0) {
+      const uint32_t peer_sfree = tp::mapa(smem_u32(sfree), rank ^ 1u);
       const uint32_t bfull_leader = tp::mapa(smem_u32(bfull), 0);
       uint32_t ph[2] = {0u, 0u};
 #ifdef FDSDF_PHASE_TIMING
-      long long t0 = clock64(), tr = 0, ti = 0, tm;
+      long long t0 = clock64(), ti = 0, tr = 0, tm;
 #endif
       for (int64_t tile = cid; tile < a.ntiles; tile += ncl)
         for (int l = 0; l < L - 2; ++l)
@@ -239,26 +251,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
 #ifdef FDSDF_PHASE_TIMING
             tm = clock64();
 #endif
+            mbar_arrive_expect_tx(&bin[slot], C::STG);
+            mbar_wait(&bin[slot], ph[slot] & 1u);
+            tp::arrive_cluster(peer_sfree);
+#ifdef FDSDF_PHASE_TIMING
+            ti += clock64() - tm;
+            tm = clock64();
+#endif
             mbar_wait(&sready[slot], ph[slot] & 1u);
 #ifdef FDSDF_PHASE_TIMING
             tr += clock64() - tm;
-            tm = clock64();
-#endif
-            mbar_arrive_expect_tx(&bin[slot], C::STG);
-            tp::bulk_s2peer(peer_b + slot * C::BSLOT, Stg, C::STG, peer_bin + slot * 8);
-            mbar_wait(&bin[slot], ph[slot] & 1u);
-#ifdef FDSDF_PHASE_TIMING
-            ti += clock64() - tm;
 #endif
             ++ph[slot];
             tp::arrive_cluster(bfull_leader + slot * 8);
-            tp::arrive_cluster(peer_sfree);
           }
 #ifdef FDSDF_PHASE_TIMING
       if (blockIdx.x < 2)
-        printf("[phase] pair exchanger rank %u: total %lld, %u hand-offs, waiting for epilogue %.0f/hand-off, copy "
-               "round trip %.0f/hand-off\n",
-               rank, clock64() - t0, ph[0] + ph[1], (double)tr / (ph[0] + ph[1]), (double)ti / (ph[0] + ph[1]));
+        printf("[phase] pair receiver rank %u: total %lld, %u hand-offs, waiting for the peer block %.0f, then "
+               "for the own half %.0f per hand-off\n",
+               rank, clock64() - t0, ph[0] + ph[1], (double)ti / (ph[0] + ph[1]), (double)tr / (ph[0] + ph[1]));
 #endif
     }
   } else {
@@ -366,12 +377,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
         for (int slot = 0; slot < 2; ++slot) {
           const int64_t cs = c0 + slot * CPS;
           // the pre-activations the backward needs, stored after the hand-off below
+          // (arrays indexed by the processing position jj; centre i = pos_i(jj))
+          auto pos_i = [&](int jj) { return rank ? (jj + CPT / 2) % CPT : jj; };
           float zst[CPT][8];
           float z0n[CPT];
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {
-            const int64_t c = cs + eg + 4 * i;
-            z0n[i] = (MODE == 2 && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
+          for (int jj = 0; jj < CPT; ++jj) {
+            const int64_t c = cs + eg + 4 * pos_i(jj);
+            z0n[jj] = (MODE == 2 && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
           }
           if (l > 0) {
             ptimer.before_wait();
@@ -381,14 +394,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
             tc::fence_after();
           }
           unsigned char* bsl = Bs + slot * C::BSLOT;
-          if (!last) {
-            // B of (slot, l+1): own columns into this CTA's B block, the peer's into the staging
-            // block, which is free once the peer has received the previous one
-            mbar_wait(sfree, (nhand & 1u) ^ 1u);
-            ++nhand;
-          }
+          // B of (slot, l+1): own columns into this CTA's B block, the peer's into the staging
+          // block.  Of this thread's centres eg + 4i, the first CPT/2 are owned by CTA 0: the
+          // locally owned ones go first, so the staging block (free once the peer has received
+          // the previous hand-off) is waited for only after half of the work.  Register arrays
+          // are indexed by the (unrolled) position jj, the centre is i.
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {
+          for (int jj = 0; jj < CPT; ++jj) {
+            const int i = pos_i(jj);
+            if (!last && jj == CPT / 2) {
+              mbar_wait(sfree, (nhand & 1u) ^ 1u);
+              ++nhand;
+            }
             const int cl = eg + 4 * i;           // centre within the slot
             const int64_t c = cs + cl;
             const bool valid = c < a.n;
@@ -422,10 +439,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
                   t2 = om * v[o + 3];
                 }
               }
-              zst[i][0] = z;
-              zst[i][1] = t0;
-              zst[i][2] = t1;
-              zst[i][3] = t2;
+              zst[jj][0] = z;
+              zst[jj][1] = t0;
+              zst[jj][2] = t1;
+              zst[jj][3] = t2;
               float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
               if (mok) {
                 const typename AF::C cc = AF::centre(z, beta);
@@ -465,11 +482,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
                   }
                 }
               }
-              const float z0 = z0n[i];
+              const float z0 = z0n[jj];
 #pragma unroll
               for (int p = 0; p < 4; ++p) {
-                zst[i][2 * p] = Av[p];
-                zst[i][2 * p + 1] = Sv[p];
+                zst[jj][2 * p] = Av[p];
+                zst[jj][2 * p + 1] = Sv[p];
               }
 #pragma unroll
               for (int p = 0; p < 8; ++p) outv[p] = 0.f;
@@ -533,19 +550,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
             }
           }
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) {  // the deferred pre-activation stores
-            const int64_t c = cs + eg + 4 * i;
+          for (int jj = 0; jj < CPT; ++jj) {  // the deferred pre-activation stores
+            const int64_t c = cs + eg + 4 * pos_i(jj);
             if (c < a.n) {
               if (MODE == 1) {
-                *zp(c, l, 0) = zst[i][0];
+                *zp(c, l, 0) = zst[jj][0];
                 if (step) {
-                  *zp(c, l, 1) = zst[i][1];
-                  *zp(c, l, 2) = zst[i][2];
-                  *zp(c, l, 3) = zst[i][3];
+                  *zp(c, l, 1) = zst[jj][1];
+                  *zp(c, l, 2) = zst[jj][2];
+                  *zp(c, l, 3) = zst[jj][3];
                 }
               } else if (step) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) *zp(c, l, 4 + q) = zst[i][q];
+                for (int q = 0; q < 8; ++q) *zp(c, l, 4 + q) = zst[jj][q];
               }
             }
           }
