@@ -69,6 +69,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// the same with a __nanosleep back-off between polls: for the long waits of the single-thread
+// roles (producer, MMA issuer), whose polling shares a scheduler with epilogue warps
+#ifndef FDSDF_WAIT_BACKOFF_NS
+#define FDSDF_WAIT_BACKOFF_NS 0
+#endif
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  if (FDSDF_WAIT_BACKOFF_NS == 0) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  while (!mbar_try_wait_sleep(bar, parity)) __nanosleep(FDSDF_WAIT_BACKOFF_NS);
+}
+
 // 1-D bulk copy global -> shared through the TMA engine, completion on an mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile(

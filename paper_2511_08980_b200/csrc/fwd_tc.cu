@@ -211,11 +211,12 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           t2 = om * w2;
         }
         if (valid) {
-          *zp(c, 0, 0) = z;
+          float* zc = zp(c, 0, 0);
+          zc[0] = z;
           if (step) {
-            *zp(c, 0, 1) = t0;
-            *zp(c, 0, 2) = t1;
-            *zp(c, 0, 3) = t2;
+            zc[1 * MPAD] = t0;
+            zc[2 * MPAD] = t1;
+            zc[3 * MPAD] = t2;
           }
         }
         float o[4] = {0.f, 0.f, 0.f, 0.f};
@@ -230,7 +231,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         tc::tmem_st4(tstash + i * CPC, o);
       } else {
         const float* ci = cis_t + cl * NCINFO;
-        const float z0 = valid ? __ldg(zp(c, 0, 0)) : 0.f;
+        float* zc0 = zp(c, 0, 0);
+        const float z0 = valid ? __ldg(zc0) : 0.f;
         float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
         if (mok) {
           const float* W0 = net.W[0];
@@ -246,8 +248,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         if (step && valid) {
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
-            *zp(c, 0, 4 + 2 * p) = Av[p];
-            *zp(c, 0, 5 + 2 * p) = Sv[p];
+            zc0[(4 + 2 * p) * MPAD] = Av[p];
+            zc0[(5 + 2 * p) * MPAD] = Sv[p];
           }
         }
         float o[8];
@@ -403,7 +405,10 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         }
         if (l > 0) {
           ptimer.before_wait();
-          mbar_wait(&bars.dfull[sp], nd & 1u);
+          // one warp polls the mbarrier, the others sleep in a hardware named barrier (no
+          // spin instructions competing with the MMA warp for issue slots)
+          if (ew == 0) mbar_wait(&bars.dfull[sp], nd & 1u);
+          bar_named(2, C::NEPI * 32);
           ptimer.after_wait();
           tc::fence_after();
         }
@@ -444,11 +449,12 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               }
             }
             if (valid) {
-              *zp(c, l, 0) = z;
+              float* zc = zp(c, l, 0);
+              zc[0] = z;
               if (step) {
-                *zp(c, l, 1) = t0;
-                *zp(c, l, 2) = t1;
-                *zp(c, l, 3) = t2;
+                zc[1 * MPAD] = t0;
+                zc[2 * MPAD] = t1;
+                zc[3 * MPAD] = t2;
               }
             }
             float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
@@ -581,10 +587,11 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               }
             }
             if (step && valid) {
+              float* zc = zp(c, l, 0);
 #pragma unroll
               for (int p = 0; p < 4; ++p) {
-                *zp(c, l, 4 + 2 * p) = Av[p];
-                *zp(c, l, 5 + 2 * p) = Sv[p];
+                zc[(4 + 2 * p) * MPAD] = Av[p];
+                zc[(5 + 2 * p) * MPAD] = Sv[p];
               }
             }
             float o[8];

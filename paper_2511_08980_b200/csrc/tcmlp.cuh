@@ -128,7 +128,7 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
         for (int h = 0; h < C::MH; ++h, ++it) {
           const int s = (int)(it % C::NST);
           const uint32_t ph = (it / C::NST) & 1u;
-          mbar_wait(&b.wempty[s], ph ^ 1u);
+          mbar_wait_backoff(&b.wempty[s], ph ^ 1u);
           mbar_arrive_expect_tx(&b.wfull[s], C::STAGE);
           bulk_g2s(Ws + s * C::STAGE, img + (((size_t)g * C::KC + kc) * C::MH + h) * C::IMGSTAGE, C::STAGE,
                    &b.wfull[s]);
@@ -164,7 +164,7 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
     for (int gs = 0; gs < ngemm * C::NSPLIT; ++gs, ++nb) {
       const int sp = gs % C::NSPLIT;  // column split of this pass
-      TC_MMA_T(tb, mbar_wait(&b.bfull[sp], (nb / C::NSPLIT) & 1u));
+      TC_MMA_T(tb, mbar_wait_backoff(&b.bfull[sp], (nb / C::NSPLIT) & 1u));
 #ifdef FDSDF_PHASE_TIMING
       const long long tstart = clock64();
 #endif
