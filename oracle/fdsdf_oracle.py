@@ -35,7 +35,7 @@ import torch
 __all__ = [
     "splitmix64", "frame_theta", "onb", "tangent_frames", "unflatten", "sdf",
     "fd_entries", "curvature", "loss_terms", "oracle_step", "oracle_eval",
-    "bordered_K", "shape_operator_K", "hessian_at",
+    "bordered_K", "shape_operator_K", "hessian_at", "fd_hessian", "oracle_hessian",
 ]
 
 F64 = torch.float64
@@ -147,6 +147,39 @@ def fd_entries(field, x0, u, v, h):
     f_vv = (f_pv - 2.0 * f0 + f_mv) / (h * h)
     f_uv = (f_pp - f_pm - f_mp + f_mm) / (4.0 * h * h)
     return f_uu, f_vv, f_uv
+
+
+def fd_hessian(field, x0, h):
+    """The world-axis 3x3 FD Hessian at centres x0 [M,3] from the 19-point stencil x0,
+    x0 +- h e_i, x0 + h(+-e_i +- e_j): the P:L83-91 formulas with
+    (u, v) = (e_i, e_j) --
+        H_ii = (f(x0 + h e_i) - 2 f(x0) + f(x0 - h e_i)) / h^2
+        H_ij = (f(x0 + h e_i + h e_j) - f(x0 + h e_i - h e_j) - f(x0 - h e_i + h e_j)
+                + f(x0 - h e_i - h e_j)) / (4 h^2)
+    -- every point formed in fp64 and evaluated separately (19 evaluations).
+    Returns [M,6] = (H_xx, H_xy, H_xz, H_yy, H_yz, H_zz)."""
+    E = torch.eye(3, dtype=x0.dtype)
+    f0 = field(x0)
+    H = {}
+    for i in range(3):
+        ei = E[i]
+        H[(i, i)] = (field(x0 + h * ei) - 2.0 * f0 + field(x0 - h * ei)) / (h * h)
+        for j in range(i + 1, 3):
+            ej = E[j]
+            H[(i, j)] = (field(x0 + h * ei + h * ej) - field(x0 + h * ei - h * ej)
+                         - field(x0 - h * ei + h * ej) + field(x0 - h * ei - h * ej)) / (4.0 * h * h)
+    return torch.stack([H[(0, 0)], H[(0, 1)], H[(0, 2)], H[(1, 1)], H[(1, 2)], H[(2, 2)]], dim=1)
+
+
+def oracle_hessian(spec, params, x, h):
+    """f and the 19-point world-axis FD Hessian of the MLP at centres x [N,3] (fp32 inputs
+    promoted exactly to fp64).  Returns (f [N], H [N,6]) as numpy fp64."""
+    layers = unflatten(spec, torch.as_tensor(np.asarray(params, np.float32), dtype=F64))
+    x0 = torch.as_tensor(np.asarray(x, np.float32), dtype=F64).reshape(-1, 3)
+    hh = float(np.float32(h))
+    field = lambda pts: sdf(spec, layers, pts)  # noqa: E731
+    with torch.no_grad():
+        return field(x0).numpy(), fd_hessian(field, x0, hh).numpy()
 
 
 def curvature(f_uu, f_vv, f_uv, gn, mask, den_mode, is_surface, p=4):
