@@ -225,7 +225,8 @@ def measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank
     """(1) the full training iteration of PAPER.md §4: fdsdf_sample (20k of a
     30k CSG surface pool + 20k box points) -> fdsdf_step (+ allreduce) -> fdsdf_adam
     (lr 5e-5); (2) fdsdf_eval throughput (f, grad f, FD Hessian, D, K, frames, mask) on
-    the same batch; (3) optionally the C5e eval sweep.  All CUDA-event timed on the stream."""
+    the same batch, and fdsdf_eval_hessian (world-axis 3x3 FD Hessian); (3)
+    optionally the C5e eval sweep.  All CUDA-event timed on the stream."""
     import torch
     from harness import csg_surface
     from paper_2511_08980_b200 import FDSDF
@@ -262,6 +263,13 @@ def measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank
                      args.steps, flush)
     out["eval"] = {"ms": ms_e, "centres": n, "stencil_points_per_s": 9.0 * n / (ms_e * 1e-3),
                    "outputs": "f, grad f, (f_uu, f_uv, f_vv), D, K, frames, mask"}
+    # world-axis FD Hessian mode: 19-point stencil per centre, 3 GIVEN-frame passes
+    Hb = model.eval_hessian(pdev, x, cfg["h"], stream=stream)
+    for i in range(args.warmup):
+        model.eval_hessian(pdev, x, cfg["h"], H=Hb, stream=stream)
+    ms_h = _event_ms(stream, lambda i: model.eval_hessian(pdev, x, cfg["h"], H=Hb, stream=stream), args.steps, flush)
+    out["eval_hessian"] = {"ms": ms_h, "centres": n, "stencil_points_per_s": 19.0 * n / (ms_h * 1e-3),
+                           "outputs": "world-axis 3x3 FD Hessian (19-point stencil) as 3 axis-frame stencil passes"}
     if args.eval_sweep and rank == 0:
         from harness import csg_surface as cs, uniform_box
         sweep = []

@@ -181,6 +181,20 @@ int64_t fdsdf_num_params(const fdsdf_ctx* ctx);
 fdsdf_status fdsdf_eval(fdsdf_ctx* ctx, const float* d_params, const float* d_x, int64_t n,
                         const fdsdf_stencil* st, const fdsdf_eval_out* out, void* stream);
 
+/* The world-axis 3x3 FD Hessian of f at n centres d_x [n][3]: the
+ * 19-point stencil x0, x0 +- h e_i, x0 + h (+-e_i +- e_j), i < j, with the P:L83-91 formulas
+ * for (u, v) = (e_i, e_j):
+ *   H_ii = (f(x0 + h e_i) - 2 f(x0) + f(x0 - h e_i)) / h^2,
+ *   H_ij = (f(x0+h(e_i+e_j)) - f(x0+h(e_i-e_j)) - f(x0-h(e_i-e_j)) + f(x0-h(e_i+e_j))) / (4 h^2).
+ * d_H [n][6] fp32 (device, caller-owned) = (H_xx, H_xy, H_xz, H_yy, H_yz, H_zz); optional
+ * d_f [n], d_grad [n][3] (NULL = not written).  Runs as three stencil passes of fdsdf_eval
+ * with GIVEN axis frames (e_x, e_y), (e_x, e_z), (e_y, e_z) in the context's workspace (the
+ * pair sums are the same arithmetic as the tangent entries; H_xx is evaluated twice, the
+ * first is kept); no degenerate mask.  Errors: ctx NULL, d_params/d_x NULL, d_H NULL with
+ * n > 0, n > max_centers, h <= 0 or non-finite -> FDSDF_E_INVALID; n == 0 -> FDSDF_E_EMPTY. */
+fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* ctx, const float* d_params, const float* d_x, int64_t n, float h,
+                                float* d_H, float* d_f, float* d_grad, void* stream);
+
 /* One training step: the loss of Eq. (1) and its gradient with respect to every parameter.
  * d_grad [P] fp32 (overwritten, or accumulated with FDSDF_STEP_ACCUMULATE);
  * d_loss [8] fp64 = (L_DM, L_DNM, L_eik, L_fd, total, n_degenerate, 0, 0), each term
@@ -260,7 +274,8 @@ enum {
   FDSDF_KSLOT_FWD_CENTRE = 7,/* tensor path: centre + tangent columns (f, grad f, frame)   */
   FDSDF_KSLOT_SAMPLE = 8,    /* fdsdf_sample                                               */
   FDSDF_KSLOT_ADAM = 9,      /* fdsdf_adam                                                 */
-  FDSDF_NUM_KSLOTS = 10
+  FDSDF_KSLOT_HESS = 10,     /* fdsdf_eval_hessian's axis-frame and scatter kernels        */
+  FDSDF_NUM_KSLOTS = 11
 };
 fdsdf_status fdsdf_set_kernel_timing(fdsdf_ctx* ctx, int enable);
 fdsdf_status fdsdf_kernel_times(fdsdf_ctx* ctx, double* ms_total, int64_t* count, int nslots, int reset);

@@ -93,6 +93,8 @@ struct fdsdf_ctx {
   unsigned char* bimg = nullptr;  // packed backward (W^T) weight image
   float* cinfo = nullptr;    // [max_centers][16]
   float* zev = nullptr;      // eval-only contexts: [max_centers][nh][mpad] centre pre-activations
+  float* hframes = nullptr;  // fdsdf_eval_hessian: [max_centers][6] axis frames
+  float* htmp = nullptr;     // fdsdf_eval_hessian: [max_centers][3] one pass's (f_uu, f_uv, f_vv)
   void* comm = nullptr;
   int rank = 0, world = 1;
   int launches = 0;
@@ -218,7 +220,7 @@ void fdsdf_destroy(fdsdf_ctx* c) {
   }
   for (cudaEvent_t e : c->spare) cudaEventDestroy(e);
   void* bufs[] = {c->wt,   c->wb,   c->zf,     c->zscr,   c->seed,  c->lossp, c->del, c->actv,
-                  c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev, c->bimg};
+                  c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev, c->bimg, c->hframes, c->htmp};
   for (void* b : bufs)
     if (b) cudaFree(b);
   cudaSetDevice(prev);
@@ -321,6 +323,8 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
   // per-CTA loss partials of the forward: the FFMA grid, or up to one CTA per SM (tensor path)
   ok = ok && alloc((void**)&c->lossp, (size_t)std::max(c->fgrid, c->nsm) * NLOSS * sizeof(double));
   ok = ok && alloc((void**)&c->dflags, sizeof(unsigned));
+  ok = ok && alloc((void**)&c->hframes, (size_t)max_centers * 6 * sizeof(float));
+  ok = ok && alloc((void**)&c->htmp, (size_t)max_centers * 3 * sizeof(float));
   if (ok && !c->eval_only) {
     ok = ok && alloc((void**)&c->zf, (size_t)max_centers * c->nh * NCOLF * mp * sizeof(float));
     ok = ok && alloc((void**)&c->seed, (size_t)max_centers * NSEED * sizeof(float));
@@ -481,6 +485,58 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   e = run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd(a, grid, strm); });
   if (prev != c->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_fail(c, e, "fwd_kernel");
+  return FDSDF_OK;
+}
+
+fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, float h,
+                                float* d_H, float* d_f, float* d_grad, void* stream) {
+  if (!c) return FDSDF_E_INVALID;
+  if (!d_H && n > 0) return fail(c, FDSDF_E_INVALID, "null d_H");
+  fdsdf_stencil st{};
+  st.h = h;
+  st.frame_mode = FDSDF_FRAME_GIVEN;
+  st.d_frames_in = c->hframes;
+  st.eps_grad = 0.f;  // the Hessian is wanted at critical points too
+  st.denom = FDSDF_DENOM_ONE;
+  st.denom_pow = 4;
+  fdsdf_status s = check_common(c, d_params, d_x, n, &st);
+  if (s != FDSDF_OK) return s;
+  cudaStream_t strm = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != c->device) cudaSetDevice(c->device);
+  static const int AX[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+  int launches = 0;
+  c->launches = 0;
+  for (int pass = 0; pass < 3; ++pass) {
+    cudaError_t e = run_slot(c, FDSDF_KSLOT_HESS, strm,
+                             [&] { return launch_axis_frames(c->hframes, n, AX[pass][0], AX[pass][1], strm); });
+    if (e != cudaSuccess) {
+      if (prev != c->device) cudaSetDevice(prev);
+      return cuda_fail(c, e, "axis_frames_kernel");
+    }
+    fdsdf_eval_out out{};
+    out.d_hess = c->htmp;
+    if (pass == 0) {
+      out.d_f = d_f;
+      out.d_grad = d_grad;
+    }
+    launches += c->launches;
+    s = fdsdf_eval(c, d_params, d_x, n, &st, &out, stream);
+    if (s != FDSDF_OK) {
+      if (prev != c->device) cudaSetDevice(prev);
+      return s;
+    }
+    launches += c->launches;
+    c->launches = 0;
+    e = run_slot(c, FDSDF_KSLOT_HESS, strm, [&] { return launch_hess_scatter(c->htmp, d_H, n, pass, strm); });
+    if (e != cudaSuccess) {
+      if (prev != c->device) cudaSetDevice(prev);
+      return cuda_fail(c, e, "hess_scatter_kernel");
+    }
+  }
+  c->launches += launches;
+  if (prev != c->device) cudaSetDevice(prev);
   return FDSDF_OK;
 }
 

@@ -16,6 +16,7 @@
 //   * box point j, coordinate d: U = (mix64(seed2 + ((iteration*n_uniform + j)*3 + d + 1) *
 //     gamma) >> 11) * 2^-53, x = half * (2U - 1) in fp64, rounded to fp32; seed2 = mix64(~seed).
 // The oracle (oracle/train_oracle.py) implements the same generators independently.
+#include <algorithm>
 #include <cmath>
 
 #include "../../include/fdsdf.h"
@@ -116,4 +117,46 @@ cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n,
   return cudaGetLastError();
 }
 
+}  // namespace fdsdf
+
+// ----------------------------------------------------------------------------- Hessian mode
+// fdsdf_eval_hessian: the world-axis Hessian as three GIVEN-frame stencil
+// passes with (u, v) = (e_a, e_b); these two kernels set the frames and scatter the pass's
+// (f_uu, f_uv, f_vv) into H = (H_xx, H_xy, H_xz, H_yy, H_yz, H_zz).
+namespace fdsdf {
+__global__ void axis_frames_kernel(float* frames, int64_t n, int a, int b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 6; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % 6);
+    frames[i] = (k < 3 ? (k == a) : (k - 3 == b)) ? 1.f : 0.f;
+  }
+}
+
+// pass 0 (e_x, e_y): xx, xy, yy;  pass 1 (e_x, e_z): xz, zz;  pass 2 (e_y, e_z): yz
+__global__ void hess_scatter_kernel(const float* __restrict__ t, float* __restrict__ H, int64_t n, int pass) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float fuu = t[i * 3 + 0], fuv = t[i * 3 + 1], fvv = t[i * 3 + 2];
+    if (pass == 0) {
+      H[i * 6 + 0] = fuu;
+      H[i * 6 + 1] = fuv;
+      H[i * 6 + 3] = fvv;
+    } else if (pass == 1) {
+      H[i * 6 + 2] = fuv;
+      H[i * 6 + 5] = fvv;
+    } else {
+      H[i * 6 + 4] = fuv;
+    }
+  }
+}
+
+static int ew_grid(int64_t work) { return (int)std::min<int64_t>(std::max<int64_t>((work + 255) / 256, 1), 4096); }
+
+cudaError_t launch_axis_frames(float* frames, int64_t n, int a, int b, cudaStream_t st) {
+  axis_frames_kernel<<<ew_grid(n * 6), 256, 0, st>>>(frames, n, a, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hess_scatter(const float* t, float* H, int64_t n, int pass, cudaStream_t st) {
+  hess_scatter_kernel<<<ew_grid(n), 256, 0, st>>>(t, H, n, pass);
+  return cudaGetLastError();
+}
 }  // namespace fdsdf

@@ -84,6 +84,8 @@ def lib():
         L.fdsdf_num_params.restype = i64
         L.fdsdf_eval.argtypes = [vp, vp, vp, i64, C.POINTER(Stencil), C.POINTER(EvalOut), vp]
         L.fdsdf_eval.restype = C.c_int
+        L.fdsdf_eval_hessian.argtypes = [vp, vp, vp, i64, C.c_float, vp, vp, vp, vp]
+        L.fdsdf_eval_hessian.restype = C.c_int
         L.fdsdf_step.argtypes = [vp, vp, vp, i64, C.POINTER(Stencil), C.POINTER(Loss), vp, vp, u32, vp]
         L.fdsdf_step.restype = C.c_int
         L.fdsdf_comm_unique_id.argtypes = [C.c_char_p]
@@ -207,6 +209,11 @@ def make_loss(cfg: dict, counts):
     return ls
 
 
+def fdsdf_eval_hessian(ctx, params, x, n, h, H, f=None, g=None, stream=None):
+    _check(lib().fdsdf_eval_hessian(ctx, _ptr(params), _ptr(x), int(n), float(h), _ptr(H), _ptr(f), _ptr(g),
+                                    _stream(stream)), ctx)
+
+
 def fdsdf_eval(ctx, params, x, n, stencil: Stencil, out: EvalOut, stream=None):
     _check(lib().fdsdf_eval(ctx, _ptr(params), _ptr(x), int(n), C.byref(stencil), C.byref(out),
                             _stream(stream)), ctx)
@@ -252,7 +259,8 @@ def fdsdf_get_device_flags(ctx) -> int:
 def fdsdf_last_launch_count(ctx) -> int:
     return int(lib().fdsdf_last_launch_count(ctx))
 
-KSLOTS = ("pack", "fwd", "bwd", "wgrad", "finalize", "allreduce", "pack_tc", "fwd_centre", "sample", "adam")
+KSLOTS = ("pack", "fwd", "bwd", "wgrad", "finalize", "allreduce", "pack_tc", "fwd_centre", "sample", "adam",
+          "hess")
 
 
 def fdsdf_set_kernel_timing(ctx, enable: bool):
@@ -317,6 +325,18 @@ class FDSDF:
         out = EvalOut(*(_ptr(o.get(k)) for k in ("f", "g", "hess", "K", "D", "frames", "mask")))
         fdsdf_eval(self.ctx, params, x, n, st, out, stream)
         return o
+
+    def eval_hessian(self, params, x, h, H=None, f=None, g=None, stream=None):
+        """World-axis 3x3 FD Hessian (19-point stencil): returns H [n,6] = (xx, xy, xz, yy, yz, zz)
+        as a device tensor; optional f [n] / g [n,3] output tensors are filled too."""
+        import torch
+        params = self._dev(params, torch.float32)
+        x = self._dev(x, torch.float32).reshape(-1, 3)
+        n = x.shape[0]
+        if H is None:
+            H = torch.empty(n, 6, device=self.device, dtype=torch.float32)
+        fdsdf_eval_hessian(self.ctx, params, x, n, h, H, f, g, stream)
+        return H
 
     def step(self, params, x, n_surface, h, loss_cfg, counts=None, frame_seed=0, index_offset=0, frames=None,
              eps_grad=1e-6, grad=None, loss=None, accumulate=False, allreduce=False, stream=None):
