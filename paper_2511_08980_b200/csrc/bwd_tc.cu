@@ -37,6 +37,11 @@ namespace fdsdf {
 #ifndef BWD_TC_PIPE_TOP
 #define BWD_TC_PIPE_TOP 1
 #endif
+// 1 (two-range mode): phase A hands sigma'(z) and sigma''(z) (r . t) of each centre to phase B
+// in a small per-thread array, instead of phase B reloading z, t and recomputing sincos(z)
+#ifndef BWD_TC_CARRY
+#define BWD_TC_CARRY 1
+#endif
 // accumulator ranges of the X GEMM: 2 (a0.[b0|b1], a1.[b0|b1], a0.b2, a2.b0: four A reads per
 // K step, stash of the 12 derivative factors) or 1 (six MMAs, stash of 20 values)
 #ifndef BWD_TC_RANGES
@@ -258,6 +263,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         const bool mok = m < M;
         const float wl = (top && mok) ? net.W[L - 1][m] : 0.f;
         float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
+        constexpr bool CARRY = BWD_TC_CARRY && BWD_SV == 12;
+        float c_s1[CPE], c_s2tr[CPE];  // CARRY: sigma'(z), sigma''(z) (r . t) per centre of this thread
         // ---- phase A (X-independent, overlaps this layer's MMA): the pair maps of every
         // centre of this thread -- A_a, S_a and the derivative factors P, Dd, Z -- from the
         // stored forward pre-activations, stashed in this thread's TMEM lane
@@ -296,6 +303,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             float pv[NCOLB];
 #pragma unroll
             for (int j = 0; j < NCOLB; ++j) pv[j] = 0.f;
+            if (CARRY) c_s1[i] = c_s2tr[i] = 0.f;
             if (mok && valid) {
               const typename AF::C cc = AF::centre(q.z, beta);
 #pragma unroll
@@ -307,6 +315,10 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                 const float tr = fmaf(sd[5], q.t0, fmaf(sd[6], q.t1, sd[7] * q.t2));
                 pv[0] = AF::value(cc, beta);
                 pv[1] = AF::d1(cc, beta) * tr;
+                if (CARRY) {
+                  c_s1[i] = AF::d1(cc, beta);
+                  c_s2tr[i] = AF::d2(cc, beta) * tr;
+                }
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                   pv[2 + 2 * p] = t[5 * p];
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         auto ldz = [&](int i, float (&z4)[4]) {
           const int64_t c = c0 + eg + EG * i;
           z4[0] = z4[1] = z4[2] = z4[3] = 0.f;
-          if (i < CPE && c < a.n && mok) {
+          if (!CARRY && i < CPE && c < a.n && mok) {
             const float* zq = a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + m;
             z4[0] = __ldg(zq);
             z4[1] = __ldg(zq + 1 * MPAD);
@@ -443,8 +455,17 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           for (int j = 0; j < NCOLB; ++j) dl[j] = pv[j] = 0.f;
           float w0p[3] = {0.f, 0.f, 0.f};
           if (mok && valid) {
-            const float tr = fmaf(r0, zc[1], fmaf(r1, zc[2], r2 * zc[3]));
-            const typename AF::C cc = AF::centre(zc[0], beta);
+            float tr = 0.f, s1, s2tr;
+            typename AF::C cc{};
+            if (CARRY) {
+              s1 = c_s1[i];
+              s2tr = c_s2tr[i];
+            } else {
+              tr = fmaf(r0, zc[1], fmaf(r1, zc[2], r2 * zc[3]));
+              cc = AF::centre(zc[0], beta);
+              s1 = AF::d1(cc, beta);
+              s2tr = AF::d2(cc, beta) * tr;
+            }
             float zbar = 0.f;
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
@@ -466,13 +487,14 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                 w0p[2] = fmaf(dA, h * dpz, w0p[2]);
               }
             }
-            const float s1 = AF::d1(cc, beta), s2 = AF::d2(cc, beta);
             const float Xc = X[0], Xt = X[1];
-            const float zb = fmaf(Xc, s1, fmaf(s2 * tr, Xt, zbar));
+            const float zb = fmaf(Xc, s1, fmaf(s2tr, Xt, zbar));
             dl[0] = om * zb;
             dl[1] = om * s1 * Xt;
-            pv[0] = AF::value(cc, beta);
-            pv[1] = s1 * tr;
+            if (SV == 20) {
+              pv[0] = AF::value(cc, beta);
+              pv[1] = s1 * tr;
+            }
             if (l == 0) {  // a^{-1}: centre -> x0, tangent -> r
               w0p[0] = fmaf(dl[0], sd[16], fmaf(dl[1], r0, w0p[0]));
               w0p[1] = fmaf(dl[0], sd[17], fmaf(dl[1], r1, w0p[1]));
