@@ -16,8 +16,10 @@
 
 namespace fdsdf {
 
+// L2 prefetch of the stored forward pre-activations: 1 = one layer of one tile (8 x 12 KB bulk
+// prefetches) issued one MMA pass before phase A reads it; 0 = none
 #ifndef BWD_TC_PREFETCH
-#define BWD_TC_PREFETCH 0
+#define BWD_TC_PREFETCH 1
 #endif
 #ifndef BWD_TC_WPK
 #define BWD_TC_WPK 3
@@ -121,17 +123,18 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     uint32_t nd = 0;
     PhaseTimer ptimer;
     ptimer.start();
-    // the stored forward pre-activations of a tile are one contiguous block of zf
-    auto prefetch_tile = [&](int64_t tile) {
-      if (et == 0 && tile < a.ntiles) {
-        const int64_t cb = tile * CT, ce = min(cb + CT, a.n);
-        const size_t per = (size_t)nh * NCOLF * MPAD * sizeof(float);
-        const char* p0 = reinterpret_cast<const char*>(a.zf) + (size_t)cb * per;
-        for (size_t off = 0; off < (size_t)(ce - cb) * per; off += 65536)
-          prefetch_l2_bulk(p0 + off, (uint32_t)min((size_t)65536, (size_t)(ce - cb) * per - off));
+    // layer l of the stored forward pre-activations of tile `tile`: per centre one contiguous
+    // NCOLF x MPAD block of zf (one thread issues the bulk L2 prefetches)
+    auto prefetch_layer = [&](int64_t tile, int l) {
+      if (BWD_TC_PREFETCH && et == 0 && tile < a.ntiles && l >= 0) {
+        for (int cl = 0; cl < CT; ++cl) {
+          const int64_t c = tile * CT + cl;
+          if (c < a.n)
+            prefetch_l2_bulk(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD, (uint32_t)(NCOLF * MPAD * sizeof(float)));
+        }
       }
     };
-    if (BWD_TC_PREFETCH) prefetch_tile(blockIdx.x);
+
 
     // per-tile seeds + coordinates, double-buffered: the next tile's are copied asynchronously
     // (cp.async) while this tile runs
@@ -216,7 +219,10 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
 #endif
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, spar ^= 1u) {
       const int64_t c0 = tile * CT;
-      if (BWD_TC_PREFETCH) prefetch_tile(tile + gridDim.x);
+      // this tile's first MMA pass reads layer L-3; the next tile's top layer (computed during
+      // this tile's passes) reads layer L-2 of that tile
+      prefetch_layer(tile, L - 3);
+      prefetch_layer(tile + gridDim.x, L - 2);
       cp_async_wait_all();
       bar_named(1, C::NEPI * 32);  // this tile's seeds are in; every thread is done with the other buffer
       const float* sds = sds0 + spar * CT * 20;
@@ -265,6 +271,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
         constexpr bool CARRY = BWD_TC_CARRY && BWD_SV == 12;
         float c_s1[CPE], c_s2tr[CPE];  // CARRY: sigma'(z), sigma''(z) (r . t) per centre of this thread
+        if (!top) prefetch_layer(tile, l - 1);  // the next pass's phase A
         // ---- phase A (X-independent, overlaps this layer's MMA): the pair maps of every
         // centre of this thread -- A_a, S_a and the derivative factors P, Dd, Z -- from the
         // stored forward pre-activations, stashed in this thread's TMEM lane
