@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           const bool valid = c < a.n;
           const float z0 = z0n;
           z0n = ldz(i + 1);
-          if (MODE == 1) {
+          if constexpr (MODE == 1) {
             float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
             if (l == 0) {
               float x0 = 0.f, x1 = 0.f, x2 = 0.f;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               put_b(cl * 4 + 2, o2);
               put_b(cl * 4 + 3, o3);
             }
-          } else if (FWD_TC_FRAG) {
+          } else if constexpr (FWD_TC_FRAG) {
             // fragment form: this thread handles pair p = lane % 4 for the 4 neurons
             // m_base + lane/4 + 8j (j = 0..3) of its warp, as laid out by tcgen05.ld 16x256b;
             // the outputs go to the B operand through stmatrix.trans (16-byte K-major chunks)
