@@ -412,14 +412,17 @@ static void fill_fwd(fdsdf_ctx* c, FwdArgs& a, const float* d_x, int64_t n, cons
 
 // tensor-core forward: mode 1 (centre + tangents -> f, g, frame) then mode 2 (stencil pairs ->
 // FD epilogue).  Sets a.ntiles per launch; records the mode-2 grid in c->last_fgrid.
-static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t strm) {
+// pairs_only: skip mode 1 and reuse the centre info / centre pre-activations a previous call
+// left in the workspace (fdsdf_eval_hessian's 2nd and 3rd frame passes)
+static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t strm, bool pairs_only = false) {
   a.wimg = c->fimg;
   a.cinfo = c->cinfo;
   const int64_t n = a.n;
   if (c->pair) {  // CTA-pair kernels: two half-tile slots in flight per pair
     a.ntiles = (n + fwd_tc2_tile_centres(1) - 1) / fwd_tc2_tile_centres(1);
     const int g1 = 2 * (int)std::min<int64_t>(c->nsm / 2, a.ntiles);
-    cudaError_t e = run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc2(a, 1, g1, strm); });
+    cudaError_t e = pairs_only ? cudaSuccess
+                               : run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc2(a, 1, g1, strm); });
     if (e != cudaSuccess) return e;
     a.ntiles = (n + fwd_tc2_tile_centres(2) - 1) / fwd_tc2_tile_centres(2);
     const int g2 = 2 * (int)std::min<int64_t>(c->nsm / 2, a.ntiles);
@@ -428,7 +431,8 @@ static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t str
   }
   a.ntiles = (n + fwd_tc_tile_centres(1) - 1) / fwd_tc_tile_centres(1);
   const int g1 = (int)std::min<int64_t>(c->nsm, a.ntiles);
-  cudaError_t e = run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc(a, 1, g1, strm); });
+  cudaError_t e = pairs_only ? cudaSuccess
+                             : run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc(a, 1, g1, strm); });
   if (e != cudaSuccess) return e;
   a.ntiles = (n + fwd_tc_tile_centres(2) - 1) / fwd_tc_tile_centres(2);
   const int g2 = (int)std::min<int64_t>(c->nsm, a.ntiles);
@@ -438,11 +442,24 @@ static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t str
 
 extern "C" {
 
+// the body of fdsdf_eval (arguments already validated); pairs_only: see launch_fwd_tc_pair
+static fdsdf_status eval_run(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n,
+                             const fdsdf_stencil* st, const fdsdf_eval_out* out, cudaStream_t strm,
+                             bool pairs_only);
+
 fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
                         const fdsdf_eval_out* out, void* stream) {
   fdsdf_status s = check_common(c, d_params, d_x, n, st);
   if (s != FDSDF_OK) return s;
-  cudaStream_t strm = (cudaStream_t)stream;
+  return eval_run(c, d_params, d_x, n, st, out, (cudaStream_t)stream, false);
+}
+
+}  // extern "C"
+
+static fdsdf_status eval_run(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n,
+                             const fdsdf_stencil* st, const fdsdf_eval_out* out, cudaStream_t strm,
+                             bool pairs_only) {
+  pairs_only = pairs_only && c->tc;  // the FFMA forward is one fused kernel
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != c->device) cudaSetDevice(c->device);
@@ -450,7 +467,7 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   c->launches = 0;
   cudaError_t e = cudaSuccess;
   if (c->tc) {
-    if (c->ngemm > 0)
+    if (c->ngemm > 0 && !pairs_only)
       e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, nullptr, strm); });
   } else if (c->ngemm > 0) {
     e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
@@ -476,7 +493,7 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   if (c->tc) {
     a.zf = c->eval_only ? c->zev : c->zf;
     a.zcols = c->eval_only ? 1 : NCOLF;
-    e = launch_fwd_tc_pair(c, a, strm);
+    e = launch_fwd_tc_pair(c, a, strm, pairs_only);
     if (prev != c->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(c, e, "fwd_tc_kernel");
     return FDSDF_OK;
@@ -487,6 +504,8 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   if (e != cudaSuccess) return cuda_fail(c, e, "fwd_kernel");
   return FDSDF_OK;
 }
+
+extern "C" {
 
 fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, float h,
                                 float* d_H, float* d_f, float* d_grad, void* stream) {
@@ -509,8 +528,13 @@ fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* c, const float* d_params, const float
   int launches = 0;
   c->launches = 0;
   for (int pass = 0; pass < 3; ++pass) {
-    cudaError_t e = run_slot(c, FDSDF_KSLOT_HESS, strm,
-                             [&] { return launch_axis_frames(c->hframes, n, AX[pass][0], AX[pass][1], strm); });
+    // tensor path, passes 1 and 2: f, grad f and the centre pre-activations are those of pass 0;
+    // only the frame changes -> rewrite the frame fields of the centre info, run the pair kernel
+    const bool pairs_only = c->tc && pass > 0;
+    cudaError_t e = run_slot(c, FDSDF_KSLOT_HESS, strm, [&] {
+      return pairs_only ? launch_cinfo_axis_frames(c->cinfo, n, AX[pass][0], AX[pass][1], strm)
+                        : launch_axis_frames(c->hframes, n, AX[pass][0], AX[pass][1], strm);
+    });
     if (e != cudaSuccess) {
       if (prev != c->device) cudaSetDevice(prev);
       return cuda_fail(c, e, "axis_frames_kernel");
@@ -522,7 +546,7 @@ fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* c, const float* d_params, const float
       out.d_grad = d_grad;
     }
     launches += c->launches;
-    s = fdsdf_eval(c, d_params, d_x, n, &st, &out, stream);
+    s = eval_run(c, d_params, d_x, n, &st, &out, strm, pairs_only);
     if (s != FDSDF_OK) {
       if (prev != c->device) cudaSetDevice(prev);
       return s;

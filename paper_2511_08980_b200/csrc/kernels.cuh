@@ -145,6 +145,7 @@ cudaError_t launch_adam(float* p, const float* g, float* m, float* v, int64_t n,
                         float eps, int64_t t, unsigned* dflags, cudaStream_t st);
 cudaError_t launch_axis_frames(float* frames, int64_t n, int a, int b, cudaStream_t st);
 cudaError_t launch_hess_scatter(const float* t, float* H, int64_t n, int pass, cudaStream_t st);
+cudaError_t launch_cinfo_axis_frames(float* cinfo, int64_t n, int a, int b, cudaStream_t st);
 int fwd_tile_centres(int mpad);   // centres per forward tile
 int bwd_tile_centres(int mpad);   // centres per backward tile
 size_t fwd_smem_bytes(int mpad);

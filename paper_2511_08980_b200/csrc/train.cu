@@ -155,6 +155,19 @@ cudaError_t launch_axis_frames(float* frames, int64_t n, int a, int b, cudaStrea
   return cudaGetLastError();
 }
 
+// the (u, v) fields [4, 10) of the 16-float centre info of every row (fdepi.cuh layout)
+__global__ void cinfo_axis_frames_kernel(float* cinfo, int64_t n, int a, int b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 6; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % 6);
+    cinfo[(i / 6) * 16 + 4 + k] = (k < 3 ? (k == a) : (k - 3 == b)) ? 1.f : 0.f;
+  }
+}
+
+cudaError_t launch_cinfo_axis_frames(float* cinfo, int64_t n, int a, int b, cudaStream_t st) {
+  cinfo_axis_frames_kernel<<<ew_grid(n * 6), 256, 0, st>>>(cinfo, n, a, b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hess_scatter(const float* t, float* H, int64_t n, int pass, cudaStream_t st) {
   hess_scatter_kernel<<<ew_grid(n), 256, 0, st>>>(t, H, n, pass);
   return cudaGetLastError();
