@@ -30,12 +30,15 @@ def _model(spec, n, path=None, eval_only=True):
 
 # (config, surface rows, uniform rows, h): C1 softplus (MPAD 128) and C2 SIREN (MPAD 256) at
 # their h, plus C2 at the h = 1e-2 of the entry gate; the centre counts leave ragged tiles
-@pytest.mark.parametrize("name,ns,nu,h", [("c1", 300, 211, None), ("c2", 333, 300, None), ("c2", 200, 177, 1e-2)])
+@pytest.mark.parametrize("name,ns,nu,h,eval_only", [("c1", 300, 211, None, True), ("c2", 333, 300, None, True),
+                                                     ("c2", 200, 177, 1e-2, True), ("c2", 150, 121, None, False)])
 @pytest.mark.parametrize("path", ["ffma", "tensor"])
-def test_hessian_parity(name, ns, nu, h, path):
+def test_hessian_parity(name, ns, nu, h, eval_only, path):
+    """eval_only = False: a training context, whose centre pre-activations live in the step
+    workspace (12 columns per layer) that the 2nd / 3rd passes reuse on the tensor path."""
     c = make_config(name, ns, nu, h=h)
     n = len(c["x"])
-    m = _model(c["spec"], n, path=path)
+    m = _model(c["spec"], n, path=path, eval_only=eval_only)
     f = torch.empty(n, device="cuda")
     g = torch.empty(n, 3, device="cuda")
     H = m.eval_hessian(c["params"], c["x"], c["h"], f=f, g=g).cpu().numpy()
