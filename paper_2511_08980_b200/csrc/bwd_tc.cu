@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                 "column permutation 8 j + cl assumes 8 centres x 10 columns, one or two accumulator ranges");
   static_assert(C::RANGES == 1 || BWD_TC_COLPERM, "two ranges are read with the permuted column loads");
   constexpr int SV = BWD_SV;
+  FDSDF_ASSERT((int)C::TCOLS >= C::MH * C::DH + C::MH * EG * CPE * SV);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = smem_raw;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
 
     // write delta (10 columns of centre slot cl, neuron m) as the next GEMM's B operand
     auto put_b10 = [&](int cl, const float (&dl)[NCOLB]) {
+      FDSDF_ASSERT(cl >= 0 && cl < CT && m >= 0 && m < MPAD);
       if (BWD_TC_COLPERM) {
         // sw128_off(8 j + cl, m) = (m / 64) BKC + 1024 j + 128 cl + (((m % 64) / 8 ^ cl) << 4) + 2 (m % 8)
         unsigned char* bp = Bs + (m >> 6) * C::BKC + cl * 128 + ((((m & 63) >> 3) ^ cl) << 4) + ((m & 7) << 1);
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       if (tl >= a.ntiles || c >= a.n || m >= net.width[ltop + 1]) return;
       const float omt = net.omega[ltop];
       const float wlt = net.W[L - 1][m];
+      FDSDF_ASSERT(c >= 0 && c < a.n);
       const float* zq = a.zf + ((size_t)c * nh + ltop) * NCOLF * MPAD + m;
       float zv[NCOLF];
 #pragma unroll
@@ -204,6 +207,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       dl[1] = omt * s1 * Xt;
       pv[0] = AF::value(cc, beta);
       pv[1] = s1 * tr;
+      FDSDF_ASSERT(c >= 0 && c < a.n && ltop >= 0 && ltop < nh);
       float* dp = a.del + ((size_t)ltop * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
       for (int j = 0; j < NCOLB; ++j) dp[j * MPAD] = dl[j];
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           Zq q{};
           const int64_t c = c0 + eg + EG * i;
           if (i < CPE && c < a.n && mok) {
+            FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
             const float* zq = a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + m;
             q.z = __ldg(zq);
             q.t0 = __ldg(zq + 1 * MPAD);
@@ -335,6 +340,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             }
             if (SV == 12) {
               if (valid && l <= L - 3) {
+                FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
                 float* ap = a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
                 for (int j = 0; j < NCOLB; ++j) ap[j * MPAD] = pv[j];
@@ -510,6 +516,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           }
           if (valid) {
             if (l >= 1) {
+              FDSDF_ASSERT(c >= 0 && c < a.n && l >= 1 && l < nh);
               float* dp = a.del + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
               for (int j = 0; j < NCOLB; ++j) dp[j * MPAD] = dl[j];

@@ -7,9 +7,26 @@
 //    logistic / expm1 / log1p helpers of the softplus identities.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace fdsdf {
+
+// Debug builds (-DFDSDF_DEBUG_ASSERT, scripts/build_variant.py): device-side bounds checks of
+// the computed shared-memory, TMEM-column and global indices of the tensor kernels (the
+// stand-in for compute-sanitizer memcheck, which this GPU pool does not allow).  No-op otherwise.
+#ifdef FDSDF_DEBUG_ASSERT
+#define FDSDF_ASSERT(cond)                                                                       \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("FDSDF_ASSERT failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #cond);                                                           \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define FDSDF_ASSERT(cond) ((void)0)
+#endif
 
 // ----------------------------------------------------------------------------- PTX: mbarrier + bulk copy
 

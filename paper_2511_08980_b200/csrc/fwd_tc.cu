@@ -178,12 +178,14 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
 
     // this thread's element of stored pre-activation column `col`, layer l, centre c
     auto zp = [&](int64_t c, int l, int col) -> float* {
+      FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && col >= 0 && col < a.zcols && m < MPAD);
       return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
     };
     auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
     // this thread's stash columns: CPE centres x CPC values (FWD_PIPE0)
     const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + MH * C::DH + (hh * C::EG + eg) * CPE * CPC;
     const bool pipe0 = FWD_PIPE0 && ngemm > 0;
+    FDSDF_ASSERT(!FWD_PIPE0 || (MH * C::DH + (hh * C::EG + eg + 1) * CPE * CPC) <= (int)C::TCOLS);
     // layer 0 of centre i of tile tl (centre info cis_t): pre-activations -> zf, activations ->
     // this thread's stash columns (exactly the l == 0 arithmetic of the epilogue below)
     auto layer0_centre = [&](int64_t tl, int i, const float* cis_t) {
@@ -231,8 +233,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         tc::tmem_st4(tstash + i * CPC, o);
       } else {
         const float* ci = cis_t + cl * NCINFO;
-        float* zc0 = zp(c, 0, 0);
-        const float z0 = valid ? __ldg(zc0) : 0.f;
+        const float z0 = valid ? __ldg(zp(c, 0, 0)) : 0.f;
         float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
         if (mok) {
           const float* W0 = net.W[0];
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           Av[3] = hs * (du - dv);
         }
         if (step && valid) {
+          float* zc0 = zp(c, 0, 0);
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
             zc0[(4 + 2 * p) * MPAD] = Av[p];

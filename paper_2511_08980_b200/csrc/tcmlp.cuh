@@ -274,6 +274,7 @@ __device__ __forceinline__ void tc_epi_arrive(const TcBars& b, int sp = 0) {
 // k/64 holds the pieces as row blocks [b0 | b1 | b2] of N rows each (SWIZZLE_128B rows)
 template <class C>
 __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float v) {
+  FDSDF_ASSERT(n >= 0 && n < C::NSPLIT * C::NS && k >= 0 && k < C::MPAD);
   const tc::Bf3 s = tc::split3(v);
   const int sp = n / C::NS, nl = n % C::NS;
   const uint32_t off = (uint32_t)((k >> 6) * C::BKC + sp * 3 * C::NS * 128) + tc::sw128_off(nl, k & 63, C::NS);
@@ -285,6 +286,7 @@ __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float 
 // TMEM ranges (range 0 + (range 1 + range 2), smallest terms first)
 template <class C>
 __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8]) {
+  FDSDF_ASSERT(col >= 0 && col + 8 <= C::NSPLIT * C::NS);
   static_assert(C::RANGES != 2, "two-range accumulators: sum the ranges at the call site");
   if (C::RANGES == 1) {
     tc::tmem_ld8(taddr + col, v);
@@ -316,6 +318,7 @@ __device__ __forceinline__ void tc_ld_sum_frag(uint32_t taddr, int col, float (&
 
 template <class C>
 __device__ __forceinline__ void tc_ld_sum2(uint32_t taddr, int col, float (&v)[2]) {
+  FDSDF_ASSERT(col >= 0 && col + 2 <= C::NSPLIT * C::NS);
   static_assert(C::RANGES != 2, "two-range accumulators: sum the ranges at the call site");
   if (C::RANGES == 1) {
     tc::tmem_ld2(taddr + col, v);

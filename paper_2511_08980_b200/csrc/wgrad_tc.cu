@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
           dv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           av[q] = dv[q];
           if (j < j1) {
+            FDSDF_ASSERT(j >= 0 && j < a.rows && r + 4 <= MPAD && layer >= 1);
             dv[q] = __ldg(reinterpret_cast<const float4*>(D + j * MPAD + r));
             av[q] = __ldg(reinterpret_cast<const float4*>(A + j * MPAD + r));
           }
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
           const int item = st + q * C::NSTG * 32;
           const int jj = item / QUADS, r = (item % QUADS) * 4;
           const uint32_t off = tc::sw128mn_off(r, jj, MPAD);
+          FDSDF_ASSERT(off + 8 <= (uint32_t)C::PIECE);
           uint32_t d01[3], d23[3], a01[3], a23[3];
           tc::split3x2(dv[q].x, dv[q].y, d01);
           tc::split3x2(dv[q].z, dv[q].w, d23);
