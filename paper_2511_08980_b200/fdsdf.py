@@ -437,6 +437,25 @@ class Trainer:
         self.mom2 = torch.zeros_like(self.grad)
         self.t = 0
 
+    def state_dict(self):
+        """Checkpoint of the training state (SURVEY §5 checkpoint / resume): parameters, the
+        Adam moments and the iteration counter (which also keys the batch sampler and the
+        frame seeds, so a resumed run continues the same sample / frame sequence).  Host
+        copies; the caller persists them (e.g. torch.save)."""
+        return {"params": self.params.cpu(), "mom1": self.mom1.cpu(), "mom2": self.mom2.cpu(), "t": int(self.t),
+                "seed": int(self.seed)}
+
+    def load_state_dict(self, st):
+        """Restore a state_dict() checkpoint (shapes must match this model)."""
+        for k in ("params", "mom1", "mom2"):
+            src = st[k]
+            dst = getattr(self, k)
+            if tuple(src.shape) != tuple(dst.shape):
+                raise ValueError(f"checkpoint {k} has shape {tuple(src.shape)}, model needs {tuple(dst.shape)}")
+            dst.copy_(src.to(dst.device, dst.dtype))
+        self.t = int(st["t"])
+        self.seed = int(st["seed"])
+
     def frame_seed(self, it):
         """Per-iteration frame seed: frames are redrawn every iteration; the same
         convention as harness.frame_seed (high 32 bits: base seed, low 32 bits: iteration)."""

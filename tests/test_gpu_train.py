@@ -108,3 +108,34 @@ def test_training_loop_matches_oracle():
     rel = np.linalg.norm(d_gpu - d_ref) / np.linalg.norm(d_ref)
     print("param-update rel L2", rel)
     assert rel <= 1e-2
+
+
+def test_checkpoint_resume_is_exact():
+    """Trainer.state_dict / load_state_dict: 2 iterations, checkpoint, 2 more -- equals 4
+    uninterrupted iterations bit for bit (parameters, moments, the iteration counter that keys
+    the sampler and the frame seeds), also when resumed into a fresh context."""
+    from paper_2511_08980_b200.fdsdf import Trainer
+    c = make_config("c1", 16, 16)
+    spec, params, lc = c["spec"], c["params"], dict(c["loss"])
+    lc.update(w_dm=1.0, lambda_dnm=100.0, lambda_eik=50.0, lambda_fd=1.0)
+    pool = sphere_surface(300, 0.5, seed=4).astype(np.float32)
+    args = (pool, 150, 150, 1.0, 1e-2, lc)
+    m = _model(spec, 300)
+    ref = Trainer(m, params, *args, seed=7, lr=1e-3)
+    for _ in range(4):
+        ref.iterate()
+    a = Trainer(m, params, *args, seed=7, lr=1e-3)
+    for _ in range(2):
+        a.iterate()
+    st = a.state_dict()
+    m2 = _model(spec, 300)
+    b = Trainer(m2, np.zeros_like(params), *args, seed=0, lr=1e-3)
+    b.load_state_dict(st)
+    for _ in range(2):
+        b.iterate()
+    torch.cuda.synchronize()
+    for k in ("params", "mom1", "mom2"):
+        assert torch.equal(getattr(ref, k).cpu(), getattr(b, k).cpu()), k
+    assert b.t == ref.t == 4
+    with pytest.raises(ValueError):
+        b.load_state_dict({**st, "params": st["params"][:-1]})
