@@ -188,3 +188,36 @@ def test_tiny_batches(n, path):
                     frames=(g["frames"][:, :3], g["frames"][:, 3:]))
     err = compare_eval(g, o)
     assert max(err[k] for k in ("f", "g", "fuu", "fuv", "fvv")) <= 1.0, err
+
+
+# ragged, unequal hidden widths (not multiples of 32 / 64): zero-padded neuron rows and K
+# ranges inside the tensor tiles (MPAD 256), both activations, a 3-GEMM network
+RAGGED = [("sine", [3, 100, 200, 150, 1]), ("softplus", [3, 37, 129, 90, 61, 1])]
+
+
+@pytest.mark.parametrize("act,widths", RAGGED)
+def test_ragged_widths_eval_and_step(act, widths, path):
+    from harness import init_params, mlp_spec, uniform_box, csg_surface
+    spec = mlp_spec(widths, act, beta=100.0)
+    params = init_params(spec, "siren" if act == "sine" else "xavier", 11)
+    xs = csg_surface(150, 3, 12).astype(np.float32)
+    xu = uniform_box(131, 1.1, 13).astype(np.float32)
+    x = np.concatenate([xs, xu])
+    n, ns, h = len(x), len(xs), 1e-2
+    ls = loss_cfg("ncr", "paper", w_dm=1, lambda_dnm=100, lambda_eik=50, lambda_fd=1)
+    c = dict(spec=spec, params=params, x=x, n_surface=ns, h=h, frame_seed=5, loss=ls)
+    m = _model(spec, n, path=path)
+    g = gpu_eval(m, c)
+    o = oracle_eval(spec, params, x, ns, h, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    err = compare_eval(g, o)
+    print(act, widths, path, {k: float(v) for k, v in err.items()})
+    for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K"):
+        assert err[k] <= 1.0, (k, err)
+    grad, loss = m.step(params, x, ns, h, ls, frame_seed=5)
+    grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
+    o = oracle_step(spec, params, x, ns, h, ls, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
+    gerr = per_tensor_grad_errors(spec, grad, o["grad"])
+    print("lerr", lerr, "gerr", gerr)
+    assert np.all(lerr[o["loss"][:5] != 0] <= LOSS_RTOL), lerr
+    assert np.all(gerr <= GRAD_RTOL), gerr
