@@ -38,6 +38,11 @@ namespace fdsdf {
 #ifndef FWD_TC_NEPI
 #define FWD_TC_NEPI 16
 #endif
+// GEMM columns per tile (mode 1: N/4 centres, mode 2: N/8 centres); with FWD_TC_NEPI the
+// epilogue warps (a multiple of 4 x M-halves whose centre groups divide the tile)
+#ifndef FWD_TC_N
+#define FWD_TC_N 64
+#endif
 #ifndef FWD_TC_PAIR_WPK
 #define FWD_TC_PAIR_WPK 3
 #endif
@@ -51,11 +56,11 @@ constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && !FWD_TC_FRAG && FWD_TC_NSPLIT == 1;
 // mode 1 (centre + tangents: they set g, the frames and the |g|^p denominators) streams all
 // three weight pieces; mode 2 (the stencil-pair differences) streams FWD_TC_PAIR_WPK
 template <int MPAD, int MODE>
-struct FtcCfg : TcCfg<MPAD, 64, FWD_TC_NEPI, 3, FWD_PIPE0 ? 64 * (MPAD / 128) : 0, FWD_TC_NSPLIT,
+struct FtcCfg : TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT,
                       MODE == 1 ? 3 : FWD_TC_PAIR_WPK> {
   // TMEM stash (FWD_PIPE0): the next tile's layer-0 outputs, (MH x EG thread groups) x CPE x
-  // columns per centre = MH x 64 columns
-  using B = TcCfg<MPAD, 64, FWD_TC_NEPI, 3, FWD_PIPE0 ? 64 * (MPAD / 128) : 0, FWD_TC_NSPLIT,
+  // columns per centre = MH x N columns
+  using B = TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT,
                   MODE == 1 ? 3 : FWD_TC_PAIR_WPK>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
@@ -73,7 +78,7 @@ bool tc_supported(int mpad, int skip) { return (mpad == 128 || mpad == 256) && s
 
 size_t tc_wimg_bytes(int mpad, int ngemm) { return (size_t)(ngemm > 0 ? ngemm : 0) * mpad * mpad * 2 * tc::WP; }
 
-int fwd_tc_tile_centres(int mode) { return mode == 1 ? 16 : 8; }
+int fwd_tc_tile_centres(int mode) { return mode == 1 ? FWD_TC_N / 4 : FWD_TC_N / 8; }
 
 // ----------------------------------------------------------------------------- weight images
 // image[g][kc][h][piece < WP][sw128 128 rows x 64 k]: forward A operand = W_l (rows = output
