@@ -9,16 +9,19 @@
 //           difference form (act.cuh; P:L83-91 regrouped); last layer -> S_p; per centre the
 //           FD epilogue (fdepi.cuh: f_uu, f_vv, f_uv, D_FD, K_FD, Eq. (1), seeds).
 // Every hidden GEMM layer is D[m][n] = sum_k W[m][k] B[k][n] with M = MPAD output neurons
-// (MPAD/128 tcgen05 M-halves), N = 64 columns, K = MPAD:
+// (MPAD/128 tcgen05 M-halves), N = FWD_TC_N (64) columns, K = MPAD (engine: tcmlp.cuh):
 //   warp 0      one thread streams the pre-packed bf16x3 weight image through a 2-stage
 //               shared-memory ring with the TMA bulk engine (cp.async.bulk + mbarrier tx);
-//   warp 1      allocates TMEM; one thread issues the 6 piece MMAs per 16-wide K step
-//               (tcgen05.mma kind::f16, fp32 accumulate in TMEM) and commits to mbarriers;
-//   warps 2..9  epilogue: thread = output neuron (TMEM lane), reads its row of D with
-//               tcgen05.ld, applies bias / omega / the activation (centre + tangents, or the
-//               cancellation-free pair maps), stores the pre-activations the backward needs,
-//               splits the outputs into bf16 pieces and writes them into the K-major
-//               SWIZZLE_128B B operand of the next layer.
+//   warp 1      allocates TMEM; the warp runs the issue loop, one elected lane issues the
+//               six bf16x6 piece products per 16-wide K step as three MMAs into three TMEM
+//               ranges (tcgen05.mma kind::f16, fp32 accumulate) and commits to mbarriers;
+//   warps 2..17 epilogue (16 warps): thread = output neuron (TMEM lane), reads its row of D
+//               with tcgen05.ld, applies bias / omega / the activation (centre + tangents, or
+//               the cancellation-free pair maps), stores the pre-activations the backward
+//               needs, splits the outputs into bf16 pieces and writes them into the K-major
+//               SWIZZLE_128B B operand of the next layer.  X-independent work -- the next
+//               tile's layer 0, the previous tile's per-centre FD epilogue -- runs while the
+//               layer's MMA is in flight.
 // Layer 0 (fan-in 3) and the last layer (fan-out 1) are computed by the epilogue threads
 // directly (FFMA) -- they are not contractions worth a tensor-core pass.
 #include "act.cuh"
@@ -164,8 +167,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
     if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
   } else {
     // ------------------------------------------------------------------ epilogue warps
-    const int ew = warp - 2;                 // 0..7
-    const int et = tid - 64;                 // 0..255
+    const int ew = warp - 2;                 // 0 .. NEPI-1
+    const int et = tid - 64;                 // 0 .. NEPI*32-1
     const int q4 = warp & 3;                 // TMEM lane quarter
     const int hh = (ew >> 2) % MH;           // M-half
     const int eg = ew / (4 * MH);            // centre group

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
   } else {
     // ------------------------------------------------------------------ stagers + readback
     const int sw = warp - 1;        // 0 .. NSTG-1
-    const int st = tid - 32;        // 0..255
+    const int st = tid - 32;        // 0 .. NSTG*32-1
     uint32_t it = 0;
     constexpr int QUADS = MPAD / 4;  // float4 per j row
     {
