@@ -11,6 +11,12 @@
 // contraction, the next B operand, and accumulates -- each thread for its own neuron, in
 // fixed tile order -- the bias gradients, dW of the last layer (fan-out 1) and of the first
 // layer (fan-in 3).
+// Schedule per layer: phase A (X-independent, while the layer's MMA runs: the pair maps'
+// derivative factors into spare TMEM columns, the layer's activations, sigma'(z) and
+// sigma''(z) (r . t) handed to phase B, part of the NEXT tile's top layer, an L2 prefetch of
+// the next layer's stored pre-activations), then phase B (with X: delta, its stores and the
+// bf16x3 split into the next B operand).  X is accumulated in two TMEM ranges:
+// a0.[b0|b1] + a1.[b0|b1] and a0.b2 + a2.b0.
 #include "act.cuh"
 #include "tcmlp.cuh"
 
