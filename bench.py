@@ -483,6 +483,11 @@ def main():
                 "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_max)) if clocks.get("sm_mhz") else None}
     step_alg = sum(alg.values())
     kernel_ms = {k: round(v, 4) for k, v in kms.items() if ktimes[k][1]}
+    # the same model for every contraction kernel: achieved algorithmic TFLOP/s and its fraction
+    # of the roofline's peak (the dominant kernel is `roofline` above)
+    roof["per_kernel"] = {k: {"achieved": alg[k] / (kms[k] * 1e-3) / 1e12,
+                              "frac": alg[k] / (kms[k] * 1e-3) / 1e12 / peak}
+                          for k in alg if kms.get(k)}
 
     # ------------------------------------------------------------------ CPU oracle baseline
     cpu = None
