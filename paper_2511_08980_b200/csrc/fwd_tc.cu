@@ -30,11 +30,6 @@
 
 namespace fdsdf {
 
-// FWD_TC_FRAG = 1: the pair epilogue in tcgen05.ld 16x256b fragment form with stmatrix.trans
-// B stores (parity-tested; measured 12% slower than the thread-per-neuron form)
-#ifndef FWD_TC_FRAG
-#define FWD_TC_FRAG 0
-#endif
 #ifndef FWD_TC_NSPLIT
 #define FWD_TC_NSPLIT 1
 #endif
@@ -55,7 +50,7 @@ namespace fdsdf {
 #ifndef FWD_TC_PIPE0
 #define FWD_TC_PIPE0 1
 #endif
-constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && !FWD_TC_FRAG && FWD_TC_NSPLIT == 1;
+constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && FWD_TC_NSPLIT == 1;
 // mode 1 (centre + tangents: they set g, the frames and the |g|^p denominators) streams all
 // three weight pieces; mode 2 (the stencil-pair differences) streams FWD_TC_PAIR_WPK
 template <int MPAD, int MODE>
@@ -123,17 +118,6 @@ cudaError_t launch_pack_tc(const Net& net, unsigned char* fimg, unsigned char* b
 }
 
 // ----------------------------------------------------------------------------- the kernel
-// shuffle a struct of floats (the activation's per-neuron centre values) from lane `src`
-template <class T>
-__device__ __forceinline__ T shfl_struct(const T& v, int src) {
-  static_assert(sizeof(T) % 4 == 0, "struct of 32-bit words");
-  T r;
-  const float* a = reinterpret_cast<const float*>(&v);
-  float* b = reinterpret_cast<float*>(&r);
-#pragma unroll
-  for (int i = 0; i < (int)(sizeof(T) / 4); ++i) b[i] = __shfl_sync(0xffffffffu, a[i], src);
-  return r;
-}
 
 template <int ACT, int MPAD, int MODE>
 __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(const FwdArgs a) {
@@ -483,92 +467,6 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               put_b(cl * 4 + 1, o1);
               put_b(cl * 4 + 2, o2);
               put_b(cl * 4 + 3, o3);
-            }
-          } else if constexpr (FWD_TC_FRAG) {
-            // fragment form: this thread handles pair p = lane % 4 for the 4 neurons
-            // m_base + lane/4 + 8j (j = 0..3) of its warp, as laid out by tcgen05.ld 16x256b;
-            // the outputs go to the B operand through stmatrix.trans (16-byte K-major chunks)
-            const float* ci = cis + cl * NCINFO;
-            const int pp = lane & 3, r0 = lane >> 2;
-            const int mb = hh * 128 + 32 * q4;  // the warp's first neuron
-            const typename AF::C ccown = AF::centre(z0, beta);  // own lane's neuron m
-            float A4[4], S4[4];
-            if (l == 0) {
-              const float* W0 = net.W[0];
-              const float hs = om * h;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int mj = mb + r0 + 8 * j;
-                float av = 0.f;
-                if (mj < M) {
-                  const float w0 = W0[mj * 3 + 0], w1 = W0[mj * 3 + 1], w2 = W0[mj * 3 + 2];
-                  // the same rounding as the thread-per-neuron form: du, dv first, then combine
-                  const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
-                  const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
-                  av = hs * (pp == 0 ? du : (pp == 1 ? dv : (pp == 2 ? du + dv : du - dv)));
-                }
-                A4[j] = av;
-                S4[j] = 0.f;
-              }
-            } else {
-              float v0[4], v1[4];
-              {
-                static_assert(C::RANGES == 3 && C::NSPLIT == 1, "fragment form: 3 ranges, 1 split");
-                const uint32_t ta = tbase + ((uint32_t)(32 * q4) << 16) + hh * C::DH + cl * 8;
-                float r[24];
-                tc::tmem_ld16x256_x6(ta, ta + (16u << 16), C::NS, r);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  v0[j] = r[j] + (r[4 + j] + r[8 + j]);
-                  v1[j] = r[12 + j] + (r[16 + j] + r[20 + j]);
-                }
-              }
-              const float vv[4][2] = {{v0[0], v0[1]}, {v0[2], v0[3]}, {v1[0], v1[1]}, {v1[2], v1[3]}};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const bool ok = mb + r0 + 8 * j < M;
-                A4[j] = ok ? om * vv[j][0] : 0.f;
-                S4[j] = ok ? om * vv[j][1] : 0.f;
-              }
-            }
-            if (step && valid) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                float* zq = a.zf + (((size_t)c * nh + l) * a.zcols) * (size_t)MPAD + mb + r0 + 8 * j;
-                zq[(4 + 2 * pp) * MPAD] = A4[j];
-                zq[(5 + 2 * pp) * MPAD] = S4[j];
-              }
-            }
-            float Aa[4], Sa[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const typename AF::C cc = shfl_struct(ccown, r0 + 8 * j);
-              Aa[j] = Sa[j] = 0.f;
-              if (mb + r0 + 8 * j < M) AF::pair_fwd(cc, A4[j], S4[j], beta, &Aa[j], &Sa[j]);
-            }
-            if (last) {
-              float v = 0.f;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int mj = mb + r0 + 8 * j;
-                v = fmaf(mj < M ? net.W[L - 1][mj] : 0.f, Sa[j], v);
-              }
-              v += __shfl_xor_sync(0xffffffffu, v, 4);
-              v += __shfl_xor_sync(0xffffffffu, v, 8);
-              v += __shfl_xor_sync(0xffffffffu, v, 16);
-              if (lane < 4) red[(ew * C::MAXC + cl) * 4 + pp] = v;
-            } else {
-              uint32_t w[4][3];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) tc::split3x2(Aa[j], Sa[j], w[j]);
-              // this lane's row address: matrix (neuron block) lane/8, row (D column) lane%8
-              const int nrow = cl * 8 + (lane & 7);
-              const int kk = mb + 8 * (lane >> 3);
-              const uint32_t rowaddr = smem_u32(Bs) + (uint32_t)((kk >> 6) * C::BKC) +
-                                       tc::sw128_off(nrow, kk & 63, C::NS);
-#pragma unroll
-              for (int k = 0; k < 3; ++k)
-                tc::stmatrix_x4_trans(rowaddr + k * C::NS * 128, w[0][k], w[1][k], w[2][k], w[3][k]);
             }
           } else {
             const float* ci = cis + cl * NCINFO;

@@ -268,52 +268,8 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
   v[3] = __uint_as_float(r3);
 }
 
-// warp-collective 16-lane fragment load (tcgen05.ld 16x256b): the warp reads TMEM lanes
-// [lane field, +16) x 8 columns; thread t gets rows t/4 and t/4 + 8 of that window at
-// columns 2(t%4), 2(t%4)+1: v = {(r, c), (r, c+1), (r+8, c), (r+8, c+1)}
-__device__ __forceinline__ void tmem_ld16x256(uint32_t taddr, float (&v)[4]) {
-  uint32_t r0, r1, r2, r3;
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-      : "r"(taddr)
-      : "memory");
-  v[0] = __uint_as_float(r0);
-  v[1] = __uint_as_float(r1);
-  v[2] = __uint_as_float(r2);
-  v[3] = __uint_as_float(r3);
-}
 
-// six 16x256b fragment loads (lane windows w0, w1 x three accumulator ranges at column
-// offsets 0, d, 2d) under ONE wait::ld
-__device__ __forceinline__ void tmem_ld16x256_x6(uint32_t t0, uint32_t t1, uint32_t d, float (&v)[24]) {
-  uint32_t r[24];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%24];\n\t"
-      "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%4,%5,%6,%7}, [%25];\n\t"
-      "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%8,%9,%10,%11}, [%26];\n\t"
-      "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%12,%13,%14,%15}, [%27];\n\t"
-      "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%16,%17,%18,%19}, [%28];\n\t"
-      "tcgen05.ld.sync.aligned.16x256b.x1.b32 {%20,%21,%22,%23}, [%29];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23])
-      : "r"(t0), "r"(t0 + d), "r"(t0 + 2 * d), "r"(t1), "r"(t1 + d), "r"(t1 + 2 * d)
-      : "memory");
-#pragma unroll
-  for (int i = 0; i < 24; ++i) v[i] = __uint_as_float(r[i]);
-}
 
-// stmatrix m8n8.x4.trans: four 8x8 b16 matrices from mma-fragment registers (thread t holds
-// row t/4, columns 2(t%4), 2(t%4)+1 of matrix i in register i), each stored TRANSPOSED: memory
-// row k of matrix i (16 bytes at the address thread 8i+k supplies) receives column k
-__device__ __forceinline__ void stmatrix_x4_trans(uint32_t saddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
-  asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(r0),
-               "r"(r1), "r"(r2), "r"(r3)
-               : "memory");
-}
 
 __device__ __forceinline__ uint32_t tmem_lane_base(int warp) { return (uint32_t)(32 * (warp & 3)) << 16; }
 

@@ -301,20 +301,6 @@ __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8
 #pragma unroll
   for (int j = 0; j < 8; ++j) v[j] += r1[j] + r2[j];
 }
-// fragment load (tcgen05.ld 16x256b) of 8 columns starting at `col`, summed over the ranges
-template <class C>
-__device__ __forceinline__ void tc_ld_sum_frag(uint32_t taddr, int col, float (&v)[4]) {
-  const int sp = col / C::NS, nl = col % C::NS;
-  const uint32_t t0 = taddr + sp * C::RANGES * C::NS + nl;
-  tc::tmem_ld16x256(t0, v);
-  if (C::RANGES == 3) {
-    float r1[4], r2[4];
-    tc::tmem_ld16x256(t0 + C::NS, r1);
-    tc::tmem_ld16x256(t0 + 2 * C::NS, r2);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] += r1[j] + r2[j];
-  }
-}
 
 template <class C>
 __device__ __forceinline__ void tc_ld_sum2(uint32_t taddr, int col, float (&v)[2]) {
