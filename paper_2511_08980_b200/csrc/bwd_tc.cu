@@ -27,40 +27,31 @@ namespace fdsdf {
 #ifndef BWD_TC_PREFETCH
 #define BWD_TC_PREFETCH 1
 #endif
-#ifndef BWD_TC_WPK
-#define BWD_TC_WPK 3
-#endif
 #ifndef BWD_TC_NEPI
 #define BWD_TC_NEPI 16
 #endif
-// B / D column of (centre cl, adjoint column j): 8 j + cl (1) or 10 cl + j (0).  With 8 j + cl
-// the SW128 row group of column j is j itself, so each thread writes a centre's ten B columns
-// at one base offset plus compile-time offsets j * 1024 (no per-element swizzle arithmetic).
-#ifndef BWD_TC_COLPERM
-#define BWD_TC_COLPERM 1
-#endif
+// B / D column of (centre cl, adjoint column j) = 8 j + cl: the SW128 row group of column j is
+// j itself, so each thread writes a centre's ten B columns at one base offset plus compile-time
+// offsets j * 1024 (no per-element swizzle arithmetic)
 // 1: the top layer of tile t+1 (adjoint seeds -> delta_{L-2}; needs no MMA) is computed during
 // tile t's MMA phases and parked in the delta buffer, so a tile starts with a reload + split
 // instead of a full epilogue pass with the tensor cores idle.
 #ifndef BWD_TC_PIPE_TOP
 #define BWD_TC_PIPE_TOP 1
 #endif
-// 1 (two-range mode): phase A hands sigma'(z) and sigma''(z) (r . t) of each centre to phase B
+// 1: phase A hands sigma'(z) and sigma''(z) (r . t) of each centre to phase B
 // in a small per-thread array, instead of phase B reloading z, t and recomputing sincos(z)
 #ifndef BWD_TC_CARRY
 #define BWD_TC_CARRY 1
 #endif
-// accumulator ranges of the X GEMM: 2 (a0.[b0|b1], a1.[b0|b1], a0.b2, a2.b0: four A reads per
-// K step, stash of the 12 derivative factors) or 1 (six MMAs, stash of 20 values)
-#ifndef BWD_TC_RANGES
-#define BWD_TC_RANGES 2
-#endif
-constexpr int BWD_SV = BWD_TC_RANGES == 2 ? 12 : 20;  // stashed values per centre
+// The X GEMM accumulates in two TMEM ranges (a0.[b0|b1] + a1.[b0|b1], a0.b2 + a2.b0: four A
+// reads per K step), which leaves room for a stash of the 12 derivative factors per centre
+constexpr int BWD_SV = 12;  // stashed values per centre: P, Dd, Z of the 4 pairs
 // TMEM stash: (MH x EG thread groups) x (centres per thread) x BWD_SV values
 #define BWD_TC_STASH(MPAD) ((BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * ((MPAD) / 128)))) * BWD_SV)
 template <int MPAD>
-struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, BWD_TC_RANGES, BWD_TC_STASH(MPAD), 1, BWD_TC_WPK> {
-  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, BWD_TC_RANGES, BWD_TC_STASH(MPAD), 1, BWD_TC_WPK>;
+struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 2, BWD_TC_STASH(MPAD)> {
+  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 2, BWD_TC_STASH(MPAD)>;
   static constexpr int CT = 8;                                      // centres per tile
   static constexpr int OFF_SD = B::OFF_X;                           // float [2][CT][20]: seeds + x
   static constexpr int OFF_BAR = OFF_SD + 2 * CT * 20 * 4;
@@ -76,9 +67,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
   using AF = Act<ACT>;
   constexpr int N = C::N, MH = C::MH, CT = C::CT, EG = C::EG;
   constexpr int CPE = CT / EG;
-  static_assert(!BWD_TC_COLPERM || (CT == 8 && NCOLB == 10 && C::NSPLIT == 1 && C::RANGES <= 2),
-                "column permutation 8 j + cl assumes 8 centres x 10 columns, one or two accumulator ranges");
-  static_assert(C::RANGES == 1 || BWD_TC_COLPERM, "two ranges are read with the permuted column loads");
+  static_assert(CT == 8 && NCOLB == 10 && C::NSPLIT == 1 && C::RANGES == 2,
+                "column permutation 8 j + cl: 8 centres x 10 columns in two accumulator ranges");
   constexpr int SV = BWD_SV;
   FDSDF_ASSERT((int)C::TCOLS >= C::MH * C::DH + C::MH * EG * CPE * SV);
 
@@ -161,18 +151,13 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     // write delta (10 columns of centre slot cl, neuron m) as the next GEMM's B operand
     auto put_b10 = [&](int cl, const float (&dl)[NCOLB]) {
       FDSDF_ASSERT(cl >= 0 && cl < CT && m >= 0 && m < MPAD);
-      if (BWD_TC_COLPERM) {
-        // sw128_off(8 j + cl, m) = (m / 64) BKC + 1024 j + 128 cl + (((m % 64) / 8 ^ cl) << 4) + 2 (m % 8)
-        unsigned char* bp = Bs + (m >> 6) * C::BKC + cl * 128 + ((((m & 63) >> 3) ^ cl) << 4) + ((m & 7) << 1);
+      // sw128_off(8 j + cl, m) = (m / 64) BKC + 1024 j + 128 cl + (((m % 64) / 8 ^ cl) << 4) + 2 (m % 8)
+      unsigned char* bp = Bs + (m >> 6) * C::BKC + cl * 128 + ((((m & 63) >> 3) ^ cl) << 4) + ((m & 7) << 1);
 #pragma unroll
-        for (int j = 0; j < NCOLB; ++j) {
-          const tc::Bf3 sp3 = tc::split3(dl[j]);
+      for (int j = 0; j < NCOLB; ++j) {
+        const tc::Bf3 sp3 = tc::split3(dl[j]);
 #pragma unroll
-          for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(bp + j * 1024 + p * C::NS * 128) = sp3.p[p];
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NCOLB; ++j) tc_put_b<C>(Bs, cl * NCOLB + j, m, dl[j]);
+        for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(bp + j * 1024 + p * C::NS * 128) = sp3.p[p];
       }
     };
     // the top layer l = L-2 for centre i of tile tl (seeds sdsT): X = W_{L-1}^T fbar-seeds, so
@@ -279,7 +264,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         const bool mok = m < M;
         const float wl = (top && mok) ? net.W[L - 1][m] : 0.f;
         float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
-        constexpr bool CARRY = BWD_TC_CARRY && BWD_SV == 12;
+        constexpr bool CARRY = BWD_TC_CARRY;
         float c_s1[CPE], c_s2tr[CPE];  // CARRY: sigma'(z), sigma''(z) (r . t) per centre of this thread
         if (!top) prefetch_layer(tile, l - 1);  // the next pass's phase A
         // ---- phase A (X-independent, overlaps this layer's MMA): the pair maps of every
@@ -328,7 +313,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
               for (int p = 0; p < 4; ++p)
                 AF::pair_bwd(cc, q.A[p], q.S[p], beta, &t[5 * p], &t[5 * p + 1], &t[5 * p + 2], &t[5 * p + 3],
                              &t[5 * p + 4]);
-              if (SV == 12) {  // the layer's activations (wgrad operand) are X-independent: stored here
+              {  // the layer's activations (wgrad operand) are X-independent: stored here
                 const float* sd = sds + cl * 20;
                 const float tr = fmaf(sd[5], q.t0, fmaf(sd[6], q.t1, sd[7] * q.t2));
                 pv[0] = AF::value(cc, beta);
@@ -344,7 +329,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                 }
               }
             }
-            if (SV == 12) {
+            {
               if (valid && l <= L - 3) {
                 FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
                 float* ap = a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
@@ -370,14 +355,6 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                 }
                 tc::tmem_st4(tstash + i * SV + 4 * k, v4);
               }
-            } else {
-              float v16[16], v4[4];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v16[j] = t[j];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) v4[j] = t[16 + j];
-              tc::tmem_st16(tstash + i * SV, v16);
-              tc::tmem_st4(tstash + i * SV + 16, v4);
             }
           }
           tc::tmem_wait_st();
@@ -431,21 +408,11 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             const float dL[NCOLB] = {sd[0], valid ? 1.f : 0.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
 #pragma unroll
             for (int j = 0; j < NCOLB; ++j) X[j] = wl * dL[j];
-          } else if constexpr (C::RANGES == 2) {
+          } else {  // the two accumulator ranges, columns cl + 8 j
             tc::tmem_ld10x2_stride8(taddr + cl, taddr + C::NS + cl, X);
-          } else if constexpr (BWD_TC_COLPERM) {
-            tc::tmem_ld10_stride8(taddr + cl, X);
-          } else {
-            float v8[8], v2[2];
-            tc_ld_sum8<C>(taddr, cl * NCOLB, v8);
-            tc_ld_sum2<C>(taddr, cl * NCOLB + 8, v2);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) X[j] = v8[j];
-            X[8] = v2[0];
-            X[9] = v2[1];
           }
-          float t[20];  // per pair: A_a, S_a, P, Dd, Z (SV == 12: only P, Dd, Z are stashed)
-          if (SV == 12) {
+          float t[20];  // per pair: A_a, S_a, P, Dd, Z (only P, Dd, Z are stashed / used here)
+          {
             float v4[4];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
@@ -458,20 +425,12 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             }
 #pragma unroll
             for (int p = 0; p < 4; ++p) t[5 * p] = t[5 * p + 1] = 0.f;
-          } else {
-            float v16[16], v4[4];
-            tc::tmem_ld16(tstash + i * SV, v16);
-            tc::tmem_ld4(tstash + i * SV + 16, v4);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) t[j] = v16[j];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) t[16 + j] = v4[j];
           }
           const float r0 = sd[5], r1 = sd[6], r2 = sd[7];
           const float u0 = sd[8], u1 = sd[9], u2 = sd[10], v0 = sd[11], v1 = sd[12], v2_ = sd[13];
-          float dl[NCOLB], pv[NCOLB];
+          float dl[NCOLB];
 #pragma unroll
-          for (int j = 0; j < NCOLB; ++j) dl[j] = pv[j] = 0.f;
+          for (int j = 0; j < NCOLB; ++j) dl[j] = 0.f;
           float w0p[3] = {0.f, 0.f, 0.f};
           if (mok && valid) {
             float tr = 0.f, s1, s2tr;
@@ -488,15 +447,13 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             float zbar = 0.f;
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
-              const float Aa = t[5 * p], Sa = t[5 * p + 1], P = t[5 * p + 2], Dd = t[5 * p + 3], Z = t[5 * p + 4];
+              const float P = t[5 * p + 2], Dd = t[5 * p + 3], Z = t[5 * p + 4];
               const float XA = X[2 + 2 * p], XS = X[3 + 2 * p];
               const float dA = om * fmaf(XA, P, 2.0f * XS * Dd);
               const float dS = om * fmaf(0.5f * XA, Dd, XS * P);
               zbar = fmaf(XA, Dd, fmaf(XS, Z, zbar));
               dl[2 + 2 * p] = dA;
               dl[3 + 2 * p] = dS;
-              pv[2 + 2 * p] = Aa;
-              pv[3 + 2 * p] = Sa;
               if (l == 0) {  // a^{-1} of pair columns: A -> h d_p, S -> 0
                 const float dpx = p == 0 ? u0 : (p == 1 ? v0 : (p == 2 ? u0 + v0 : u0 - v0));
                 const float dpy = p == 0 ? u1 : (p == 1 ? v1 : (p == 2 ? u1 + v1 : u1 - v1));
@@ -510,10 +467,6 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             const float zb = fmaf(Xc, s1, fmaf(s2tr, Xt, zbar));
             dl[0] = om * zb;
             dl[1] = om * s1 * Xt;
-            if (SV == 20) {
-              pv[0] = AF::value(cc, beta);
-              pv[1] = s1 * tr;
-            }
             if (l == 0) {  // a^{-1}: centre -> x0, tangent -> r
               w0p[0] = fmaf(dl[0], sd[16], fmaf(dl[1], r0, w0p[0]));
               w0p[1] = fmaf(dl[0], sd[17], fmaf(dl[1], r1, w0p[1]));
@@ -527,21 +480,9 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
 #pragma unroll
               for (int j = 0; j < NCOLB; ++j) dp[j * MPAD] = dl[j];
             }
-            if (SV == 20 && l <= L - 3) {
-              float* ap = a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
-#pragma unroll
-              for (int j = 0; j < NCOLB; ++j) ap[j * MPAD] = pv[j];
-            }
           }
           if (l >= 1) put_b10(cl, dl);
           s_db += dl[0];
-          if (SV == 20 && top) {
-            const float dL[NCOLB] = {sd[0], valid ? 1.f : 0.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
-            float v = 0.f;
-#pragma unroll
-            for (int j = 0; j < NCOLB; ++j) v = fmaf(dL[j], pv[j], v);
-            s_vL += v;
-          }
           if (l == 0) {
             s_w0[0] += w0p[0];
             s_w0[1] += w0p[1];

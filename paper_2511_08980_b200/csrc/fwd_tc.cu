@@ -41,9 +41,6 @@ namespace fdsdf {
 #ifndef FWD_TC_N
 #define FWD_TC_N 64
 #endif
-#ifndef FWD_TC_PAIR_WPK
-#define FWD_TC_PAIR_WPK 3
-#endif
 // 1: layer 0 of tile t+1 (fan-in 3, no MMA) is computed in tile t's MMA phases and parked in
 // spare TMEM columns, so a tile starts with a split of the parked outputs into the B operand
 // instead of a full epilogue pass with the tensor cores idle
@@ -51,15 +48,11 @@ namespace fdsdf {
 #define FWD_TC_PIPE0 1
 #endif
 constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && FWD_TC_NSPLIT == 1;
-// mode 1 (centre + tangents: they set g, the frames and the |g|^p denominators) streams all
-// three weight pieces; mode 2 (the stencil-pair differences) streams FWD_TC_PAIR_WPK
 template <int MPAD, int MODE>
-struct FtcCfg : TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT,
-                      MODE == 1 ? 3 : FWD_TC_PAIR_WPK> {
+struct FtcCfg : TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT> {
   // TMEM stash (FWD_PIPE0): the next tile's layer-0 outputs, (MH x EG thread groups) x CPE x
   // columns per centre = MH x N columns
-  using B = TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT,
-                  MODE == 1 ? 3 : FWD_TC_PAIR_WPK>;
+  using B = TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1

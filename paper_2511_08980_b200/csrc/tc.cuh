@@ -177,29 +177,6 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, float (&v)[2]) {
   v[1] = __uint_as_float(r1);
 }
 
-// columns taddr + 8 j, j = 0..9 (one 32-bit column each, a single wait)
-__device__ __forceinline__ void tmem_ld10_stride8(uint32_t taddr, float (&v)[10]) {
-  uint32_t r[10];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%10];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%1}, [%11];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%2}, [%12];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%3}, [%13];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%4}, [%14];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%5}, [%15];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%6}, [%16];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%7}, [%17];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%8}, [%18];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%9}, [%19];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9])
-      : "r"(taddr), "r"(taddr + 8), "r"(taddr + 16), "r"(taddr + 24), "r"(taddr + 32), "r"(taddr + 40),
-        "r"(taddr + 48), "r"(taddr + 56), "r"(taddr + 64), "r"(taddr + 72)
-      : "memory");
-#pragma unroll
-  for (int j = 0; j < 10; ++j) v[j] = __uint_as_float(r[j]);
-}
 
 // columns ta + 8 j and tb + 8 j, j = 0..9, summed pairwise (two accumulator ranges), one wait
 __device__ __forceinline__ void tmem_ld10x2_stride8(uint32_t ta, uint32_t tb, float (&v)[10]) {
@@ -235,19 +212,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// warp-collective TMEM stores (thread t -> lane 32*(w%4)+t, consecutive columns); a
-// tmem_wait_st() must separate them from later tcgen05.ld of the same columns
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
-      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
-      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
-      : "memory");
-}
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const float (&v)[4]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__float_as_uint(v[0])),
                "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3]))
@@ -274,7 +238,7 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
 __device__ __forceinline__ uint32_t tmem_lane_base(int warp) { return (uint32_t)(32 * (warp & 3)) << 16; }
 
 // the packed weight images hold WP = 3 exact bf16 pieces per weight (48 KB per (K chunk,
-// M-half) stage); a kernel may stream only the first WPK of them (see TcCfg::WPK)
+// M-half) stage)
 constexpr int WP = 3;
 // the six piece products (i, j), i + j <= 2, smallest first
 __host__ __device__ constexpr int prod_a(int q) { return q == 0 ? 2 : (q == 1 || q == 3) ? 1 : 0; }

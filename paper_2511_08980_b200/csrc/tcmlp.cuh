@@ -20,20 +20,16 @@
 
 namespace fdsdf {
 
-template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1, int WPK_ = 3>
+template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
   static constexpr int MH = MPAD / 128;         // tcgen05 M-halves (M = 128 each)
   static constexpr int KC = MPAD / 64;          // K chunks (one 128-byte swizzle row each)
-  // weight pieces streamed: 3 = the fp32-accurate bf16x6 products; 2 = W' = w0 + w1
-  // (|W' - W| <= 2^-18 |W|) with all three activation pieces: products a0 b0, a0 b1, a0 b2,
-  // a1 b0, a1 b1 ("bf16x5"), for kernels whose gates tolerate that fixed perturbation of
-  // the hidden weights (the stencil-pair columns and the backward)
-  static constexpr int WPK = WPK_;
+  // weight stage (kc, h): the three bf16 pieces of 128 rows x 64 K (48 KB), 2-deep ring
   static constexpr int IMGSTAGE = tc::WP * 128 * 128;  // stage stride in the packed image
-  static constexpr int STAGE = WPK * 128 * 128;        // weight stage (kc, h) in shared memory
-  static constexpr int NST = WPK == 3 ? 2 : 3;         // weight ring depth (96 KB either way)
+  static constexpr int STAGE = IMGSTAGE;               // weight stage in shared memory
+  static constexpr int NST = 2;
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
   static constexpr int BKC = 3 * N * 128;       // one K chunk of B
   // column splits: the tile's N columns are NSPLIT independent MMA passes of NS columns each,
@@ -55,7 +51,7 @@ struct TcCfg {
   static constexpr int STASH = STASH_;
   static constexpr int TUSE = MH * DH + STASH;
   static constexpr uint32_t TCOLS = TUSE <= 32 ? 32 : TUSE <= 64 ? 64 : TUSE <= 128 ? 128 : TUSE <= 256 ? 256 : 512;
-  static_assert(RANGES >= 1 && RANGES <= 3, "one accumulator range (6 MMAs), two (4 MMAs) or three (3 MMAs)");
+  static_assert(RANGES == 2 || RANGES == 3, "two accumulator ranges (4 MMAs per K step) or three (3 MMAs)");
   static_assert(NS % 16 == 0 && NS >= 16 && RANGES * NS <= 256, "tcgen05 M=128 needs N % 16 == 0, <= 256");
   static_assert(NSPLIT == 1 || NSPLIT == 2, "one or two column splits");
   static_assert(TUSE <= 512, "TMEM has 512 columns");
@@ -184,9 +180,9 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
               const uint64_t bd = tc::sdesc_sw128(ba + sub * 32);
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
-              if (C::WPK == 3) tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
             }
-          } else if (C::RANGES == 2) {
+          } else {
             // a0 . [b0|b1] and a1 . [b0|b1] (N = 2N: ranges 0, 1), then a0 . b2 and a2 . b0
             // (N = N: range 0) -- the six products, four A reads per K step instead of six
 #pragma unroll
@@ -198,14 +194,6 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b2, id1, 1u);
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), b01, id1, 1u);
             }
-          } else {  // the six piece products into one range
-#pragma unroll
-            for (int sub = 0; sub < 4; ++sub)
-#pragma unroll
-              for (int q = 3 - C::WPK; q < 6; ++q)  // WPK = 2: skip (a2, b0)
-                tc::mma_bf16_w(d, tc::sdesc_sw128(wa + tc::prod_a(q) * 16384 + sub * 32),
-                             tc::sdesc_sw128(ba + tc::prod_b(q) * C::NS * 128 + sub * 32), id1,
-                             (kc == 0 && sub == 0 && q == 3 - C::WPK) ? 0u : 1u);
           }
           tc::mma_commit_w(&b.wempty[s]);
         }
@@ -287,11 +275,7 @@ __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float 
 template <class C>
 __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8]) {
   FDSDF_ASSERT(col >= 0 && col + 8 <= C::NSPLIT * C::NS);
-  static_assert(C::RANGES != 2, "two-range accumulators: sum the ranges at the call site");
-  if (C::RANGES == 1) {
-    tc::tmem_ld8(taddr + col, v);
-    return;
-  }
+  static_assert(C::RANGES == 3, "three accumulator ranges (two-range users sum at the call site)");
   float r1[8], r2[8];
   const int sp = col / C::NS, nl = col % C::NS;  // 8 columns never straddle a split
   const uint32_t t0 = taddr + sp * 3 * C::NS + nl;
@@ -305,11 +289,7 @@ __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8
 template <class C>
 __device__ __forceinline__ void tc_ld_sum2(uint32_t taddr, int col, float (&v)[2]) {
   FDSDF_ASSERT(col >= 0 && col + 2 <= C::NSPLIT * C::NS);
-  static_assert(C::RANGES != 2, "two-range accumulators: sum the ranges at the call site");
-  if (C::RANGES == 1) {
-    tc::tmem_ld2(taddr + col, v);
-    return;
-  }
+  static_assert(C::RANGES == 3, "three accumulator ranges (two-range users sum at the call site)");
   float r1[2], r2[2];
   const int sp = col / C::NS, nl = col % C::NS;
   const uint32_t t0 = taddr + sp * 3 * C::NS + nl;
