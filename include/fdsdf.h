@@ -152,7 +152,8 @@ enum {
                                 /* (forward, backward, weight gradient) with the fp32-accurate */
                                 /* bf16x6 piece scheme; needs hidden widths   */
                                 /* <= 256 and no skip layer, else FDSDF_E_UNSUPPORTED.        */
-                                /* Neither flag: the tensor path where supported, else FFMA.  */
+                                /* Neither flag: the tensor path where supported, else the    */
+                                /* hybrid path (128/256/512-padded widths), else FFMA.       */
                                 /* Both flags -> FDSDF_E_INVALID.                             */
 };
 /* Environment read at create time: FDSDF_MAX_SM=k (k >= 2) caps the persistent grids at k
@@ -250,8 +251,11 @@ const char* fdsdf_status_string(fdsdf_status s);
 const char* fdsdf_last_error(const fdsdf_ctx* ctx);
 /* Returns and clears the sticky device flags (synchronises the context's device). */
 fdsdf_status fdsdf_get_device_flags(fdsdf_ctx* ctx, uint32_t* out);
-/* Which contraction path the context runs: FDSDF_PATH_FFMA or FDSDF_PATH_TENSOR (-1: NULL). */
-enum { FDSDF_PATH_FFMA = 0, FDSDF_PATH_TENSOR = 1 };
+/* Which contraction path the context runs (-1: NULL): FDSDF_PATH_FFMA; FDSDF_PATH_TENSOR (every
+ * contraction on the tensor cores); FDSDF_PATH_HYBRID (networks with 512-wide layers or the
+ * skip layer, default flags: the forward -- centre and stencil passes -- and the weight
+ * gradient on the tensor cores, the backward on the FFMA kernel). */
+enum { FDSDF_PATH_FFMA = 0, FDSDF_PATH_TENSOR = 1, FDSDF_PATH_HYBRID = 2 };
 int32_t fdsdf_path(const fdsdf_ctx* ctx);
 /* Number of kernel launches enqueued by the last eval/step call on this context. */
 int32_t fdsdf_last_launch_count(const fdsdf_ctx* ctx);

@@ -89,6 +89,9 @@ struct fdsdf_ctx {
   // tensor-core (tcgen05 bf16x6) forward
   bool tc = false;
   bool pair = false;              // CTA-pair (cta_group::2) forward kernels
+  bool tcf = false;               // tensor-core forward (fwd_tc.cu): the tensor path, or the
+                                  // hybrid path of 512-wide / skip-layer networks
+  bool tcw = false;               // tensor-core weight gradient (wgrad_tc.cu): ditto
   unsigned char* fimg = nullptr;  // packed forward weight image
   unsigned char* bimg = nullptr;  // packed backward (W^T) weight image
   float* cinfo = nullptr;    // [max_centers][16]
@@ -154,7 +157,9 @@ const char* fdsdf_version(void) {
   return "fdsdf 0.2 (sm_100a, pair-symmetric difference form; fp32 FFMA and tcgen05 bf16x6 paths)";
 }
 
-int32_t fdsdf_path(const fdsdf_ctx* c) { return c ? (c->tc ? FDSDF_PATH_TENSOR : FDSDF_PATH_FFMA) : -1; }
+int32_t fdsdf_path(const fdsdf_ctx* c) {
+  return c ? (c->tc ? FDSDF_PATH_TENSOR : (c->tcf ? FDSDF_PATH_HYBRID : FDSDF_PATH_FFMA)) : -1;
+}
 
 const char* fdsdf_status_string(fdsdf_status s) {
   switch (s) {
@@ -272,6 +277,12 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
       const char* ev = getenv("FDSDF_PAIR");
       c->pair = mp_tc == 256 && c->L >= 3 && ev && ev[0] == '1';
     }
+    // networks the full tensor path does not cover (512-wide layers, the skip layer) still run
+    // their forward and weight gradient on the tensor cores when the padded width is a tcgen05
+    // tile (128/256/512); only the backward stays on the FFMA kernel (same zf / seed / del /
+    // actv layouts)
+    c->tcf = c->tc || (!(flags & FDSDF_CREATE_FFMA) && c->mpad >= 128 && tc_fwd_supported(c->mpad));
+    c->tcw = c->tcf && wgrad_tc_supported(c->mpad);
   }
   c->P = fdsdf_spec_num_params(spec);
   for (int l = 0; l < c->L; ++l) {
@@ -332,14 +343,14 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     ok = ok && alloc((void**)&c->actv, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
     const size_t bslots = c->tc ? (size_t)c->nsm * bwd_tc_acc_slots(mp) : (size_t)c->bgrid;
     ok = ok && alloc((void**)&c->bacc, std::max<size_t>(bslots, c->bgrid) * c->nacc * sizeof(float));
-    const int nsplit_max = c->tc ? std::max(c->nsplit, c->nsm) : c->nsplit;
+    const int nsplit_max = c->tcw ? std::max(c->nsplit, c->nsm) : c->nsplit;
     ok = ok && alloc((void**)&c->part, (size_t)std::max(0, c->ngemm) * nsplit_max * mp * mp * sizeof(float));
   }
-  if (ok && c->tc) {
+  if (ok && c->tcf) {
     ok = ok && alloc((void**)&c->fimg, tc_wimg_bytes(mp, c->ngemm));
     ok = ok && alloc((void**)&c->cinfo, (size_t)max_centers * 16 * sizeof(float));
     if (c->eval_only) ok = ok && alloc((void**)&c->zev, (size_t)max_centers * c->nh * mp * sizeof(float));
-    if (!c->eval_only) ok = ok && alloc((void**)&c->bimg, tc_wimg_bytes(mp, c->ngemm));
+    if (c->tc && !c->eval_only) ok = ok && alloc((void**)&c->bimg, tc_wimg_bytes(mp, c->ngemm));
   }
   if (ok) ok = cudaMemset(c->dflags, 0, sizeof(unsigned)) == cudaSuccess;
   cudaSetDevice(prev);
@@ -429,12 +440,12 @@ static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t str
     c->last_fgrid = g2;
     return run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd_tc2(a, 2, g2, strm); });
   }
-  a.ntiles = (n + fwd_tc_tile_centres(1) - 1) / fwd_tc_tile_centres(1);
+  a.ntiles = (n + fwd_tc_tile_centres(1, c->mpad) - 1) / fwd_tc_tile_centres(1, c->mpad);
   const int g1 = (int)std::min<int64_t>(c->nsm, a.ntiles);
   cudaError_t e = pairs_only ? cudaSuccess
                              : run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc(a, 1, g1, strm); });
   if (e != cudaSuccess) return e;
-  a.ntiles = (n + fwd_tc_tile_centres(2) - 1) / fwd_tc_tile_centres(2);
+  a.ntiles = (n + fwd_tc_tile_centres(2, c->mpad) - 1) / fwd_tc_tile_centres(2, c->mpad);
   const int g2 = (int)std::min<int64_t>(c->nsm, a.ntiles);
   c->last_fgrid = g2;
   return run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd_tc(a, 2, g2, strm); });
@@ -459,14 +470,14 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
 static fdsdf_status eval_run(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n,
                              const fdsdf_stencil* st, const fdsdf_eval_out* out, cudaStream_t strm,
                              bool pairs_only) {
-  pairs_only = pairs_only && c->tc;  // the FFMA forward is one fused kernel
+  pairs_only = pairs_only && c->tcf;  // the FFMA forward is one fused kernel
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != c->device) cudaSetDevice(c->device);
   fill_net(c, d_params);
   c->launches = 0;
   cudaError_t e = cudaSuccess;
-  if (c->tc) {
+  if (c->tcf) {
     if (c->ngemm > 0 && !pairs_only)
       e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, nullptr, strm); });
   } else if (c->ngemm > 0) {
@@ -490,7 +501,7 @@ static fdsdf_status eval_run(fdsdf_ctx* c, const float* d_params, const float* d
     a.out_frames = out->d_frames;
     a.out_mask = out->d_mask;
   }
-  if (c->tc) {
+  if (c->tcf) {
     a.zf = c->eval_only ? c->zev : c->zf;
     a.zcols = c->eval_only ? 1 : NCOLF;
     e = launch_fwd_tc_pair(c, a, strm, pairs_only);
@@ -530,7 +541,7 @@ fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* c, const float* d_params, const float
   for (int pass = 0; pass < 3; ++pass) {
     // tensor path, passes 1 and 2: f, grad f and the centre pre-activations are those of pass 0;
     // only the frame changes -> rewrite the frame fields of the centre info, run the pair kernel
-    const bool pairs_only = c->tc && pass > 0;
+    const bool pairs_only = c->tcf && pass > 0;
     cudaError_t e = run_slot(c, FDSDF_KSLOT_HESS, strm, [&] {
       return pairs_only ? launch_cinfo_axis_frames(c->cinfo, n, AX[pass][0], AX[pass][1], strm)
                         : launch_axis_frames(c->hframes, n, AX[pass][0], AX[pass][1], strm);
@@ -597,12 +608,10 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   fill_net(c, d_params);
   c->launches = 0;
   cudaError_t e = cudaSuccess;
-  if (c->tc) {
-    if (c->ngemm > 0)
-      e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, c->bimg, strm); });
-  } else if (c->ngemm > 0) {
+  if (c->tcf && c->ngemm > 0)  // tensor forward image (and, on the tensor path, the backward's)
+    e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, c->bimg, strm); });
+  if (e == cudaSuccess && !c->tc && c->ngemm > 0)  // FFMA backward / weight gradient
     e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
-  }
   if (e != cudaSuccess) return done(cuda_fail(c, e, "pack_tc"));
 
   FwdArgs a{};
@@ -621,7 +630,7 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   a.zf = c->zf;
   a.seed = c->seed;
   int fgrid = (int)std::min<int64_t>(c->fgrid, a.ntiles);
-  if (c->tc) {
+  if (c->tcf) {
     a.zcols = NCOLF;
     e = launch_fwd_tc_pair(c, a, strm);
     fgrid = c->last_fgrid;
@@ -663,11 +672,11 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   w.rows = n * NCOLB;
   w.stride_layer = n * NCOLB * c->mpad;
   w.mpad = c->mpad;
-  w.nsplit = c->tc ? wgrad_tc_splits(c->nsm, w.rows) : c->nsplit;
+  w.nsplit = c->tcw ? wgrad_tc_splits(c->nsm, w.rows, c->mpad) : c->nsplit;
   w.first_layer = 1;
   if (c->ngemm > 0)
     e = run_slot(c, FDSDF_KSLOT_WGRAD, strm, [&] {
-      return c->tc ? launch_wgrad_tc(w, c->ngemm, strm) : launch_wgrad(w, c->ngemm, strm);
+      return c->tcw ? launch_wgrad_tc(w, c->ngemm, strm) : launch_wgrad(w, c->ngemm, strm);
     });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "wgrad_kernel"));
 

@@ -48,11 +48,16 @@ namespace fdsdf {
 #define FWD_TC_PIPE0 1
 #endif
 constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && FWD_TC_NSPLIT == 1;
+// tile width: FWD_TC_N columns up to 256-wide layers; 32 for 512-wide ones (C3), where a wider
+// B operand (32 x 512 x 3 pieces = 96 KB) would not fit next to the weight ring
+constexpr int fwd_tc_n(int mpad) { return mpad == 512 ? 32 : FWD_TC_N; }
 template <int MPAD, int MODE>
-struct FtcCfg : TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT> {
+struct FtcCfg : TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
+                      FWD_TC_NSPLIT> {
   // TMEM stash (FWD_PIPE0): the next tile's layer-0 outputs, (MH x EG thread groups) x CPE x
   // columns per centre = MH x N columns
-  using B = TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MPAD / 128) : 0, FWD_TC_NSPLIT>;
+  using B = TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
+                  FWD_TC_NSPLIT>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
@@ -67,9 +72,13 @@ struct FtcCfg : TcCfg<MPAD, FWD_TC_N, FWD_TC_NEPI, 3, FWD_PIPE0 ? FWD_TC_N * (MP
 
 bool tc_supported(int mpad, int skip) { return (mpad == 128 || mpad == 256) && skip < 0; }
 
+// the tensor-core forward alone (centre + pair kernels) also covers 512-wide layers and the skip
+// layer; such networks run their backward / weight gradient on the FFMA kernels
+bool tc_fwd_supported(int mpad) { return mpad == 128 || mpad == 256 || mpad == 512; }
+
 size_t tc_wimg_bytes(int mpad, int ngemm) { return (size_t)(ngemm > 0 ? ngemm : 0) * mpad * mpad * 2 * tc::WP; }
 
-int fwd_tc_tile_centres(int mode) { return mode == 1 ? FWD_TC_N / 4 : FWD_TC_N / 8; }
+int fwd_tc_tile_centres(int mode, int mpad) { return mode == 1 ? fwd_tc_n(mpad) / 4 : fwd_tc_n(mpad) / 8; }
 
 // ----------------------------------------------------------------------------- weight images
 // image[g][kc][h][piece < WP][sw128 128 rows x 64 k]: forward A operand = W_l (rows = output
@@ -80,7 +89,7 @@ __global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char
   const int g = blockIdx.y;
   const int l = g + 1;
   const int M = net.width[l + 1];
-  const int K = net.width[l];
+  const int K = net.width[l] + (l == net.skip ? 3 : 0);  // fan-in: cat(a, x) at the skip layer
   const float* W = net.W[l];
   const size_t per_layer = (size_t)mp * mp * 2 * tc::WP;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < mp * mp; idx += gridDim.x * blockDim.x) {
@@ -167,6 +176,40 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
       return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
     };
     auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
+    // cat(a, x) / sqrt(2) at the input of the skip layer net.skip (IGR convention, SURVEY §8c
+    // item 14): when layer l's outputs feed it, every output is scaled by 1/sqrt(2) and the
+    // threads of rows M .. M+2 (no neuron of layer l) supply the x part (as fwd.cu does)
+    constexpr float RSQ2 = 0.70710678118654752f;
+    auto skip_centre = [&](int l, int64_t c, bool valid, float& o0, float& o1, float& o2, float& o3) {
+      if (l + 1 != net.skip) return;
+      const int M = net.width[l + 1];
+      if (m >= M && m < M + 3) {  // value x_d, tangents e_d
+        const int d = m - M;
+        o0 = valid ? a.x[c * 3 + d] : 0.f;
+        o1 = d == 0 ? 1.f : 0.f;
+        o2 = d == 1 ? 1.f : 0.f;
+        o3 = d == 2 ? 1.f : 0.f;
+      }
+      o0 *= RSQ2;
+      o1 *= RSQ2;
+      o2 *= RSQ2;
+      o3 *= RSQ2;
+    };
+    auto skip_pairs = [&](int l, const float* ci, float (&o)[8]) {
+      if (l + 1 != net.skip) return;
+      const int M = net.width[l + 1];
+      if (m >= M && m < M + 3) {  // odd part of x0 +- h d_p = h d_p, even part 0
+        const int d = m - M;
+        const float ud = ci[4 + d], vd = ci[7 + d];
+        o[0] = h * ud;
+        o[2] = h * vd;
+        o[4] = h * (ud + vd);
+        o[6] = h * (ud - vd);
+        o[1] = o[3] = o[5] = o[7] = 0.f;
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) o[p] *= RSQ2;
+    };
     // this thread's stash columns: CPE centres x CPC values (FWD_PIPE0)
     const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + MH * C::DH + (hh * C::EG + eg) * CPE * CPC;
     const bool pipe0 = FWD_PIPE0 && ngemm > 0;
@@ -215,6 +258,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           o[2] = s1 * t1;
           o[3] = s1 * t2;
         }
+        skip_centre(0, c, valid, o[0], o[1], o[2], o[3]);
         tc::tmem_st4(tstash + i * CPC, o);
       } else {
         const float* ci = cis_t + cl * NCINFO;
@@ -247,6 +291,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
 #pragma unroll
           for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &o[2 * p], &o[2 * p + 1]);
         }
+        skip_pairs(0, ci, o);
         float o4[4] = {o[0], o[1], o[2], o[3]};
         tc::tmem_st4(tstash + i * CPC, o4);
         o4[0] = o[4];
@@ -453,6 +498,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               o2 = s1 * t1;
               o3 = s1 * t2;
             }
+            skip_centre(l, c, valid, o0, o1, o2, o3);
             if (last) {
               reduce4(cl, o0, o1, o2, o3);
             } else {
@@ -503,6 +549,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
 #pragma unroll
               for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &o[2 * p], &o[2 * p + 1]);
             }
+            skip_pairs(l, ci, o);
             if (last) {
               reduce4(cl, o[1], o[3], o[5], o[7]);
             } else {
@@ -567,6 +614,10 @@ cudaError_t launch_fwd_tc(const FwdArgs& a, int mode, int grid, cudaStream_t st)
   FDSDF_CASE(ACT_SOFTPLUS, 128, 2)
   FDSDF_CASE(ACT_SOFTPLUS, 256, 1)
   FDSDF_CASE(ACT_SOFTPLUS, 256, 2)
+  FDSDF_CASE(ACT_SINE, 512, 1)
+  FDSDF_CASE(ACT_SINE, 512, 2)
+  FDSDF_CASE(ACT_SOFTPLUS, 512, 1)
+  FDSDF_CASE(ACT_SOFTPLUS, 512, 2)
 #undef FDSDF_CASE
   return cudaErrorInvalidValue;
 }

@@ -128,7 +128,8 @@ bool tc_supported(int mpad, int skip);
 size_t tc_wimg_bytes(int mpad, int ngemm);          // one packed weight image (fwd or bwd)
 cudaError_t launch_pack_tc(const Net& net, unsigned char* fwd_img, unsigned char* bwd_img, cudaStream_t st);
 cudaError_t launch_fwd_tc(const FwdArgs& a, int mode, int grid, cudaStream_t st);
-int fwd_tc_tile_centres(int mode);                  // 16 (mode 1) / 8 (mode 2)
+int fwd_tc_tile_centres(int mode, int mpad);        // mode 1: N/4, mode 2: N/8 centres
+bool tc_fwd_supported(int mpad);                    // tensor forward (fwd_tc.cu) for this width
 // CTA-pair variants (fwd_tc2.cu): mpad 256, L >= 3; grid = 2 x clusters
 cudaError_t launch_fwd_tc2(const FwdArgs& a, int mode, int grid, cudaStream_t st);
 int fwd_tc2_tile_centres(int mode);                 // 32 (mode 1) / 16 (mode 2) per pair tile
@@ -136,7 +137,8 @@ cudaError_t launch_bwd_tc(const BwdArgs& a, int grid, cudaStream_t st);
 int bwd_tc_tile_centres();                          // 8
 int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
 cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, cudaStream_t st);
-int wgrad_tc_splits(int nsm, int64_t rows);         // split-K factor of the tensor wgrad
+int wgrad_tc_splits(int nsm, int64_t rows, int mpad);  // split-K factor of the tensor wgrad
+bool wgrad_tc_supported(int mpad);                      // MPAD 128 / 256 / 512
 // training iteration (train.cu)
 int feistel_half_bits(int64_t n_pool);
 cudaError_t launch_sample(const float* pool, int64_t n_pool, int64_t n_pick, float half, int64_t n_uniform,

@@ -3,10 +3,12 @@
 //
 //   dW_l[m][k] = sum_j delta_l[j][m] * a_{l-1}[j][k]     j over (centre, column): 10 per centre
 //
-// Split-K: CTA (s, l) owns a contiguous j-range of GEMM layer l and computes the full
-// MPAD x MPAD block into TMEM (M = MPAD rows in 128-row halves, N = MPAD), then writes its partial
-// (never atomically added); finalize_kernel sums the partials in split order, so the result
-// is bitwise reproducible.
+// Split-K: CTA (s, b, l) owns a contiguous j-range of GEMM layer l and computes output block b
+// (BW x BW, BW = min(MPAD, 256): the whole layer for MPAD <= 256, one of four 256 x 256 blocks
+// for MPAD = 512) into TMEM (M = BW rows in 128-row halves, N = BW), then writes its part of the
+// split's partial (never atomically added); finalize_kernel sums the partials in split order, so
+// the result is bitwise reproducible. The blocks of one split are adjacent in the grid, so they
+// run together and read the same delta / a rows through L2.
 //   warp 0      TMEM owner + MMA issuer (one thread): per 32-wide j chunk, 2 K-steps x
 //               M-halves x 6 piece products, tcgen05.mma kind::f16 with BOTH operands
 //               MN-major (delta and a are stored j-major, m / k contiguous);
@@ -21,29 +23,35 @@ namespace fdsdf {
 
 template <int MPAD>
 struct WtcCfg {
+  static constexpr int BW = MPAD > 256 ? 256 : MPAD;  // output block edge
+  static constexpr int NB = MPAD / BW;              // blocks per edge
   static constexpr int JC = 32;                     // j per stage (4 swizzle atoms along K)
-  static constexpr int MH = MPAD / 128;
-  static constexpr int PIECE = MPAD * JC * 2;       // one bf16 piece of one operand chunk
+  static constexpr int MH = BW / 128;
+  static constexpr int PIECE = BW * JC * 2;         // one bf16 piece of one operand chunk
   static constexpr int OPER = 3 * PIECE;            // one operand chunk (3 pieces)
   static constexpr int STAGE = 2 * OPER;            // delta chunk + a chunk
   static constexpr int NST = 2;
-  static constexpr int KSTRIDE = (MPAD / 64) * 1024;  // byte stride between swizzle atoms along K
+  static constexpr int KSTRIDE = (BW / 64) * 1024;  // byte stride between swizzle atoms along K
   static constexpr int NSTG = 16;                   // stager warps
   static constexpr int NTHR = (1 + NSTG) * 32;
   static constexpr int OFF_BAR = NST * STAGE;
   static constexpr int BYTES = OFF_BAR + 64 + 1024;
-  static constexpr uint32_t TCOLS = MH * MPAD <= 128 ? 128 : (MH * MPAD <= 256 ? 256 : 512);
+  static constexpr uint32_t TCOLS = MH * BW <= 128 ? 128 : (MH * BW <= 256 ? 256 : 512);
 };
 
-int wgrad_tc_splits(int nsm, int64_t rows) {
+bool wgrad_tc_supported(int mpad) { return mpad == 128 || mpad == 256 || mpad == 512; }
+
+// one split per SM-sized slice of the grid: about nsm CTAs per layer in all
+int wgrad_tc_splits(int nsm, int64_t rows, int mpad) {
   const int64_t chunks = (rows + 31) / 32;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(nsm, chunks));
+  const int nb2 = mpad > 256 ? (mpad / 256) * (mpad / 256) : 1;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, nsm / nb2), chunks));
 }
 
 template <int MPAD>
 __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const WgradArgs a) {
   using C = WtcCfg<MPAD>;
-  constexpr int JC = C::JC, MH = C::MH, NST = C::NST;
+  constexpr int JC = C::JC, MH = C::MH, NST = C::NST, BW = C::BW, NB = C::NB;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = smem_raw;
@@ -68,7 +76,8 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
   tc::fence_after();
   const uint32_t tbase = *tslot;
 
-  const int split = blockIdx.x;
+  const int split = blockIdx.x / (NB * NB);
+  const int bm = (blockIdx.x % (NB * NB)) / NB, bn = blockIdx.x % NB;  // output block rows / cols
   const int64_t per = ((a.rows + a.nsplit - 1) / a.nsplit + JC - 1) / JC * JC;
   const int64_t j0 = (int64_t)split * per;
   const int64_t j1 = min(a.rows, j0 + per);
@@ -78,7 +87,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
   if (warp == 0) {
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(128, MPAD, 1, 1);
+      constexpr uint32_t idesc = tc::idesc_bf16(128, BW, 1, 1);
       uint32_t it = 0;
       {
         for (int ch = 0; ch < nchunk; ++ch, ++it) {
@@ -98,7 +107,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
                                                        1024, C::KSTRIDE);
                 const uint64_t bd =
                     tc::sdesc_sw128_mn(aa + tc::prod_b(q) * C::PIECE + ks * 2 * C::KSTRIDE, 1024, C::KSTRIDE);
-                tc::mma_bf16(tbase + h * MPAD, ad, bd, idesc, (ch | ks | q) != 0 ? 1u : 0u);
+                tc::mma_bf16(tbase + h * BW, ad, bd, idesc, (ch | ks | q) != 0 ? 1u : 0u);
               }
           tc::mma_commit(&sempty[s]);
         }
@@ -110,11 +119,11 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
     const int sw = warp - 1;        // 0 .. NSTG-1
     const int st = tid - 32;        // 0 .. NSTG*32-1
     uint32_t it = 0;
-    constexpr int QUADS = MPAD / 4;  // float4 per j row
+    constexpr int QUADS = BW / 4;  // float4 per j row of the block
     {
       const int layer = a.first_layer + li;
-      const float* D = a.del + (size_t)layer * a.stride_layer;
-      const float* A = a.actv + (size_t)(layer - 1) * a.stride_layer;
+      const float* D = a.del + (size_t)layer * a.stride_layer + bm * BW;
+      const float* A = a.actv + (size_t)(layer - 1) * a.stride_layer + bn * BW;
       for (int ch = 0; ch < nchunk; ++ch, ++it) {
         const int s = (int)(it % NST);
         mbar_wait(&sempty[s], ((it / NST) & 1u) ^ 1u);
@@ -132,7 +141,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
           dv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           av[q] = dv[q];
           if (j < j1) {
-            FDSDF_ASSERT(j >= 0 && j < a.rows && r + 4 <= MPAD && layer >= 1);
+            FDSDF_ASSERT(j >= 0 && j < a.rows && r + 4 <= BW && layer >= 1);
             dv[q] = __ldg(reinterpret_cast<const float4*>(D + j * MPAD + r));
             av[q] = __ldg(reinterpret_cast<const float4*>(A + j * MPAD + r));
           }
@@ -141,7 +150,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
         for (int q = 0; q < NIT; ++q) {
           const int item = st + q * C::NSTG * 32;
           const int jj = item / QUADS, r = (item % QUADS) * 4;
-          const uint32_t off = tc::sw128mn_off(r, jj, MPAD);
+          const uint32_t off = tc::sw128mn_off(r, jj, BW);
           FDSDF_ASSERT(off + 8 <= (uint32_t)C::PIECE);
           uint32_t d01[3], d23[3], a01[3], a23[3];
           tc::split3x2(dv[q].x, dv[q].y, d01);
@@ -164,11 +173,11 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
       float* out = a.part + ((size_t)li * a.nsplit + split) * MPAD * MPAD;
       for (int h = sw >> 2; h < MH; h += C::NSTG / 4) {
         const int q4 = (warp & 3);
-        const int m = h * 128 + 32 * q4 + lane;
-        const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + h * MPAD;
-        float* row = out + (size_t)m * MPAD;
+        const int m = bm * BW + h * 128 + 32 * q4 + lane;
+        const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + h * BW;
+        float* row = out + (size_t)m * MPAD + bn * BW;
 #pragma unroll 1
-        for (int k0 = 0; k0 < MPAD; k0 += 16) {
+        for (int k0 = 0; k0 < BW; k0 += 16) {
           float v[16];
           tc::tmem_ld16(taddr + k0, v);
           if (nchunk == 0) {  // empty j-range: the accumulator was never written
@@ -193,12 +202,13 @@ static cudaError_t launch_wgrad_tc_t(const WgradArgs& a, int nglayers, cudaStrea
   using C = WtcCfg<MPAD>;
   cudaError_t e = cudaFuncSetAttribute(wgrad_tc_kernel<MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
   if (e != cudaSuccess) return e;
-  wgrad_tc_kernel<MPAD><<<dim3(a.nsplit, nglayers), C::NTHR, C::BYTES, st>>>(a);
+  wgrad_tc_kernel<MPAD><<<dim3(a.nsplit * C::NB * C::NB, nglayers), C::NTHR, C::BYTES, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, cudaStream_t st) {
   if (nglayers <= 0) return cudaSuccess;
+  if (a.mpad == 512) return launch_wgrad_tc_t<512>(a, nglayers, st);
   if (a.mpad == 256) return launch_wgrad_tc_t<256>(a, nglayers, st);
   if (a.mpad == 128) return launch_wgrad_tc_t<128>(a, nglayers, st);
   return cudaErrorInvalidValue;

@@ -23,7 +23,7 @@ KIND = {"ncr": 0, "nsh": 1}
 FD_FORM = {"abs": 0, "square": 1}
 STEP_ACCUMULATE, STEP_ALLREDUCE = 1, 2
 CREATE_EVAL_ONLY, CREATE_FFMA, CREATE_TENSOR = 1, 2, 4
-PATH = {0: "ffma", 1: "tensor"}
+PATH = {0: "ffma", 1: "tensor", 2: "hybrid"}
 FLAG_NONFINITE_INPUT, FLAG_NONFINITE_LOSS, FLAG_ALL_FD_SKIPPED, FLAG_NONFINITE_GRAD = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_EMPTY", 3: "E_CUDA", 4: "E_NCCL", 5: "E_NOMEM",
           6: "E_UNSUPPORTED"}

@@ -114,8 +114,11 @@ def test_c4_h_sweep(h):
     assert err["mask"] == 0
 
 
-def test_c3_full_size_ffma():
-    """C3 (softplus 3->512x8->1 with the skip layer, 100k centres; FFMA path):
+@pytest.mark.parametrize("path", [None, "ffma"])
+def test_c3_full_size(path):
+    """C3 (softplus 3->512x8->1 with the skip layer, 100k centres; default = the hybrid path:
+    tensor-core forward with the skip input and weight gradient, FFMA backward; and the FFMA
+    path):
     f, grad f, FD entries, D, K on 400 sampled rows of the full-size eval against the oracle
     (GIVEN frames exported by the GPU); the full-size step is finite and bitwise reproducible.
     The oracle cannot afford the full C3 step (~11 TFLOP in fp64 on the host), so the step's
@@ -124,8 +127,8 @@ def test_c3_full_size_ffma():
     from paper_2511_08980_b200 import FDSDF
     c = make_config("c3")
     n = len(c["x"])
-    m = FDSDF(c["spec"], 0, max_centers=n)
-    assert m.path == "ffma"
+    m = FDSDF(c["spec"], 0, max_centers=n, path=path)
+    assert m.path == ("hybrid" if path is None else "ffma"), m.path
     ev = gpu_eval(m, c, denom=c["loss"]["denom"])
     rng = np.random.default_rng(33)
     idx = np.sort(rng.choice(n, 400, replace=False))
@@ -146,7 +149,7 @@ def test_c3_full_size_ffma():
     dt = time.perf_counter() - t0
     g1, l1 = g1.cpu().numpy(), l1.cpu().numpy()
     g2, l2 = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])
-    print(f"c3 full-size step {dt * 1e3:.1f} ms (wall, 1st call), loss {l1[:5]}")
+    print(f"c3 full-size step [{m.path}] {dt * 1e3:.1f} ms (wall, 1st call), loss {l1[:5]}")
     assert np.isfinite(l1).all() and np.isfinite(g1).all()
     assert np.array_equal(g1, g2.cpu().numpy()) and np.array_equal(l1, l2.cpu().numpy())
     m.close()

@@ -34,7 +34,12 @@ def path(request):
 def _model(spec, n, eval_only=False, path=None):
     from paper_2511_08980_b200 import FDSDF
     if path == "tensor" and (spec.get("skip_at", -1) >= 0 or max(spec["widths"][1:-1]) > 256):
-        pytest.skip("tensor path needs widths <= 256 and no skip layer (C3 runs FFMA)")
+        # the full tensor path needs widths <= 256 and no skip layer; such networks (C3) take the
+        # default hybrid path (tensor-core forward with the skip input and weight gradient, FFMA
+        # backward)
+        m = FDSDF(spec, 0, max_centers=n, eval_only=eval_only)
+        assert m.path == "hybrid", m.path
+        return m
     m = FDSDF(spec, 0, max_centers=n, eval_only=eval_only, path=path)
     assert path is None or m.path == path
     return m
