@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(NTH, 2) bwd_kernel(const BwdArgs a) {
       const bool store_act = (l <= L - 3) && valid;
       float* delp = a.del + (size_t)l * nrows * MPAD + (size_t)c * NCOLB * MPAD;
       float* actp = a.actv + (size_t)l * nrows * MPAD + (size_t)c * NCOLB * MPAD;
-      const float* zq = a.zf + ((size_t)c * nh + l) * NCOLF * MPAD;
+      // this (centre, layer)'s stored pre-activations: float4 groups per neuron (kernels.cuh)
+      const float4* zq = reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD);
 
       float w0s[2][4][3];  // dW_0 partials (l == 0), parked after the epilogue barrier
 #pragma unroll
@@ -147,18 +148,12 @@ __global__ void __launch_bounds__(NTH, 2) bwd_kernel(const BwdArgs a) {
         const int mb = tile_row<MPAD>(rg, q * 4);
         float zc[4], tr[4];
         {
-          float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f), t0 = z4, t1 = z4, t2 = z4;
-          if (valid) {
-            z4 = *reinterpret_cast<const float4*>(zq + 0 * MPAD + mb);
-            t0 = *reinterpret_cast<const float4*>(zq + 1 * MPAD + mb);
-            t1 = *reinterpret_cast<const float4*>(zq + 2 * MPAD + mb);
-            t2 = *reinterpret_cast<const float4*>(zq + 3 * MPAD + mb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 g0 = valid ? zq[mb + j] : make_float4(0.f, 0.f, 0.f, 0.f);  // (z, t0, t1, t2)
+            zc[j] = g0.x;
+            tr[j] = fmaf(r0, g0.y, fmaf(r1, g0.z, r2 * g0.w));
           }
-          zc[0] = z4.x; zc[1] = z4.y; zc[2] = z4.z; zc[3] = z4.w;
-          tr[0] = fmaf(r0, t0.x, fmaf(r1, t1.x, r2 * t2.x));
-          tr[1] = fmaf(r0, t0.y, fmaf(r1, t1.y, r2 * t2.y));
-          tr[2] = fmaf(r0, t0.z, fmaf(r1, t1.z, r2 * t2.z));
-          tr[3] = fmaf(r0, t0.w, fmaf(r1, t1.w, r2 * t2.w));
         }
         typename AF::C cc[4];
 #pragma unroll
@@ -175,13 +170,14 @@ __global__ void __launch_bounds__(NTH, 2) bwd_kernel(const BwdArgs a) {
         // ---------------------------------------------------------------- 4 pairs
 #pragma unroll 1
         for (int p = 0; p < 4; ++p) {
-          float4 A4 = make_float4(0.f, 0.f, 0.f, 0.f), S4 = A4;
-          if (valid) {
-            A4 = *reinterpret_cast<const float4*>(zq + (4 + 2 * p) * MPAD + mb);
-            S4 = *reinterpret_cast<const float4*>(zq + (5 + 2 * p) * MPAD + mb);
+          float Av[4], Sv[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {  // (A_p, S_p): half (p & 1) of group 1 + p / 2
+            const float2 as = valid ? reinterpret_cast<const float2*>(zq + (1 + (p >> 1)) * MPAD + mb + j)[p & 1]
+                                    : make_float2(0.f, 0.f);
+            Av[j] = as.x;
+            Sv[j] = as.y;
           }
-          const float Av[4] = {A4.x, A4.y, A4.z, A4.w};
-          const float Sv[4] = {S4.x, S4.y, S4.z, S4.w};
           // offset d_p (for the skip x-part and layer-0 weight gradient)
           const float dpx = p == 0 ? u0 : (p == 1 ? v0 : (p == 2 ? u0 + v0 : u0 - v0));
           const float dpy = p == 0 ? u1 : (p == 1 ? v1 : (p == 2 ? u1 + v1 : u1 - v1));

@@ -171,10 +171,16 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       const float omt = net.omega[ltop];
       const float wlt = net.W[L - 1][m];
       FDSDF_ASSERT(c >= 0 && c < a.n);
-      const float* zq = a.zf + ((size_t)c * nh + ltop) * NCOLF * MPAD + m;
+      const float4* zq = reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + ltop) * NCOLF * MPAD) + m;
       float zv[NCOLF];
 #pragma unroll
-      for (int j = 0; j < NCOLF; ++j) zv[j] = __ldg(zq + j * MPAD);
+      for (int g = 0; g < ZG; ++g) {
+        const float4 v = __ldg(zq + g * MPAD);
+        zv[4 * g] = v.x;
+        zv[4 * g + 1] = v.y;
+        zv[4 * g + 2] = v.z;
+        zv[4 * g + 3] = v.w;
+      }
       const float* sd = sdsT + cl * 20;
       const float dL[NCOLB] = {sd[0], 1.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
       const typename AF::C cc = AF::centre(zv[0], beta);
@@ -278,16 +284,20 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           const int64_t c = c0 + eg + EG * i;
           if (i < CPE && c < a.n && mok) {
             FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
-            const float* zq = a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + m;
-            q.z = __ldg(zq);
-            q.t0 = __ldg(zq + 1 * MPAD);
-            q.t1 = __ldg(zq + 2 * MPAD);
-            q.t2 = __ldg(zq + 3 * MPAD);
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              q.A[p] = __ldg(zq + (4 + 2 * p) * MPAD);
-              q.S[p] = __ldg(zq + (5 + 2 * p) * MPAD);
-            }
+            const float4* zq = reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD) + m;
+            const float4 g0 = __ldg(zq), g1 = __ldg(zq + MPAD), g2 = __ldg(zq + 2 * MPAD);
+            q.z = g0.x;
+            q.t0 = g0.y;
+            q.t1 = g0.z;
+            q.t2 = g0.w;
+            q.A[0] = g1.x;
+            q.S[0] = g1.y;
+            q.A[1] = g1.z;
+            q.S[1] = g1.w;
+            q.A[2] = g2.x;
+            q.S[2] = g2.y;
+            q.A[3] = g2.z;
+            q.S[3] = g2.w;
           }
           return q;
         };
@@ -379,11 +389,11 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           const int64_t c = c0 + eg + EG * i;
           z4[0] = z4[1] = z4[2] = z4[3] = 0.f;
           if (!CARRY && i < CPE && c < a.n && mok) {
-            const float* zq = a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + m;
-            z4[0] = __ldg(zq);
-            z4[1] = __ldg(zq + 1 * MPAD);
-            z4[2] = __ldg(zq + 2 * MPAD);
-            z4[3] = __ldg(zq + 3 * MPAD);
+            const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD) + m);
+            z4[0] = g0.x;
+            z4[1] = g0.y;
+            z4[2] = g0.z;
+            z4[3] = g0.w;
           }
         };
         float zn[4];

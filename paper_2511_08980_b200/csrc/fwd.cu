@@ -86,11 +86,12 @@ __global__ void __launch_bounds__(NTH, 2) fwd_kernel(const FwdArgs a) {
 #pragma unroll
   for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
 
-  // pointer to the stored pre-activation column `col` of layer l for tile slot / centre c
-  auto zp = [&](int slot, int64_t c, int l, int col) -> float* {
-    const int64_t idx = step ? c : slot;
-    return zbase + ((idx * nh + l) * zcols + col) * (int64_t)MPAD;
+  // stored pre-activations of layer l for tile slot / centre c: step -> float4 group g of
+  // neuron m (kernels.cuh zf layout); eval scratch -> the centre values, [MPAD]
+  auto zg4 = [&](int64_t c, int l, int g, int m) -> float4* {
+    return reinterpret_cast<float4*>(zbase + ((c * nh + l) * zcols + 4 * g) * (int64_t)MPAD) + m;
   };
+  auto zev = [&](int slot, int l) -> float* { return zbase + ((int64_t)slot * nh + l) * (int64_t)MPAD; };
 
   float acc[8][8];
   float acc2[8][2];
@@ -159,12 +160,11 @@ __global__ void __launch_bounds__(NTH, 2) fwd_kernel(const FwdArgs a) {
           }
           const int mb = tile_row<MPAD>(rg, q * 4);
           if (valid) {
-            *reinterpret_cast<float4*>(zp(slot, c, l, 0) + mb) = make_float4(zv[0], zv[1], zv[2], zv[3]);
             if (step) {
 #pragma unroll
-              for (int d = 0; d < 3; ++d)
-                *reinterpret_cast<float4*>(zp(slot, c, l, 1 + d) + mb) =
-                    make_float4(tv[0][d], tv[1][d], tv[2][d], tv[3][d]);
+              for (int j = 0; j < 4; ++j) *zg4(c, l, 0, mb + j) = make_float4(zv[j], tv[j][0], tv[j][1], tv[j][2]);
+            } else {
+              *reinterpret_cast<float4*>(zev(slot, l) + mb) = make_float4(zv[0], zv[1], zv[2], zv[3]);
             }
           }
 #pragma unroll
@@ -242,10 +242,15 @@ __global__ void __launch_bounds__(NTH, 2) fwd_kernel(const FwdArgs a) {
       for (int l = 0; l <= L - 2; ++l) {
         // prefetch the centre pre-activations of this layer (written in phase 1)
         float zpre[8];
-        {
-          const float4 z0 = valid ? *reinterpret_cast<const float4*>(zp(slot, c, l, 0) + tile_row<MPAD>(rg, 0))
+        if (step) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) zpre[4 * q + j] = valid ? zg4(c, l, 0, tile_row<MPAD>(rg, 4 * q) + j)->x : 0.f;
+        } else {
+          const float4 z0 = valid ? *reinterpret_cast<const float4*>(zev(slot, l) + tile_row<MPAD>(rg, 0))
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-          const float4 z1 = valid ? *reinterpret_cast<const float4*>(zp(slot, c, l, 0) + tile_row<MPAD>(rg, 4))
+          const float4 z1 = valid ? *reinterpret_cast<const float4*>(zev(slot, l) + tile_row<MPAD>(rg, 4))
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
           zpre[0] = z0.x; zpre[1] = z0.y; zpre[2] = z0.z; zpre[3] = z0.w;
           zpre[4] = z1.x; zpre[5] = z1.y; zpre[6] = z1.z; zpre[7] = z1.w;
@@ -297,11 +302,9 @@ __global__ void __launch_bounds__(NTH, 2) fwd_kernel(const FwdArgs a) {
           const int mb = tile_row<MPAD>(rg, q * 4);
           if (step && valid) {
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              *reinterpret_cast<float4*>(zp(slot, c, l, 4 + 2 * p) + mb) =
-                  make_float4(Av[0][p], Av[1][p], Av[2][p], Av[3][p]);
-              *reinterpret_cast<float4*>(zp(slot, c, l, 5 + 2 * p) + mb) =
-                  make_float4(Sv[0][p], Sv[1][p], Sv[2][p], Sv[3][p]);
+            for (int j = 0; j < 4; ++j) {
+              *zg4(c, l, 1, mb + j) = make_float4(Av[j][0], Sv[j][0], Av[j][1], Sv[j][1]);
+              *zg4(c, l, 2, mb + j) = make_float4(Av[j][2], Sv[j][2], Av[j][3], Sv[j][3]);
             }
           }
 #pragma unroll

@@ -170,10 +170,15 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
 #pragma unroll
     for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
 
-    // this thread's element of stored pre-activation column `col`, layer l, centre c
-    auto zp = [&](int64_t c, int l, int col) -> float* {
-      FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && col >= 0 && col < a.zcols && m < MPAD);
-      return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
+    // this thread's stored pre-activations of layer l, centre c (kernels.cuh zf layout): float4
+    // group g (step), the centre value z (step or eval)
+    auto zg4 = [&](int64_t c, int l, int g) -> float4* {
+      FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && g >= 0 && g < ZG && a.zcols == NCOLF && m < MPAD);
+      return reinterpret_cast<float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + (size_t)g * 4 * MPAD) + m;
+    };
+    auto zc = [&](int64_t c, int l) -> float* {
+      FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && m < MPAD);
+      return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (a.zcols == 1 ? m : 4 * m);
     };
     auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
     // cat(a, x) / sqrt(2) at the input of the skip layer net.skip (IGR convention, SURVEY §8c
@@ -241,13 +246,10 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           t2 = om * w2;
         }
         if (valid) {
-          float* zc = zp(c, 0, 0);
-          zc[0] = z;
-          if (step) {
-            zc[1 * MPAD] = t0;
-            zc[2 * MPAD] = t1;
-            zc[3 * MPAD] = t2;
-          }
+          if (step)
+            *zg4(c, 0, 0) = make_float4(z, t0, t1, t2);
+          else
+            *zc(c, 0) = z;
         }
         float o[4] = {0.f, 0.f, 0.f, 0.f};
         if (mok) {
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         tc::tmem_st4(tstash + i * CPC, o);
       } else {
         const float* ci = cis_t + cl * NCINFO;
-        const float z0 = valid ? __ldg(zp(c, 0, 0)) : 0.f;
+        const float z0 = valid ? __ldg(zc(c, 0)) : 0.f;
         float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
         if (mok) {
           const float* W0 = net.W[0];
@@ -276,12 +278,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           Av[3] = hs * (du - dv);
         }
         if (step && valid) {
-          float* zc0 = zp(c, 0, 0);
-#pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            zc0[(4 + 2 * p) * MPAD] = Av[p];
-            zc0[(5 + 2 * p) * MPAD] = Sv[p];
-          }
+          *zg4(c, 0, 1) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
+          *zg4(c, 0, 2) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
         }
         float o[8];
 #pragma unroll
@@ -422,7 +420,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         // mode 2: the centre pre-activation of this neuron, prefetched one centre ahead
         auto ldz = [&](int i) -> float {
           const int64_t c = c0 + sp * CPSPL + eg + C::EG * i;
-          return (MODE == 2 && i < CPEs && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
+          return (MODE == 2 && i < CPEs && c < a.n) ? __ldg(zc(c, l)) : 0.f;
         };
         float z0n = ldz(0);
         if (pipe0 && l >= l0first) {  // the next tile's layer 0, spread over this tile's MMA phases
@@ -481,13 +479,10 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               }
             }
             if (valid) {
-              float* zc = zp(c, l, 0);
-              zc[0] = z;
-              if (step) {
-                zc[1 * MPAD] = t0;
-                zc[2 * MPAD] = t1;
-                zc[3 * MPAD] = t2;
-              }
+              if (step)
+                *zg4(c, l, 0) = make_float4(z, t0, t1, t2);
+              else
+                *zc(c, l) = z;
             }
             float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
             if (mok) {
@@ -534,12 +529,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               }
             }
             if (step && valid) {
-              float* zc = zp(c, l, 0);
-#pragma unroll
-              for (int p = 0; p < 4; ++p) {
-                zc[(4 + 2 * p) * MPAD] = Av[p];
-                zc[(5 + 2 * p) * MPAD] = Sv[p];
-              }
+              *zg4(c, l, 1) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
+              *zg4(c, l, 2) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
             }
             float o[8];
 #pragma unroll

@@ -293,8 +293,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
 #pragma unroll
     for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
 
-    auto zp = [&](int64_t c, int l, int col) -> float* {
-      return a.zf + (((size_t)c * nh + l) * a.zcols + col) * (size_t)MPAD + m;
+    // this thread's stored pre-activations (kernels.cuh zf layout): float4 group g (step), the
+    // centre value z (step or eval)
+    auto zg4 = [&](int64_t c, int l, int g) -> float4* {
+      return reinterpret_cast<float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + (size_t)g * 4 * MPAD) + m;
+    };
+    auto zc = [&](int64_t c, int l) -> float* {
+      return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (a.zcols == 1 ? m : 4 * m);
     };
     // 8 accumulator columns [c8, c8 + 8) of a slot (pair-wide column numbers, within one owner
     // CTA's 32): R01 holds owner o's columns as [o][b0 | b1 products][32], R2 as [o][32]
@@ -384,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
 #pragma unroll
           for (int jj = 0; jj < CPT; ++jj) {
             const int64_t c = cs + eg + 4 * pos_i(jj);
-            z0n[jj] = (MODE == 2 && c < a.n) ? __ldg(zp(c, l, 0)) : 0.f;
+            z0n[jj] = (MODE == 2 && c < a.n) ? __ldg(zc(c, l)) : 0.f;
           }
           if (l > 0) {
             ptimer.before_wait();
@@ -554,15 +559,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
             const int64_t c = cs + eg + 4 * pos_i(jj);
             if (c < a.n) {
               if (MODE == 1) {
-                *zp(c, l, 0) = zst[jj][0];
-                if (step) {
-                  *zp(c, l, 1) = zst[jj][1];
-                  *zp(c, l, 2) = zst[jj][2];
-                  *zp(c, l, 3) = zst[jj][3];
-                }
+                if (step)
+                  *zg4(c, l, 0) = make_float4(zst[jj][0], zst[jj][1], zst[jj][2], zst[jj][3]);
+                else
+                  *zc(c, l) = zst[jj][0];
               } else if (step) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) *zp(c, l, 4 + q) = zst[jj][q];
+                *zg4(c, l, 1) = make_float4(zst[jj][0], zst[jj][1], zst[jj][2], zst[jj][3]);
+                *zg4(c, l, 2) = make_float4(zst[jj][4], zst[jj][5], zst[jj][6], zst[jj][7]);
               }
             }
           }

@@ -13,6 +13,11 @@ constexpr int NCW = 8;             // compute warps per CTA
 constexpr int NCT = NCW * 32;      // compute threads
 constexpr int NTH = NCT;           // thread 0 also issues the TMA weight slabs
 constexpr int NCOLF = 12;          // stored forward columns per centre: c, t0..2, (A,S) x 4
+// zf (the step's stored pre-activations) layout: [n][nh][NCOLF/4][mpad][4] -- per (centre,
+// hidden layer), the 12 columns in float4 groups per neuron m: g0 = (z, t0, t1, t2),
+// g1 = (A0, S0, A1, S1), g2 = (A2, S2, A3, S3) (one 16-byte access per group and neuron; a
+// warp's 32 neurons are 512 contiguous bytes).  Eval scratch (zcols = 1): [..][nh][mpad].
+constexpr int ZG = NCOLF / 4;      // float4 groups of zf per (centre, layer)
 constexpr int NCOLB = 10;          // backward columns: c, t_r, (A,S) x 4
 constexpr int NSEED = 16;          // per-centre: fbar, Sbar_u, Sbar_v, Sbar_p, Sbar_q, r(3), u(3), v(3), pad
 constexpr int NLOSS = 6;           // dm, dnm, eik, fd, n_degenerate, n_nonfinite
@@ -58,7 +63,7 @@ struct FwdArgs {
   float* out_frames;
   uint8_t* out_mask;
   // workspace
-  float* zf;             // step: [n][nh][12][mpad]; eval: per-CTA scratch
+  float* zf;             // step: [n][nh][3][mpad][4] (NCOLF above); eval: z only
   float* seed;           // [n][8]
   double* lossp;         // [gridDim.x][NLOSS]
   unsigned* dflags;      // sticky device flags
@@ -72,7 +77,7 @@ struct FwdArgs {
 struct BwdArgs {
   Net net;
   const float* x;
-  const float* zf;       // [n][nh][12][mpad]
+  const float* zf;       // [n][nh][3][mpad][4] (NCOLF above)
   const float* seed;     // [n][8]
   int64_t n;
   float h;
