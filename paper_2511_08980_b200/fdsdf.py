@@ -169,7 +169,7 @@ def fdsdf_spec_num_params(spec: dict) -> int:
 
 def fdsdf_create(spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False,
                  path: str | None = None):
-    """path: None (library default), "ffma" or "tensor"."""
+    """path: None (library default: "tensor" where supported, else "hybrid"), "ffma" or "tensor"."""
     s = make_spec(spec)
     h = C.c_void_p()
     flags = (CREATE_EVAL_ONLY if eval_only else 0) | {None: 0, "ffma": CREATE_FFMA, "tensor": CREATE_TENSOR}[path]
