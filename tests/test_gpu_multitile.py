@@ -22,13 +22,14 @@ from harness import make_config
 from oracle import oracle_step, oracle_eval
 from gpu_util import compare_eval, gpu_eval, per_tensor_grad_errors
 from paper_2511_08980_b200 import FDSDF
-name, ns, nu = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+name, ns, nu, path = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
 c = make_config(name, ns, nu)
 n = len(c["x"])
 m = FDSDF(c["spec"], 0, max_centers=n)
-assert m.path == "tensor", m.path
+assert m.path == path, m.path
 ev = gpu_eval(m, c, denom=c["loss"]["denom"])
-o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
+o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]),
+                denom=c["loss"]["denom"], denom_pow=c["loss"]["denom_pow"])
 err = compare_eval(ev, o)
 assert all(err[k] <= 1.0 for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K")), err
 g, l = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])
@@ -49,12 +50,15 @@ def _built():
     build()
 
 
-# (config, surface rows, off-surface rows, SMs): c2 (SIREN 256, MPAD 256) 1313 centres on 2
-# SMs -> 41 / 82 tiles per CTA in the forward / backward; c1 (softplus 64, MPAD 128) on 3 SMs
-@pytest.mark.parametrize("name,ns,nu,sms", [("c2", 700, 613, 2), ("c1", 509, 400, 3)])
-def test_many_tiles_per_cta(name, ns, nu, sms):
+# (config, surface rows, off-surface rows, SMs, path): c2 (SIREN 256, MPAD 256) 1313 centres on
+# 2 SMs -> 41 / 82 tiles per CTA in the forward / backward; c1 (softplus 64, MPAD 128) on 3 SMs;
+# c3 (softplus 512 with the skip layer, hybrid path: N = 32 forward tiles of 4 centres) 131
+# centres on 2 SMs -> 16-17 forward tiles per CTA, one weight-gradient split of four blocks
+@pytest.mark.parametrize("name,ns,nu,sms,path", [("c2", 700, 613, 2, "tensor"), ("c1", 509, 400, 3, "tensor"),
+                                                 ("c3", 70, 61, 2, "hybrid")])
+def test_many_tiles_per_cta(name, ns, nu, sms, path):
     env = dict(os.environ, FDSDF_MAX_SM=str(sms))
-    r = subprocess.run([sys.executable, "-c", SCRIPT, name, str(ns), str(nu)], env=env, capture_output=True,
-                       text=True, timeout=600)
+    r = subprocess.run([sys.executable, "-c", SCRIPT, name, str(ns), str(nu), path], env=env,
+                       capture_output=True, text=True, timeout=600)
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0 and "MULTITILE-OK" in r.stdout

@@ -23,7 +23,8 @@ c = make_config("c2", 700, 613)
 n = len(c["x"])
 m = FDSDF(c["spec"], 0, max_centers=n)
 ev = gpu_eval(m, c, denom=c["loss"]["denom"])
-o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
+o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]),
+                denom=c["loss"]["denom"], denom_pow=c["loss"]["denom_pow"])
 err = compare_eval(ev, o)
 assert all(err[k] <= 1.0 for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K")), err
 g, l = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])

@@ -196,14 +196,17 @@ def test_tiny_batches(n, path):
 
 
 # ragged, unequal hidden widths (not multiples of 32 / 64): zero-padded neuron rows and K
-# ranges inside the tensor tiles (MPAD 256), both activations, a 3-GEMM network
-RAGGED = [("sine", [3, 100, 200, 150, 1]), ("softplus", [3, 37, 129, 90, 61, 1])]
+# ranges inside the tensor tiles (MPAD 256), both activations, a 3-GEMM network; and two
+# networks of the hybrid path: a skip layer whose input cat(a, x) crosses a padding boundary
+# (126 + 3 -> MPAD 256) and ragged 512-padded widths with a skip layer
+RAGGED = [("sine", [3, 100, 200, 150, 1], -1), ("softplus", [3, 37, 129, 90, 61, 1], -1),
+          ("softplus", [3, 100, 126, 90, 1], 2), ("sine", [3, 300, 333, 290, 1], 2)]
 
 
-@pytest.mark.parametrize("act,widths", RAGGED)
-def test_ragged_widths_eval_and_step(act, widths, path):
+@pytest.mark.parametrize("act,widths,skip", RAGGED)
+def test_ragged_widths_eval_and_step(act, widths, skip, path):
     from harness import init_params, mlp_spec, uniform_box, csg_surface
-    spec = mlp_spec(widths, act, beta=100.0)
+    spec = mlp_spec(widths, act, beta=100.0, skip_at=skip)
     params = init_params(spec, "siren" if act == "sine" else "xavier", 11)
     xs = csg_surface(150, 3, 12).astype(np.float32)
     xu = uniform_box(131, 1.1, 13).astype(np.float32)
@@ -215,7 +218,7 @@ def test_ragged_widths_eval_and_step(act, widths, path):
     g = gpu_eval(m, c)
     o = oracle_eval(spec, params, x, ns, h, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
     err = compare_eval(g, o)
-    print(act, widths, path, {k: float(v) for k, v in err.items()})
+    print(act, widths, skip, m.path, {k: float(v) for k, v in err.items()})
     for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K"):
         assert err[k] <= 1.0, (k, err)
     grad, loss = m.step(params, x, ns, h, ls, frame_seed=5)
