@@ -171,14 +171,14 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
     for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
 
     // this thread's stored pre-activations of layer l, centre c (kernels.cuh zf layout): float4
-    // group g (step), the centre value z (step or eval)
+    // group g (step), the centre value z (step: in group 0; eval: z only, contiguous over m)
     auto zg4 = [&](int64_t c, int l, int g) -> float4* {
       FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && g >= 0 && g < ZG && a.zcols == NCOLF && m < MPAD);
       return reinterpret_cast<float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + (size_t)g * 4 * MPAD) + m;
     };
     auto zc = [&](int64_t c, int l) -> float* {
       FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && m < MPAD);
-      return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (a.zcols == 1 ? m : 4 * m);
+      return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (step ? 4 * m : m);
     };
     auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
     // cat(a, x) / sqrt(2) at the input of the skip layer net.skip (IGR convention, SURVEY §8c

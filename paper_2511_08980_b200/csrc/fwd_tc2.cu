@@ -294,12 +294,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(F2Cfg<MODE>::NTHR, 1
     for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
 
     // this thread's stored pre-activations (kernels.cuh zf layout): float4 group g (step), the
-    // centre value z (step or eval)
+    // centre value z (step: in group 0; eval: z only, contiguous over m)
     auto zg4 = [&](int64_t c, int l, int g) -> float4* {
       return reinterpret_cast<float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + (size_t)g * 4 * MPAD) + m;
     };
     auto zc = [&](int64_t c, int l) -> float* {
-      return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (a.zcols == 1 ? m : 4 * m);
+      return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (step ? 4 * m : m);
     };
     // 8 accumulator columns [c8, c8 + 8) of a slot (pair-wide column numbers, within one owner
     // CTA's 32): R01 holds owner o's columns as [o][b0 | b1 products][32], R2 as [o][32]
