@@ -434,6 +434,30 @@ def main():
     extras = {}
     if not args.no_extras and (world == 1 or lib_ar):
         extras = measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank, dev)
+    if not args.no_extras and world == 1 and model.path != "ffma":
+        # the same step with the opt-in 3-product weight gradient (FDSDF_CREATE_WGRAD_BF16X3,
+        # DESIGN.md §4b): reported beside the headline, never as it
+        m3 = FDSDF(spec, local, max_centers=n, path=None if args.path == "default" else args.path,
+                   wgrad_bf16x3=True)
+
+        def step3(i):
+            F.fdsdf_step(m3.ctx, params, x, n, stencil(i), ls, grad, loss, 0, stream)
+
+        for i in range(args.warmup):
+            step3(i)
+        ms3 = _event_ms(stream, step3, args.steps, flush)
+        m3.set_kernel_timing(True)
+        m3.kernel_times(reset=True)
+        for i in range(3):
+            step3(i)
+        torch.cuda.synchronize()
+        kt3 = m3.kernel_times(reset=True)
+        m3.close()
+        extras["step_wgrad_bf16x3"] = {
+            "ms_per_step": ms3, "value": 9.0 * n / (ms3 * 1e-3), "unit": UNIT,
+            "wgrad_ms": kt3["wgrad"][0] / max(kt3["wgrad"][1], 1),
+            "what": "opt-in FDSDF_CREATE_WGRAD_BF16X3: weight gradient with 3 bf16 piece products "
+                    "(~3*2^-16 per product); forward / delta propagation bf16x6; same oracle gates"}
 
     # ------------------------------------------------------------------ roofline of the dominant kernel
     P_mm, P_gemm = p_mm(spec)

@@ -148,13 +148,20 @@ typedef struct fdsdf_ctx fdsdf_ctx;
 enum {
   FDSDF_CREATE_EVAL_ONLY = 1u,  /* no step workspace                                          */
   FDSDF_CREATE_FFMA = 2u,       /* run every contraction as fp32 FFMA (the validation path)   */
-  FDSDF_CREATE_TENSOR = 4u      /* require the tcgen05 tensor-core path: every MLP contraction */
+  FDSDF_CREATE_TENSOR = 4u,     /* require the tcgen05 tensor-core path: every MLP contraction */
                                 /* (forward, backward, weight gradient) with the fp32-accurate */
                                 /* bf16x6 piece scheme; needs hidden widths   */
                                 /* <= 256 and no skip layer, else FDSDF_E_UNSUPPORTED.        */
                                 /* Neither flag: the tensor path where supported, else the    */
                                 /* hybrid path (128/256/512-padded widths), else FFMA.       */
                                 /* Both flags -> FDSDF_E_INVALID.                             */
+  FDSDF_CREATE_WGRAD_BF16X3 = 8u /* opt-in: the weight-gradient contraction with the three    */
+                                /* leading bf16 piece products only (a0 b0 + a0 b1 + a1 b0,   */
+                                /* each to ~3 * 2^-16 relative instead of bf16x6's ~2^-24;    */
+                                /* DESIGN.md §4b); forward and delta propagation unchanged.   */
+                                /* Needs the tensor-core weight gradient (tensor or hybrid    */
+                                /* path): with FDSDF_CREATE_FFMA -> FDSDF_E_INVALID, else on  */
+                                /* an FFMA-only network -> FDSDF_E_UNSUPPORTED.               */
 };
 /* Environment read at create time: FDSDF_MAX_SM=k (k >= 2) caps the persistent grids at k
  * SMs (GPU sharing; the tests use it to run many tiles per CTA at oracle-sized inputs);

@@ -92,6 +92,7 @@ struct fdsdf_ctx {
   bool tcf = false;               // tensor-core forward (fwd_tc.cu): the tensor path, or the
                                   // hybrid path of 512-wide / skip-layer networks
   bool tcw = false;               // tensor-core weight gradient (wgrad_tc.cu): ditto
+  bool wgrad3 = false;            // FDSDF_CREATE_WGRAD_BF16X3: the weight gradient's 3-product form
   unsigned char* fimg = nullptr;  // packed forward weight image
   unsigned char* bimg = nullptr;  // packed backward (W^T) weight image
   float* cinfo = nullptr;    // [max_centers][16]
@@ -283,6 +284,11 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     // actv layouts)
     c->tcf = c->tc || (!(flags & FDSDF_CREATE_FFMA) && c->mpad >= 128 && tc_fwd_supported(c->mpad));
     c->tcw = c->tcf && wgrad_tc_supported(c->mpad);
+    c->wgrad3 = (flags & FDSDF_CREATE_WGRAD_BF16X3) != 0;
+    if (c->wgrad3 && !c->tcw) {  // only the tensor-core weight gradient has the 3-product form
+      delete c;
+      return (flags & FDSDF_CREATE_FFMA) ? FDSDF_E_INVALID : FDSDF_E_UNSUPPORTED;
+    }
   }
   c->P = fdsdf_spec_num_params(spec);
   for (int l = 0; l < c->L; ++l) {
@@ -676,7 +682,7 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   w.first_layer = 1;
   if (c->ngemm > 0)
     e = run_slot(c, FDSDF_KSLOT_WGRAD, strm, [&] {
-      return c->tcw ? launch_wgrad_tc(w, c->ngemm, strm) : launch_wgrad(w, c->ngemm, strm);
+      return c->tcw ? launch_wgrad_tc(w, c->ngemm, c->wgrad3, strm) : launch_wgrad(w, c->ngemm, strm);
     });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "wgrad_kernel"));
 

@@ -142,7 +142,7 @@ int fwd_tc2_tile_centres(int mode);                 // 32 (mode 1) / 16 (mode 2)
 cudaError_t launch_bwd_tc(const BwdArgs& a, int grid, cudaStream_t st);
 int bwd_tc_tile_centres();                          // 8
 int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
-cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, cudaStream_t st);
+cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, bool bf16x3, cudaStream_t st);
 int wgrad_tc_splits(int nsm, int64_t rows, int mpad);  // split-K factor of the tensor wgrad
 bool wgrad_tc_supported(int mpad);                      // MPAD 128 / 256 / 512
 // training iteration (train.cu)

@@ -21,6 +21,9 @@
 
 namespace fdsdf {
 
+// NPROD: bf16 piece products per MAC -- 6 = bf16x6 (fp32-accurate, the default);
+// 3 = a0 b0 + a0 b1 + a1 b0 (FDSDF_CREATE_WGRAD_BF16X3: each product to ~3 * 2^-16 relative; the
+// third pieces are neither split nor stored)
 template <int MPAD>
 struct WtcCfg {
   static constexpr int BW = MPAD > 256 ? 256 : MPAD;  // output block edge
@@ -48,9 +51,12 @@ int wgrad_tc_splits(int nsm, int64_t rows, int mpad) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, nsm / nb2), chunks));
 }
 
-template <int MPAD>
+template <int MPAD, int NPROD>
 __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const WgradArgs a) {
+  static_assert(NPROD == 6 || NPROD == 3, "bf16x6 or the three leading products");
   using C = WtcCfg<MPAD>;
+  constexpr int Q0 = 6 - NPROD;       // products q0..5 of tc::prod_a / prod_b (smallest first)
+  constexpr int NPC = NPROD == 6 ? 3 : 2;  // pieces staged per operand
   constexpr int JC = C::JC, MH = C::MH, NST = C::NST, BW = C::BW, NB = C::NB;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -101,13 +107,13 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
 #pragma unroll
             for (int h = 0; h < MH; ++h)
 #pragma unroll
-              for (int q = 0; q < 6; ++q) {
+              for (int q = Q0; q < 6; ++q) {
                 const uint64_t ad = tc::sdesc_sw128_mn(da + tc::prod_a(q) * C::PIECE + ks * 2 * C::KSTRIDE +
                                                            h * 2 * 1024,
                                                        1024, C::KSTRIDE);
                 const uint64_t bd =
                     tc::sdesc_sw128_mn(aa + tc::prod_b(q) * C::PIECE + ks * 2 * C::KSTRIDE, 1024, C::KSTRIDE);
-                tc::mma_bf16(tbase + h * BW, ad, bd, idesc, (ch | ks | q) != 0 ? 1u : 0u);
+                tc::mma_bf16(tbase + h * BW, ad, bd, idesc, (ch | ks | (q - Q0)) != 0 ? 1u : 0u);
               }
           tc::mma_commit(&sempty[s]);
         }
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
           tc::split3x2(av[q].x, av[q].y, a01);
           tc::split3x2(av[q].z, av[q].w, a23);
 #pragma unroll
-          for (int p = 0; p < 3; ++p) {
+          for (int p = 0; p < NPC; ++p) {
             *reinterpret_cast<uint2*>(dst + p * C::PIECE + off) = make_uint2(d01[p], d23[p]);
             *reinterpret_cast<uint2*>(dst + C::OPER + p * C::PIECE + off) = make_uint2(a01[p], a23[p]);
           }
@@ -197,21 +203,27 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
   if (warp == 0) tc::tmem_dealloc(tbase, C::TCOLS);
 }
 
-template <int MPAD>
+template <int MPAD, int NPROD>
 static cudaError_t launch_wgrad_tc_t(const WgradArgs& a, int nglayers, cudaStream_t st) {
   using C = WtcCfg<MPAD>;
-  cudaError_t e = cudaFuncSetAttribute(wgrad_tc_kernel<MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  cudaError_t e =
+      cudaFuncSetAttribute(wgrad_tc_kernel<MPAD, NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
   if (e != cudaSuccess) return e;
-  wgrad_tc_kernel<MPAD><<<dim3(a.nsplit * C::NB * C::NB, nglayers), C::NTHR, C::BYTES, st>>>(a);
+  wgrad_tc_kernel<MPAD, NPROD><<<dim3(a.nsplit * C::NB * C::NB, nglayers), C::NTHR, C::BYTES, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, cudaStream_t st) {
-  if (nglayers <= 0) return cudaSuccess;
-  if (a.mpad == 512) return launch_wgrad_tc_t<512>(a, nglayers, st);
-  if (a.mpad == 256) return launch_wgrad_tc_t<256>(a, nglayers, st);
-  if (a.mpad == 128) return launch_wgrad_tc_t<128>(a, nglayers, st);
+template <int NPROD>
+static cudaError_t launch_wgrad_tc_p(const WgradArgs& a, int nglayers, cudaStream_t st) {
+  if (a.mpad == 512) return launch_wgrad_tc_t<512, NPROD>(a, nglayers, st);
+  if (a.mpad == 256) return launch_wgrad_tc_t<256, NPROD>(a, nglayers, st);
+  if (a.mpad == 128) return launch_wgrad_tc_t<128, NPROD>(a, nglayers, st);
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, bool bf16x3, cudaStream_t st) {
+  if (nglayers <= 0) return cudaSuccess;
+  return bf16x3 ? launch_wgrad_tc_p<3>(a, nglayers, st) : launch_wgrad_tc_p<6>(a, nglayers, st);
 }
 
 }  // namespace fdsdf

@@ -22,7 +22,7 @@ DENOM = {"paper": 0, "one": 1, "grad": 2}
 KIND = {"ncr": 0, "nsh": 1}
 FD_FORM = {"abs": 0, "square": 1}
 STEP_ACCUMULATE, STEP_ALLREDUCE = 1, 2
-CREATE_EVAL_ONLY, CREATE_FFMA, CREATE_TENSOR = 1, 2, 4
+CREATE_EVAL_ONLY, CREATE_FFMA, CREATE_TENSOR, CREATE_WGRAD_BF16X3 = 1, 2, 4, 8
 PATH = {0: "ffma", 1: "tensor", 2: "hybrid"}
 FLAG_NONFINITE_INPUT, FLAG_NONFINITE_LOSS, FLAG_ALL_FD_SKIPPED, FLAG_NONFINITE_GRAD = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_EMPTY", 3: "E_CUDA", 4: "E_NCCL", 5: "E_NOMEM",
@@ -168,11 +168,13 @@ def fdsdf_spec_num_params(spec: dict) -> int:
 
 
 def fdsdf_create(spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False,
-                 path: str | None = None):
-    """path: None (library default: "tensor" where supported, else "hybrid"), "ffma" or "tensor"."""
+                 path: str | None = None, wgrad_bf16x3: bool = False):
+    """path: None (library default: "tensor" where supported, else "hybrid"), "ffma" or "tensor";
+    wgrad_bf16x3: FDSDF_CREATE_WGRAD_BF16X3 (include/fdsdf.h)."""
     s = make_spec(spec)
     h = C.c_void_p()
     flags = (CREATE_EVAL_ONLY if eval_only else 0) | {None: 0, "ffma": CREATE_FFMA, "tensor": CREATE_TENSOR}[path]
+    flags |= CREATE_WGRAD_BF16X3 if wgrad_bf16x3 else 0
     _check(lib().fdsdf_create(C.byref(s), int(device), int(max_centers), flags, C.byref(h)))
     return h
 
@@ -282,11 +284,11 @@ class FDSDF:
     """A context bound to one device: eval() / step() on torch CUDA tensors."""
 
     def __init__(self, spec: dict, device: int = 0, max_centers: int = 1 << 16, eval_only: bool = False,
-                 path: str | None = None):
+                 path: str | None = None, wgrad_bf16x3: bool = False):
         import torch
         self.spec = spec
         self.device = torch.device("cuda", device)
-        self.ctx = fdsdf_create(spec, device, max_centers, eval_only, path)
+        self.ctx = fdsdf_create(spec, device, max_centers, eval_only, path, wgrad_bf16x3)
         self.path = PATH[int(lib().fdsdf_path(self.ctx))]
         self.P = int(lib().fdsdf_num_params(self.ctx))
         self.max_centers = int(max_centers)
