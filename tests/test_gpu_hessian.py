@@ -25,13 +25,19 @@ def _built():
 
 def _model(spec, n, path=None, eval_only=True):
     from paper_2511_08980_b200 import FDSDF
+    if path == "tensor" and (spec.get("skip_at", -1) >= 0 or max(spec["widths"][1:-1]) > 256):
+        m = FDSDF(spec, 0, max_centers=n, eval_only=eval_only)  # the hybrid path's tensor forward
+        assert m.path == "hybrid", m.path
+        return m
     return FDSDF(spec, 0, max_centers=n, eval_only=eval_only, path=path)
 
 
 # (config, surface rows, uniform rows, h): C1 softplus (MPAD 128) and C2 SIREN (MPAD 256) at
-# their h, plus C2 at the h = 1e-2 of the entry gate; the centre counts leave ragged tiles
+# their h, plus C2 at the h = 1e-2 of the entry gate; C3 (skip layer, MPAD 512: the hybrid path
+# under "tensor"); the centre counts leave ragged tiles
 @pytest.mark.parametrize("name,ns,nu,h,eval_only", [("c1", 300, 211, None, True), ("c2", 333, 300, None, True),
-                                                     ("c2", 200, 177, 1e-2, True), ("c2", 150, 121, None, False)])
+                                                     ("c2", 200, 177, 1e-2, True), ("c2", 150, 121, None, False),
+                                                     ("c3", 60, 51, None, True), ("c3", 50, 41, None, False)])
 @pytest.mark.parametrize("path", ["ffma", "tensor"])
 def test_hessian_parity(name, ns, nu, h, eval_only, path):
     """eval_only = False: a training context, whose centre pre-activations live in the step
