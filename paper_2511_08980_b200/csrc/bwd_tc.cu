@@ -117,6 +117,9 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
 #pragma unroll
     for (int l = 0; l < MAXL; ++l) r_db[l] = 0.f;
     float r_dWL = 0.f, r_dbL = 0.f, r_dW0[3] = {0.f, 0.f, 0.f};
+    // db of the top layer, accumulated by top_centre in a register (r_db, indexed by the
+    // runtime layer, lives in local memory); added to r_db[ltop] once at the end
+    float r_dbtop = 0.f;
     uint32_t nd = 0;
     PhaseTimer ptimer;
     ptimer.start();
@@ -164,18 +167,27 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     // delta_{L-2} needs no MMA.  Writes delta to a.del and accumulates db_{L-2} and dW_{L-1}.
     const int ltop = L - 2;
     const bool pipe_top = BWD_TC_PIPE_TOP && ngemm > 0;
-    auto top_centre = [&](int64_t tl, int i, const float* sdsT) {
+    // this thread's stored pre-activations of top-layer centre i of tile tl (zero if none)
+    auto top_load = [&](int64_t tl, int i, float4 (&zg)[ZG]) {
+      const int64_t c = tl * CT + eg + EG * i;
+#pragma unroll
+      for (int g = 0; g < ZG; ++g) zg[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (tl >= a.ntiles || c >= a.n || m >= net.width[ltop + 1]) return;
+      const float4* zq = reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + ltop) * NCOLF * MPAD) + m;
+#pragma unroll
+      for (int g = 0; g < ZG; ++g) zg[g] = __ldg(zq + g * MPAD);
+    };
+    auto top_centre = [&](int64_t tl, int i, const float* sdsT, const float4 (&zg)[ZG]) {
       const int cl = eg + EG * i;
       const int64_t c = tl * CT + cl;
       if (tl >= a.ntiles || c >= a.n || m >= net.width[ltop + 1]) return;
       const float omt = net.omega[ltop];
       const float wlt = net.W[L - 1][m];
       FDSDF_ASSERT(c >= 0 && c < a.n);
-      const float4* zq = reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + ltop) * NCOLF * MPAD) + m;
       float zv[NCOLF];
 #pragma unroll
       for (int g = 0; g < ZG; ++g) {
-        const float4 v = __ldg(zq + g * MPAD);
+        const float4 v = zg[g];
         zv[4 * g] = v.x;
         zv[4 * g + 1] = v.y;
         zv[4 * g + 2] = v.z;
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       float v = 0.f;
 #pragma unroll
       for (int j = 0; j < NCOLB; ++j) v = fmaf(dL[j], pv[j], v);
-      r_db[ltop] += dl[0];
+      r_dbtop += dl[0];
       r_dWL += v;
     };
     uint32_t spar = 0;
@@ -237,9 +249,12 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         // the first GEMM's B operand: delta_{L-2} of this tile, computed during the previous
         // tile (here only for the CTA's first tile) and reloaded from a.del (this thread's writes)
         if (tile == blockIdx.x)
-          for (int i = 0; i < CPE; ++i) top_centre(tile, i, sds);
+          for (int i = 0; i < CPE; ++i) {
+            float4 zg[ZG];
+            top_load(tile, i, zg);
+            top_centre(tile, i, sds, zg);
+          }
         const bool mt = m < net.width[ltop + 1];
-        float dn[NCOLB];
         auto ldd = [&](int i, float (&d)[NCOLB]) {
           const int64_t c = c0 + eg + EG * i;
           const bool ok = i < CPE && c < a.n && mt;
@@ -247,6 +262,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
 #pragma unroll
           for (int j = 0; j < NCOLB; ++j) d[j] = ok ? dp[j * MPAD] : 0.f;
         };
+        float dn[NCOLB];
         ldd(0, dn);
 #pragma unroll 1
         for (int i = 0; i < CPE; ++i) {
@@ -270,6 +286,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         const bool mok = m < M;
         const float wl = (top && mok) ? net.W[L - 1][m] : 0.f;
         float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
+        const float db_l = r_db[l];  // local-memory read issued here, consumed after phase B
         constexpr bool CARRY = BWD_TC_CARRY;
         float c_s1[CPE], c_s2tr[CPE];  // CARRY: sigma'(z), sigma''(z) (r . t) per centre of this thread
         if (!top) prefetch_layer(tile, l - 1);  // the next pass's phase A
@@ -316,7 +333,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             float pv[NCOLB];
 #pragma unroll
             for (int j = 0; j < NCOLB; ++j) pv[j] = 0.f;
-            if (CARRY) c_s1[i] = c_s2tr[i] = 0.f;
+            float cs1 = 0.f, cs2tr = 0.f;
             if (mok && valid) {
               const typename AF::C cc = AF::centre(q.z, beta);
 #pragma unroll
@@ -329,8 +346,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                 pv[0] = AF::value(cc, beta);
                 pv[1] = AF::d1(cc, beta) * tr;
                 if (CARRY) {
-                  c_s1[i] = AF::d1(cc, beta);
-                  c_s2tr[i] = AF::d2(cc, beta) * tr;
+                  cs1 = AF::d1(cc, beta);
+                  cs2tr = AF::d2(cc, beta) * tr;
                 }
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
@@ -338,6 +355,10 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                   pv[3 + 2 * p] = t[5 * p + 1];
                 }
               }
+            }
+            if (CARRY) {
+              c_s1[i] = cs1;
+              c_s2tr[i] = cs2tr;
             }
             {
               if (valid && l <= L - 3) {
@@ -379,7 +400,11 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             bar_named(1, C::NEPI * 32);  // the next tile's seeds are in
           }
 #pragma unroll 1
-          for (int i = g; i < CPE; i += ngemm) top_centre(tile + gridDim.x, i, sds_next);
+          for (int i = g; i < CPE; i += ngemm) {
+            float4 zg[ZG];
+            top_load(tile + gridDim.x, i, zg);
+            top_centre(tile + gridDim.x, i, sds_next, zg);
+          }
         }
 #ifdef FDSDF_PHASE_TIMING
         t_top += clock64() - t_pa1;
@@ -398,6 +423,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         };
         float zn[4];
         ldz(0, zn);
+        // CARRY values of the next centre, read one centre ahead (local memory)
+        float cs1n = CARRY ? c_s1[0] : 0.f, cs2n = CARRY ? c_s2tr[0] : 0.f;
         if (!top) {
           ptimer.before_wait();
           mbar_wait(bars.dfull, nd & 1u);
@@ -412,6 +439,11 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           const bool valid = c < a.n;
           const float zc[4] = {zn[0], zn[1], zn[2], zn[3]};
           ldz(i + 1, zn);
+          const float cs1 = cs1n, cs2 = cs2n;
+          if (CARRY && i + 1 < CPE) {
+            cs1n = c_s1[i + 1];
+            cs2n = c_s2tr[i + 1];
+          }
           const float* sd = sds + cl * 20;
           float X[NCOLB];
           if (top) {
@@ -446,8 +478,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             float tr = 0.f, s1, s2tr;
             typename AF::C cc{};
             if (CARRY) {
-              s1 = c_s1[i];
-              s2tr = c_s2tr[i];
+              s1 = cs1;
+              s2tr = cs2;
             } else {
               tr = fmaf(r0, zc[1], fmaf(r1, zc[2], r2 * zc[3]));
               cc = AF::centre(zc[0], beta);
@@ -505,7 +537,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         } else if (!top) {
           tc::fence_before();
         }
-        r_db[l] += s_db;
+        r_db[l] = db_l + s_db;
         if (top) r_dWL += s_vL;
         if (l == 0) {
           r_dW0[0] += s_w0[0];
@@ -519,6 +551,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         r_dbL += v;
       }
     }
+    r_db[ltop] += r_dbtop;
     // write this thread's slots (every element of the slot is owned by exactly one thread)
     for (int l = 0; l <= L - 2; ++l) acc_db[(size_t)l * MPAD + m] = r_db[l];
     acc_dWL[m] = r_dWL;
