@@ -219,6 +219,11 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
     const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + MH * C::DH + (hh * C::EG + eg) * CPE * CPC;
     const bool pipe0 = FWD_PIPE0 && ngemm > 0;
     FDSDF_ASSERT(!FWD_PIPE0 || (MH * C::DH + (hh * C::EG + eg + 1) * CPE * CPC) <= (int)C::TCOLS);
+    // this thread's layer-0 weight row and bias (fan-in 3; constant over the kernel, loaded once
+    // instead of before every centre's layer-0 arithmetic)
+    const bool mok0 = m < net.width[1];
+    const float w0r0 = mok0 ? net.W[0][m * 3 + 0] : 0.f, w0r1 = mok0 ? net.W[0][m * 3 + 1] : 0.f,
+                w0r2 = mok0 ? net.W[0][m * 3 + 2] : 0.f, b0r = (MODE == 1 && mok0) ? net.b[0][m] : 0.f;
     // layer 0 of centre i of tile tl (centre info cis_t): pre-activations -> zf, activations ->
     // this thread's stash columns (exactly the l == 0 arithmetic of the epilogue below)
     auto layer0_centre = [&](int64_t tl, int i, const float* cis_t) {
@@ -238,9 +243,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
         }
         if (mok) {
-          const float* W0 = net.W[0];
-          const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
-          z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + net.b[0][m]);
+          const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
+          z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0r);
           t0 = om * w0;
           t1 = om * w1;
           t2 = om * w2;
@@ -267,8 +271,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         const float z0 = valid ? __ldg(zc(c, 0)) : 0.f;
         float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
         if (mok) {
-          const float* W0 = net.W[0];
-          const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+          const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
           const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
           const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
           const float hs = om * h;
@@ -375,6 +378,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         const float om = net.omega[l];
         const bool mok = m < M;
         const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
+        const float bias_l = (MODE == 1 && l > 0 && mok) ? net.b[l][m] : 0.f;  // once per layer
         // last layer: sum over this warp's 32 neurons of w_L[m] * out_j, one slot per centre
         auto reduce4 = [&](int cl, float p0, float p1, float p2, float p3) {
           float pv[4] = {wl * p0, wl * p1, wl * p2, wl * p3};
@@ -460,9 +464,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
                 if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
               }
               if (mok) {
-                const float* W0 = net.W[0];
-                const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
-                z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + net.b[0][m]);
+                const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
+                z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0r);
                 t0 = om * w0;
                 t1 = om * w1;
                 t2 = om * w2;
@@ -470,12 +473,14 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
             } else {
               float v[8];
               tc_ld_sum8<C>(taddr, (cl >> 1) * 8, v);
-              const int o = (cl & 1) * 4;
+              // centre cl's 4 columns are the half (cl & 1) of the 8 loaded (warp-uniform):
+              // register selects, not a runtime index (which would put v in local memory)
+              const bool hi = (cl & 1) != 0;
               if (mok) {
-                z = om * (v[o] + net.b[l][m]);
-                t0 = om * v[o + 1];
-                t1 = om * v[o + 2];
-                t2 = om * v[o + 3];
+                z = om * ((hi ? v[4] : v[0]) + bias_l);
+                t0 = om * (hi ? v[5] : v[1]);
+                t1 = om * (hi ? v[6] : v[2]);
+                t2 = om * (hi ? v[7] : v[3]);
               }
             }
             if (valid) {
@@ -507,8 +512,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
             float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
             if (l == 0) {
               if (mok) {
-                const float* W0 = net.W[0];
-                const float w0 = W0[m * 3 + 0], w1 = W0[m * 3 + 1], w2 = W0[m * 3 + 2];
+                const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
                 const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
                 const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
                 const float hs = om * h;
