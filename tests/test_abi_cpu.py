@@ -129,3 +129,33 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b|#include.*oracle", txt, flags=re.M), f
+
+
+def test_header_constants_match_binding():
+    """Every enum value and flag the binding hard-codes equals the header's (include/fdsdf.h),
+    parsed from the header text (no compiler, no GPU)."""
+    import re
+    from paper_2511_08980_b200 import fdsdf as F
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "fdsdf.h")).read()
+    vals = {k: int(v) for k, v in re.findall(r"\b(FDSDF_[A-Z0-9_]+)\s*=\s*(\d+)u?\b", hdr)}
+    mx = re.search(r"#define\s+FDSDF_MAX_LINEAR\s+(\d+)", hdr)
+    assert mx and int(mx.group(1)) == F.MAX_LINEAR
+    assert {"softplus": vals["FDSDF_ACT_SOFTPLUS"], "sine": vals["FDSDF_ACT_SINE"]} == F.ACT
+    assert (vals["FDSDF_FRAME_RANDOM"], vals["FDSDF_FRAME_GIVEN"]) == (F.FRAME_RANDOM, F.FRAME_GIVEN)
+    assert {k.lower(): vals["FDSDF_DENOM_" + k] for k in ("PAPER", "ONE", "GRAD")} == F.DENOM
+    assert {"ncr": vals["FDSDF_LOSS_NCR"], "nsh": vals["FDSDF_LOSS_NSH"]} == F.KIND
+    assert {"abs": vals["FDSDF_FD_ABS"], "square": vals["FDSDF_FD_SQUARE"]} == F.FD_FORM
+    assert (vals["FDSDF_STEP_ACCUMULATE"], vals["FDSDF_STEP_ALLREDUCE"]) == (F.STEP_ACCUMULATE, F.STEP_ALLREDUCE)
+    assert (vals["FDSDF_CREATE_EVAL_ONLY"], vals["FDSDF_CREATE_FFMA"], vals["FDSDF_CREATE_TENSOR"],
+            vals["FDSDF_CREATE_WGRAD_BF16X3"]) == (F.CREATE_EVAL_ONLY, F.CREATE_FFMA, F.CREATE_TENSOR,
+                                                   F.CREATE_WGRAD_BF16X3)
+    assert {vals["FDSDF_PATH_" + k.upper()]: k for k in F.PATH.values()} == F.PATH
+    assert (vals["FDSDF_FLAG_NONFINITE_INPUT"], vals["FDSDF_FLAG_NONFINITE_LOSS"], vals["FDSDF_FLAG_ALL_FD_SKIPPED"],
+            vals["FDSDF_FLAG_NONFINITE_GRAD"]) == (F.FLAG_NONFINITE_INPUT, F.FLAG_NONFINITE_LOSS,
+                                                   F.FLAG_ALL_FD_SKIPPED, F.FLAG_NONFINITE_GRAD)
+    assert {vals["FDSDF_" + v]: v for v in F.STATUS.values()} == F.STATUS
+    slots = {k: v for k, v in vals.items() if k.startswith("FDSDF_KSLOT_") and k != "FDSDF_KSLOT_NUM"}
+    assert sorted(slots.values()) == list(range(len(F.KSLOTS)))
+    assert all(F.KSLOTS[v] == k[len("FDSDF_KSLOT_"):].lower() for k, v in slots.items()), slots
+    if "FDSDF_KSLOT_NUM" in vals:
+        assert vals["FDSDF_KSLOT_NUM"] == len(F.KSLOTS)
