@@ -215,6 +215,19 @@ fdsdf_status fdsdf_step(fdsdf_ctx* ctx, const float* d_params, const float* d_x,
                         const fdsdf_stencil* st, const fdsdf_loss* ls, float* d_grad,
                         double* d_loss, uint32_t flags, void* stream);
 
+/* The same step with HOST buffers (the end-to-end call): h_x [n][3] fp32 host memory (pinned
+ * for an asynchronous copy; pageable memory works but the copy then blocks the host) is copied
+ * into the context's device staging buffer, the step runs into the context's own gradient /
+ * loss buffers, and both are copied back to h_grad [P] fp32 and h_loss [8] fp64 (host
+ * memory) -- all enqueued on `stream`; the caller synchronises it before reading h_grad /
+ * h_loss.  d_params stays device memory (the model state lives on the GPU).  With
+ * FDSDF_STEP_ACCUMULATE the context's gradient buffer (zero at create) accumulates across
+ * calls and h_grad receives the running sum.  Errors: as fdsdf_step (validated before
+ * anything is enqueued); h_x / h_grad / h_loss NULL -> FDSDF_E_INVALID. */
+fdsdf_status fdsdf_step_host(fdsdf_ctx* ctx, const float* d_params, const float* h_x, int64_t n,
+                             const fdsdf_stencil* st, const fdsdf_loss* ls, float* h_grad,
+                             double* h_loss, uint32_t flags, void* stream);
+
 /* Data-parallel plumbing: rank 0 calls fdsdf_comm_unique_id, the caller
  * broadcasts the 128 bytes (e.g. through its torch process group), every rank calls
  * fdsdf_comm_init.  NCCL is loaded at run time (libnccl.so.2); missing -> FDSDF_E_NCCL.

@@ -78,6 +78,9 @@ struct fdsdf_ctx {
   float* wt = nullptr;
   float* wb = nullptr;
   float* zf = nullptr;       // step workspace
+  float* xstage = nullptr;   // fdsdf_step_host: device copy of the points [max_centers][3]
+  float* hgrad = nullptr;    //                  the gradient [P] (accumulates with ACCUMULATE)
+  double* hloss = nullptr;   //                  the loss [8]
   float* zscr = nullptr;     // eval scratch (per CTA)
   float* seed = nullptr;
   double* lossp = nullptr;
@@ -226,7 +229,8 @@ void fdsdf_destroy(fdsdf_ctx* c) {
   }
   for (cudaEvent_t e : c->spare) cudaEventDestroy(e);
   void* bufs[] = {c->wt,   c->wb,   c->zf,     c->zscr,   c->seed,  c->lossp, c->del, c->actv,
-                  c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev, c->bimg, c->hframes, c->htmp};
+                  c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev, c->bimg, c->hframes, c->htmp,
+                  c->xstage, c->hgrad, c->hloss};
   for (void* b : bufs)
     if (b) cudaFree(b);
   cudaSetDevice(prev);
@@ -344,6 +348,10 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
   ok = ok && alloc((void**)&c->htmp, (size_t)max_centers * 3 * sizeof(float));
   if (ok && !c->eval_only) {
     ok = ok && alloc((void**)&c->zf, (size_t)max_centers * c->nh * NCOLF * mp * sizeof(float));
+    ok = ok && alloc((void**)&c->xstage, (size_t)max_centers * 3 * sizeof(float));
+    ok = ok && alloc((void**)&c->hgrad, (size_t)c->P * sizeof(float));
+    ok = ok && alloc((void**)&c->hloss, 8 * sizeof(double));
+    if (ok) ok = cudaMemset(c->hgrad, 0, (size_t)c->P * sizeof(float)) == cudaSuccess;
     ok = ok && alloc((void**)&c->seed, (size_t)max_centers * NSEED * sizeof(float));
     ok = ok && alloc((void**)&c->del, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
     ok = ok && alloc((void**)&c->actv, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
@@ -581,8 +589,14 @@ fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* c, const float* d_params, const float
   return FDSDF_OK;
 }
 
-fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
-                        const fdsdf_loss* ls, float* d_grad, double* d_loss, uint32_t flags, void* stream) {
+}  // extern "C"
+
+// fdsdf_step, and fdsdf_step_host (h_x != nullptr: the points are copied host -> d_x first;
+// h_grad / h_loss != nullptr: the results are copied back after the step), all enqueued on the
+// caller's stream after validation, so an error still enqueues nothing
+static fdsdf_status step_impl(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
+                              const fdsdf_loss* ls, float* d_grad, double* d_loss, uint32_t flags, void* stream,
+                              const float* h_x, float* h_grad, double* h_loss) {
   fdsdf_status s = check_common(c, d_params, d_x, n, st);
   if (s != FDSDF_OK) return s;
   if (c->eval_only) return fail(c, FDSDF_E_INVALID, "context created EVAL_ONLY");
@@ -614,6 +628,10 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   fill_net(c, d_params);
   c->launches = 0;
   cudaError_t e = cudaSuccess;
+  if (h_x) {
+    e = cudaMemcpyAsync(const_cast<float*>(d_x), h_x, (size_t)n * 3 * sizeof(float), cudaMemcpyHostToDevice, strm);
+    if (e != cudaSuccess) return done(cuda_fail(c, e, "host -> device copy of the points"));
+  }
   if (c->tcf && c->ngemm > 0)  // tensor forward image (and, on the tensor path, the backward's)
     e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, c->bimg, strm); });
   if (e == cudaSuccess && !c->tc && c->ngemm > 0)  // FFMA backward / weight gradient
@@ -716,7 +734,27 @@ fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, i
     });
     if (r1 || r2 || r3) return done(fail(c, FDSDF_E_NCCL, "ncclAllReduce failed"));
   }
+  if (h_grad) {
+    e = cudaMemcpyAsync(h_grad, d_grad, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, strm);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_loss, d_loss, 8 * sizeof(double), cudaMemcpyDeviceToHost, strm);
+    if (e != cudaSuccess) return done(cuda_fail(c, e, "device -> host copy of the results"));
+  }
   return done(FDSDF_OK);
+}
+
+extern "C" {
+
+fdsdf_status fdsdf_step(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
+                        const fdsdf_loss* ls, float* d_grad, double* d_loss, uint32_t flags, void* stream) {
+  return step_impl(c, d_params, d_x, n, st, ls, d_grad, d_loss, flags, stream, nullptr, nullptr, nullptr);
+}
+
+fdsdf_status fdsdf_step_host(fdsdf_ctx* c, const float* d_params, const float* h_x, int64_t n, const fdsdf_stencil* st,
+                             const fdsdf_loss* ls, float* h_grad, double* h_loss, uint32_t flags, void* stream) {
+  if (!c) return FDSDF_E_INVALID;
+  if (c->eval_only) return fail(c, FDSDF_E_INVALID, "context created EVAL_ONLY");
+  if (!h_x || !h_grad || !h_loss) return fail(c, FDSDF_E_INVALID, "null pointer argument");
+  return step_impl(c, d_params, c->xstage, n, st, ls, c->hgrad, c->hloss, flags, stream, h_x, h_grad, h_loss);
 }
 
 fdsdf_status fdsdf_sample(fdsdf_ctx* c, const float* d_pool, int64_t n_pool, int64_t n_pick, float box_half,

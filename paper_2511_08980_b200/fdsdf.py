@@ -88,6 +88,8 @@ def lib():
         L.fdsdf_eval_hessian.restype = C.c_int
         L.fdsdf_step.argtypes = [vp, vp, vp, i64, C.POINTER(Stencil), C.POINTER(Loss), vp, vp, u32, vp]
         L.fdsdf_step.restype = C.c_int
+        L.fdsdf_step_host.argtypes = [vp, vp, vp, i64, C.POINTER(Stencil), C.POINTER(Loss), vp, vp, u32, vp]
+        L.fdsdf_step_host.restype = C.c_int
         L.fdsdf_comm_unique_id.argtypes = [C.c_char_p]
         L.fdsdf_comm_unique_id.restype = C.c_int
         L.fdsdf_comm_init.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
@@ -224,6 +226,18 @@ def fdsdf_eval(ctx, params, x, n, stencil: Stencil, out: EvalOut, stream=None):
 def fdsdf_step(ctx, params, x, n, stencil: Stencil, loss: Loss, grad, loss_out, flags=0, stream=None):
     _check(lib().fdsdf_step(ctx, _ptr(params), _ptr(x), int(n), C.byref(stencil), C.byref(loss),
                             _ptr(grad), _ptr(loss_out), int(flags), _stream(stream)), ctx)
+
+
+def fdsdf_step_host(ctx, params, x_host, n, stencil: Stencil, loss: Loss, grad_host, loss_host, flags=0,
+                    stream=None):
+    """fdsdf_step with HOST buffers (include/fdsdf.h): x_host [n,3] fp32, grad_host [P] fp32 and
+    loss_host [8] fp64 are CPU tensors (pinned for asynchronous copies); params is a CUDA tensor.
+    Synchronise the stream before reading grad_host / loss_host."""
+    for t in (x_host, grad_host, loss_host):
+        if getattr(t, "is_cuda", False):
+            raise ValueError("fdsdf_step_host takes host (CPU) buffers for x, grad and loss")
+    _check(lib().fdsdf_step_host(ctx, _ptr(params), _ptr(x_host), int(n), C.byref(stencil), C.byref(loss),
+                                 _ptr(grad_host), _ptr(loss_host), int(flags), _stream(stream)), ctx)
 
 
 def fdsdf_sample(ctx, pool, n_pick, box_half, n_uniform, seed, iteration, out, stream=None):
