@@ -167,6 +167,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
     // delta_{L-2} needs no MMA.  Writes delta to a.del and accumulates db_{L-2} and dW_{L-1}.
     const int ltop = L - 2;
     const bool pipe_top = BWD_TC_PIPE_TOP && ngemm > 0;
+    // this thread's last-layer weight (fan-out 1), loaded once instead of per top-layer centre
+    const float wlast = m < net.width[ltop + 1] ? net.W[L - 1][m] : 0.f;
     // this thread's stored pre-activations of top-layer centre i of tile tl (zero if none)
     auto top_load = [&](int64_t tl, int i, float4 (&zg)[ZG]) {
       const int64_t c = tl * CT + eg + EG * i;
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       const int64_t c = tl * CT + cl;
       if (tl >= a.ntiles || c >= a.n || m >= net.width[ltop + 1]) return;
       const float omt = net.omega[ltop];
-      const float wlt = net.W[L - 1][m];
+      const float wlt = wlast;
       FDSDF_ASSERT(c >= 0 && c < a.n);
       float zv[NCOLF];
 #pragma unroll
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         const int M = net.width[l + 1];
         const float om = net.omega[l];
         const bool mok = m < M;
-        const float wl = (top && mok) ? net.W[L - 1][m] : 0.f;
+        const float wl = (top && mok) ? wlast : 0.f;
         float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
         const float db_l = r_db[l];  // local-memory read issued here, consumed after phase B
         constexpr bool CARRY = BWD_TC_CARRY;
