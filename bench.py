@@ -48,8 +48,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the train-iteration and eval measurements")
-    ap.add_argument("--eval-sweep", action="store_true",
-                    help="C5e: fdsdf_eval throughput for 1e4 .. 1e7 centres (rank 0, adds 'eval_sweep')")
+    ap.add_argument("--no-eval-sweep", action="store_true",
+                    help="skip C5e: fdsdf_eval throughput for 1e4 .. 1e7 centres (N = 1 only, 'eval_sweep')")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the C5 block (BASELINE configs[4]: 200k centres per GPU, every N)")
     ap.add_argument("--path", choices=("default", "ffma", "tensor"), default="default",
                     help="contraction path of the library (default: the library's choice)")
     return ap.parse_args()
@@ -64,6 +66,18 @@ def measured_bf16_peak():
         return v, "measured (MEASURED_PEAKS.json, burst)"
     except (OSError, ValueError, KeyError):
         return 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def source_hash():
+    """sha256 (16 hex) over the library's CUDA sources: tags the ncu DRAM capture with the build"""
+    import hashlib
+    d = os.path.join(ROOT, "paper_2511_08980_b200", "csrc")
+    hs = hashlib.sha256()
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh")):
+            hs.update(f.encode())
+            hs.update(open(os.path.join(d, f), "rb").read())
+    return hs.hexdigest()[:16]
 
 
 def p_mm(spec):
@@ -133,50 +147,58 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- oracle (CPU) arm
 
 
-def oracle_rate(cfg, budget_s=10.0, max_reps=3):
-    """Time the fp64 oracle (as it stands) on the workload: full step(s) over all centres,
-    repeated until ~budget_s.  Returns (stencil points/s, seconds per step, cores, sample)."""
-    import torch
-    from oracle import oracle_step
-    x = cfg["x"]
+def _oracle_sample(cfg, nsub):
+    """the first rows of each role in the workload's proportion (surface, then uniform)"""
+    x, ns = cfg["x"], cfg["n_surface"]
     n = len(x)
-    reps, t_tot = 0, 0.0
-    while reps < max_reps and (reps == 0 or t_tot < budget_s):
+    s = min(ns, max(1, round(nsub * ns / n)))
+    u = min(n - ns, nsub - s)
+    return np.concatenate([x[:s], x[ns:ns + u]]), s, u
+
+
+def oracle_rate(cfg, budget_s=15.0):
+    """cpu_baseline: the plain single-threaded fp64 C oracle (oracle/c/fdsdf_oracle.c) as it
+    stands, on ONE host core, over a bounded sample of the workload (~budget_s of CPU work,
+    sized by a timed probe).  Returns (stencil points/s, seconds per centre, cores, sample)."""
+    from oracle.c_oracle import c_oracle_step
+
+    def one(nsub):
+        xs, s, u = _oracle_sample(cfg, nsub)
         t0 = time.perf_counter()
-        oracle_step(cfg["spec"], cfg["params"], x, cfg["n_surface"], cfg["h"], cfg["loss"],
-                    frame_seed=cfg["frame_seed"], index_offset=cfg["index_offset"],
-                    counts=cfg["counts"], need_grad=True)
-        t_tot += time.perf_counter() - t0
-        reps += 1
-    per = t_tot / reps
-    return 9.0 * n / per, per, torch.get_num_threads(), f"{reps} full step(s) of {n} centres (all of the rank-0 shard)"
+        c_oracle_step(cfg["spec"], cfg["params"], xs, s, cfg["h"], cfg["loss"], frame_seed=cfg["frame_seed"],
+                      counts=cfg["counts"], need_grad=True, threads=1)
+        return time.perf_counter() - t0, s, u
+
+    dt, _, _ = one(16)
+    nsub = int(min(len(cfg["x"]), max(16, budget_s / (dt / 16))))
+    dt, s, u = one(nsub)
+    return 9.0 * (s + u) / dt, dt / (s + u), 1, (f"one full oracle step (forward, FD epilogue, loss, weight "
+                                                 f"gradient) over {s + u} of the workload's {len(cfg['x'])} centres "
+                                                 f"({s} surface + {u} uniform rows), single-threaded C, fp64")
 
 
 def run_reference(args):
-    """The reference arm: the fp64 oracle as it stands, on this box's host cores (rank 0 alone;
-    under torchrun the other ranks exit 0 at once, so rank 0 takes every core of its affinity
-    mask instead of torchrun's OMP_NUM_THREADS=1).  Each step is one oracle step over a sample
-    of the workload's centres (surface and uniform rows in the workload's proportion), sized
-    from a timed probe so that the whole --warmup + --steps run stays within ~3 minutes."""
+    """The reference arm: the plain fp64 C oracle as it stands, on this box's host cores (rank 0
+    alone; under torchrun the other ranks exit 0 at once).  The oracle itself is single-threaded;
+    the harness runs it on `cores` contiguous row chunks in parallel threads and adds the chunks
+    in order.  Each step is one oracle step over a sample of the workload's centres (surface and
+    uniform rows in the workload's proportion), sized from a timed probe so that the whole
+    --warmup + --steps run stays within ~3 minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import torch
-    torch.set_num_threads(max(1, len(os.sched_getaffinity(0))))
+    from oracle.c_oracle import c_oracle_step
+    cores = max(1, len(os.sched_getaffinity(0)))
     cfg = workload(args.config, 0, 1)
-    from oracle import oracle_step
-    x, ns = cfg["x"], cfg["n_surface"]
-    n = len(x)
+    n = len(cfg["x"])
 
     def one(nsub):
-        s = min(ns, max(1, round(nsub * ns / n)))
-        u = min(n - ns, nsub - s)
-        xs = np.concatenate([x[:s], x[ns:ns + u]])
-        oracle_step(cfg["spec"], cfg["params"], xs, s, cfg["h"], cfg["loss"],
-                    frame_seed=cfg["frame_seed"], counts=cfg["counts"], need_grad=True)
+        xs, s, u = _oracle_sample(cfg, nsub)
+        c_oracle_step(cfg["spec"], cfg["params"], xs, s, cfg["h"], cfg["loss"], frame_seed=cfg["frame_seed"],
+                      counts=cfg["counts"], need_grad=True, threads=cores)
         return s, u
 
-    probe = min(n, 2000)
+    probe = min(n, 8 * cores)
     t0 = time.perf_counter()
     one(probe)
     per_centre = (time.perf_counter() - t0) / probe
@@ -194,9 +216,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "steps_per_s": 1.0 / per,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfg["config_json"],
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
-                         "sample": f"each step = one full oracle step (forward, FD epilogue, loss, weight gradient) "
-                                   f"over {s + u} of the workload's {n} centres ({s} surface + {u} uniform rows)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"each step = one full step of the plain fp64 C oracle (forward, FD epilogue, "
+                                   f"loss, weight gradient) over {s + u} of the workload's {n} centres ({s} surface "
+                                   f"+ {u} uniform rows), as {cores} single-threaded row chunks in parallel"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -291,7 +314,7 @@ def measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank
     ms_h = _event_ms(stream, lambda i: model.eval_hessian(pdev, x, cfg["h"], H=Hb, stream=stream), args.steps, flush)
     out["eval_hessian"] = {"ms": ms_h, "centres": n, "stencil_points_per_s": 19.0 * n / (ms_h * 1e-3),
                            "outputs": "world-axis 3x3 FD Hessian (19-point stencil) as 3 axis-frame stencil passes"}
-    if args.eval_sweep and rank == 0:
+    if not args.no_eval_sweep and world == 1:
         from harness import csg_surface as cs, uniform_box
         sweep = []
         nmax = 10_000_000
@@ -313,8 +336,98 @@ def measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank
     return out
 
 
+def measure_c5(args, spec, local, rank, world, dev, stream, flush, barrier):
+    """BASELINE.json configs[4] at this N: 200k centres per GPU (100k CSG surface + 100k uniform,
+    rank-seeded shards, global index offsets and counts), the full step with the in-step NCCL
+    allreduce, event-timed, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_08980_b200 import FDSDF
+    from paper_2511_08980_b200 import fdsdf as F
+    from harness import frame_seed
+    c = workload("c5", rank, world)
+    n = len(c["x"])
+    m = FDSDF(spec, local, max_centers=n, path=None if args.path == "default" else args.path)
+    coll = setup_comm(m, world, rank, dev) if world > 1 else None
+    lib_ar = coll is not None and coll.startswith("fdsdf")
+    x = torch.from_numpy(c["x"]).to(dev)
+    p = torch.from_numpy(c["params"]).to(dev)
+    g = torch.zeros(m.P, device=dev, dtype=torch.float32)
+    lo = torch.zeros(8, device=dev, dtype=torch.float64)
+    lc = c["loss"]
+    ls = F.make_loss(lc, c["counts"])
+
+    def step(i):
+        st = F.make_stencil(c["h"], c["n_surface"], frame_seed(4, i), c["index_offset"], None, lc["eps_grad"],
+                            lc["denom"], lc["denom_pow"])
+        F.fdsdf_step(m.ctx, p, x, n, st, ls, g, lo, F.STEP_ALLREDUCE if lib_ar else 0, stream)
+        if world > 1 and not lib_ar:
+            dist.all_reduce(g)
+            dist.all_reduce(lo)
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    k = max(3, min(args.steps, 10))
+    ms = _event_ms(stream, lambda i: step(args.warmup + i), k, flush)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ok = bool(np.isfinite(lo.cpu().numpy()[4]))
+    m.close()
+    return {"workload": c["config_json"]["workload"], "centres_per_gpu": n, "global_centres": n * world,
+            "steps": k, "ms_per_step": ms, "steps_per_s": 1e3 / ms, "value": 9.0 * n * world / (ms * 1e-3),
+            "unit": UNIT, "finite_loss": ok, "collective": coll}
+
+
+def setup_comm(model, world, rank, dev):
+    """The library's own NCCL communicator (the in-step allreduce of FDSDF_STEP_ALLREDUCE): rank 0
+    draws the unique id, torch.distributed broadcasts it.  Should loading / initialising it fail
+    on a box, fall back to torch.distributed's NCCL all-reduce of the same two buffers on the
+    same stream (reported in the JSON line)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_08980_b200 import fdsdf as F
+    ok = 1
+    try:
+        uid = F.fdsdf_comm_unique_id() if rank == 0 else bytes(128)
+    except F.FdsdfError:
+        uid, ok = bytes(128), 0
+    t = torch.tensor(list(uid) + [ok], dtype=torch.uint8, device=dev)
+    dist.broadcast(t, 0)
+    ok = int(t[128].item())
+    if ok:
+        try:
+            model.comm_init(bytes(t[:128].cpu().tolist()), rank, world)
+        except F.FdsdfError as e:
+            print(f"[bench] rank {rank}: fdsdf_comm_init failed ({e})", file=sys.stderr)
+            ok = 0
+    okt = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    return "fdsdf NCCL (in-step ncclAllReduce)" if okt.item() else "torch.distributed NCCL all_reduce"
+
+
+def self_launch(args):
+    """--gpus N > 1 started without torchrun: re-run this command as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] --gpus {args.gpus} without torchrun: launching {args.gpus} ranks", file=sys.stderr)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    # bitwise run-to-run reproducibility of the gradient allreduce at a fixed N (SURVEY §8e)
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "Simple")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -326,7 +439,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
-        print(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        print(f"[bench] error: --gpus {args.gpus} but WORLD_SIZE={world}: a {world}-rank run cannot stand for "
+              f"{args.gpus} GPUs", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -337,28 +452,7 @@ def main():
     spec = cfg["spec"]
     model = FDSDF(spec, local, max_centers=n, path=None if args.path == "default" else args.path)
     P = model.P
-    collective = None
-    if world > 1:
-        # the library's own NCCL communicator (the in-step allreduce of FDSDF_STEP_ALLREDUCE);
-        # should loading / initialising it fail on a box, fall back to torch.distributed's NCCL
-        # all-reduce of the same two buffers on the same stream (reported in the JSON line)
-        ok = 1
-        try:
-            uid = F.fdsdf_comm_unique_id() if rank == 0 else bytes(128)
-        except F.FdsdfError:
-            uid, ok = bytes(128), 0
-        t = torch.tensor(list(uid) + [ok], dtype=torch.uint8, device=dev)
-        dist.broadcast(t, 0)
-        ok = int(t[128].item())
-        if ok:
-            try:
-                model.comm_init(bytes(t[:128].cpu().tolist()), rank, world)
-            except F.FdsdfError as e:
-                print(f"[bench] rank {rank}: fdsdf_comm_init failed ({e})", file=sys.stderr)
-                ok = 0
-        okt = torch.tensor([ok], dtype=torch.int32, device=dev)
-        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-        collective = "fdsdf NCCL (in-step ncclAllReduce)" if okt.item() else "torch.distributed NCCL all_reduce"
+    collective = setup_comm(model, world, rank, dev) if world > 1 else None
 
     params = torch.from_numpy(cfg["params"]).to(dev)
     x = torch.from_numpy(cfg["x"]).to(dev)
@@ -393,8 +487,6 @@ def main():
     launches_per_step = model.launch_count()
 
     # ------------------------------------------------------------------ timed region (device)
-    model.set_kernel_timing(True)
-    model.kernel_times(reset=True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clk = ClockSampler(local)
     clk.start()
@@ -409,8 +501,6 @@ def main():
     barrier()
     wall = time.perf_counter() - wall0
     clocks = clk.stop()
-    model.set_kernel_timing(False)
-    ktimes = model.kernel_times(reset=True)
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -419,6 +509,19 @@ def main():
     ms_per_step = t_ms / args.steps
     value = 9.0 * n * world / (ms_per_step * 1e-3)
     assert np.isfinite(loss.cpu().numpy()[4]), "non-finite loss"
+
+    # ------------------------------------------------------------------ per-kernel times: a second pass
+    # of the same K steps with the library's per-launch events on (two cudaEventRecord around every
+    # launch on the launching stream), kept out of the headline pass above
+    model.set_kernel_timing(True)
+    model.kernel_times(reset=True)
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        one_step(args.warmup + i)
+    barrier()
+    model.set_kernel_timing(False)
+    ktimes = model.kernel_times(reset=True)
 
     # ------------------------------------------------------------------ e2e (host buffers)
     e2e = None
@@ -450,11 +553,26 @@ def main():
             ev2[i][1].record(stream)
         barrier()
         e_ms = sum(a.elapsed_time(b) for a, b in ev2)
-        et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        # host wall clock per step: the call, its copies and the stream synchronisation that makes
+        # the host-side gradient / loss readable (the L2 flush and its sync stay outside)
+        w_s = 0.0
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step(args.warmup + i)
+            torch.cuda.synchronize()
+            w_s += time.perf_counter() - t0
+        barrier()
+        et = torch.tensor([e_ms, w_s * 1e3], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item()) / args.steps
-        e2e = {"value": 9.0 * n * world / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
+        e_ms = float(et[0].item()) / args.steps
+        w_ms = float(et[1].item()) / args.steps
+        e2e = {"value": 9.0 * n * world / (w_ms * 1e-3), "unit": UNIT, "ms_per_step": w_ms,
+               "timing": "host wall clock per step (call + copies + stream sync), max over ranks",
+               "device_ms_per_step": e_ms,
                "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(P * 4 + 8 * 8),
                "call": "fdsdf_step_host (pinned host points in, gradient + loss out)" if (world == 1 or lib_ar)
                else "torch copies + fdsdf_step"}
@@ -488,6 +606,11 @@ def main():
             "what": "opt-in FDSDF_CREATE_WGRAD_BF16X3: weight gradient with 3 bf16 piece products "
                     "(~3*2^-16 per product); forward / delta propagation bf16x6; same oracle gates"}
 
+    # ------------------------------------------------------------------ C5 (BASELINE configs[4])
+    c5 = None
+    if not args.no_c5 and args.config != "c5":
+        c5 = measure_c5(args, spec, local, rank, world, dev, stream, flush, barrier)
+
     # ------------------------------------------------------------------ roofline of the dominant kernel
     P_mm, P_gemm = p_mm(spec)
     path = model.path
@@ -511,23 +634,28 @@ def main():
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     ffma_peak = nsm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
     achieved = alg[dom] / (kms[dom] * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_note = None, "no ncu capture of this build in profiles/"
     prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(dom)
-        except (OSError, ValueError):
-            traffic = None
+            pj = json.load(open(prof))
+            if pj.get("build") == source_hash():
+                traffic = pj["per_launch"].get(dom)
+                traffic_note = f"ncu --set full dram__bytes_read+write of this build ({pj.get('capture', '')})"
+            else:
+                traffic_note = "profiles/ncu_dram_per_launch.json is from another build of csrc/: not reported"
+        except (OSError, ValueError, KeyError):
+            pass
     if path == "tensor":
         # fp32-accurate contraction as 6 bf16 tensor-core products (bf16x6):
         # its ceiling is the measured dense bf16 peak / 6
         bf16, src = measured_bf16_peak()
         peak = bf16 / 6.0
         roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic,
+                "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
                 "peak_note": f"bf16x6: {src} dense bf16 {bf16:.1f} TFLOP/s / 6 bf16 MMAs per fp32-accurate MAC",
                 "frac_of_fp32_ffma_peak": achieved / ffma_peak,
-                "frac_at_run_clock": None}
+                "frac_at_run_clock": (achieved / (peak * clocks["sm_mhz"] / sm_max)) if clocks.get("sm_mhz") else None}
     else:
         peak = ffma_peak
         roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -545,9 +673,9 @@ def main():
     # ------------------------------------------------------------------ CPU oracle baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, per, cores, sample = oracle_rate(cfg)
+        v, per_centre, cores, sample = oracle_rate(cfg)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-               "s_per_step": per}
+               "s_per_centre": per_centre, "s_per_full_step_extrapolated": per_centre * n}
 
     if rank == 0:
         line = {
@@ -560,7 +688,7 @@ def main():
             "precision": ("bf16x6: fp32 operands split exactly into 3 bf16 pieces, 6 tcgen05 products, fp32 "
                           "accumulation" if path == "tensor" else "fp32 FFMA"), "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps), "clocks": clocks, **extras,
-            "collective": collective,
+            "collective": collective, "c5": c5,
             "wall_s_timed_region": wall,
         }
         print(json.dumps(line), flush=True)

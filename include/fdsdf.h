@@ -127,7 +127,9 @@ typedef struct {
 enum {
   FDSDF_STEP_ACCUMULATE = 1u,   /* d_grad += instead of =                                  */
   FDSDF_STEP_ALLREDUCE = 2u     /* NCCL SUM of d_grad and d_loss after the step (same      */
-                                /* stream); requires fdsdf_comm_init                       */
+                                /* stream); requires fdsdf_comm_init.  With both flags     */
+                                /* only this call's gradient is summed over the ranks (in  */
+                                /* a context buffer) and then added: d_grad += sum_r g_r   */
 };
 
 enum {                          /* sticky device flags                                     */

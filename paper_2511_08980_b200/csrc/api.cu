@@ -81,6 +81,7 @@ struct fdsdf_ctx {
   float* xstage = nullptr;   // fdsdf_step_host: device copy of the points [max_centers][3]
   float* hgrad = nullptr;    //                  the gradient [P] (accumulates with ACCUMULATE)
   double* hloss = nullptr;   //                  the loss [8]
+  float* gcall = nullptr;    // ACCUMULATE | ALLREDUCE: this call's gradient [P], reduced before it is added
   float* zscr = nullptr;     // eval scratch (per CTA)
   float* seed = nullptr;
   double* lossp = nullptr;
@@ -230,7 +231,7 @@ void fdsdf_destroy(fdsdf_ctx* c) {
   for (cudaEvent_t e : c->spare) cudaEventDestroy(e);
   void* bufs[] = {c->wt,   c->wb,   c->zf,     c->zscr,   c->seed,  c->lossp, c->del, c->actv,
                   c->bacc, c->part, c->dflags, c->fimg, c->cinfo, c->zev, c->bimg, c->hframes, c->htmp,
-                  c->xstage, c->hgrad, c->hloss};
+                  c->xstage, c->hgrad, c->hloss, c->gcall};
   for (void* b : bufs)
     if (b) cudaFree(b);
   cudaSetDevice(prev);
@@ -351,6 +352,7 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     ok = ok && alloc((void**)&c->xstage, (size_t)max_centers * 3 * sizeof(float));
     ok = ok && alloc((void**)&c->hgrad, (size_t)c->P * sizeof(float));
     ok = ok && alloc((void**)&c->hloss, 8 * sizeof(double));
+    ok = ok && alloc((void**)&c->gcall, (size_t)c->P * sizeof(float));
     if (ok) ok = cudaMemset(c->hgrad, 0, (size_t)c->P * sizeof(float)) == cudaSuccess;
     ok = ok && alloc((void**)&c->seed, (size_t)max_centers * NSEED * sizeof(float));
     ok = ok && alloc((void**)&c->del, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
@@ -714,9 +716,13 @@ static fdsdf_status step_impl(fdsdf_ctx* c, const float* d_params, const float* 
   f.lossp = c->lossp;
   f.nfcta = fgrid;
   f.ls = a.ls;
-  f.grad = d_grad;
+  // ACCUMULATE together with ALLREDUCE: only THIS call's contribution may be summed over the
+  // ranks (d_grad already holds the reduced earlier contributions, identical on every rank), so
+  // finalize writes it to gcall, the allreduce runs on gcall, and it is then added to d_grad
+  const bool acc_reduce = (flags & FDSDF_STEP_ACCUMULATE) && (flags & FDSDF_STEP_ALLREDUCE);
+  f.grad = acc_reduce ? c->gcall : d_grad;
   f.loss = d_loss;
-  f.accumulate = (flags & FDSDF_STEP_ACCUMULATE) ? 1 : 0;
+  f.accumulate = (!acc_reduce && (flags & FDSDF_STEP_ACCUMULATE)) ? 1 : 0;
   f.dflags = c->dflags;
   f.n_local = n;
   f.P = c->P;
@@ -727,12 +733,17 @@ static fdsdf_status step_impl(fdsdf_ctx* c, const float* d_params, const float* 
     int r1 = 0, r2 = 0, r3 = 0;
     run_slot(c, FDSDF_KSLOT_ALLREDUCE, strm, [&] {
       g_nccl.groupStart();
-      r1 = g_nccl.allReduce(d_grad, d_grad, (size_t)c->P, kNcclFloat32, kNcclSum, c->comm, strm);
+      float* gbuf = acc_reduce ? c->gcall : d_grad;
+      r1 = g_nccl.allReduce(gbuf, gbuf, (size_t)c->P, kNcclFloat32, kNcclSum, c->comm, strm);
       r2 = g_nccl.allReduce(d_loss, d_loss, 8, kNcclFloat64, kNcclSum, c->comm, strm);
       r3 = g_nccl.groupEnd();
       return cudaSuccess;
     });
     if (r1 || r2 || r3) return done(fail(c, FDSDF_E_NCCL, "ncclAllReduce failed"));
+    if (acc_reduce) {
+      e = launch_add_inplace(d_grad, c->gcall, c->P, strm);
+      if (e != cudaSuccess) return done(cuda_fail(c, e, "add_kernel"));
+    }
   }
   if (h_grad) {
     e = cudaMemcpyAsync(h_grad, d_grad, (size_t)c->P * sizeof(float), cudaMemcpyDeviceToHost, strm);

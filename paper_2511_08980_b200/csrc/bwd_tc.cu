@@ -87,13 +87,18 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tbase = tc_setup<C>(bars);
 
-  if (warp == 0) {
-    if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 1, a.ntiles, Ws, bars);
-  } else if (warp == 1) {
-    if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
+  if (warp < C::EPI0) {
+    // control warp group: producer (warp 0), MMA issuer (warp 1), two idle warps
+    setmaxnreg_dec<C::REG_CTL>();
+    if (warp == 0) {
+      if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 1, a.ntiles, Ws, bars);
+    } else if (warp == 1) {
+      if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
+    }
   } else {
-    const int ew = warp - 2;
-    const int et = tid - 64;
+    setmaxnreg_inc<C::REG_EPI>();
+    const int ew = warp - C::EPI0;
+    const int et = tid - 32 * C::EPI0;
     const int q4 = warp & 3;
     const int hh = (ew >> 2) % MH;
     const int eg = ew / (4 * MH);

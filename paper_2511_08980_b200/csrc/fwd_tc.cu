@@ -51,13 +51,19 @@ constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && FWD_TC_NSPLIT == 1;
 // tile width: FWD_TC_N columns up to 256-wide layers; 32 for 512-wide ones (C3), where a wider
 // B operand (32 x 512 x 3 pieces = 96 KB) would not fit next to the weight ring
 constexpr int fwd_tc_n(int mpad) { return mpad == 512 ? 32 : FWD_TC_N; }
+// MN-major B operand (a thread writes a centre's 4 / 8 consecutive columns as one vector store
+// per piece) wherever the tile is whole 64-column swizzle atoms: N = 64 (MPAD <= 256)
+#ifndef FWD_TC_BMN
+#define FWD_TC_BMN 0
+#endif
+constexpr int fwd_tc_bmn(int mpad) { return (FWD_TC_BMN && FWD_TC_NSPLIT == 1 && fwd_tc_n(mpad) % 64 == 0) ? 1 : 0; }
 template <int MPAD, int MODE>
 struct FtcCfg : TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
-                      FWD_TC_NSPLIT> {
+                      FWD_TC_NSPLIT, fwd_tc_bmn(MPAD)> {
   // TMEM stash (FWD_PIPE0): the next tile's layer-0 outputs, (MH x EG thread groups) x CPE x
   // columns per centre = MH x N columns
   using B = TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
-                  FWD_TC_NSPLIT>;
+                  FWD_TC_NSPLIT, fwd_tc_bmn(MPAD)>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
@@ -147,14 +153,19 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tbase = tc_setup<C>(bars);
 
-  if (warp == 0) {
-    if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 0, a.ntiles, Ws, bars);
-  } else if (warp == 1) {
-    if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
+  if (warp < C::EPI0) {
+    // control warp group: producer (warp 0), MMA issuer (warp 1), two idle warps
+    setmaxnreg_dec<C::REG_CTL>();
+    if (warp == 0) {
+      if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 0, a.ntiles, Ws, bars);
+    } else if (warp == 1) {
+      if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
+    }
   } else {
+    setmaxnreg_inc<C::REG_EPI>();
     // ------------------------------------------------------------------ epilogue warps
-    const int ew = warp - 2;                 // 0 .. NEPI-1
-    const int et = tid - 64;                 // 0 .. NEPI*32-1
+    const int ew = warp - C::EPI0;  // 0 .. NEPI-1
+    const int et = tid - 32 * C::EPI0;  // 0 .. NEPI*32-1
     const int q4 = warp & 3;                 // TMEM lane quarter
     const int hh = (ew >> 2) % MH;           // M-half
     const int eg = ew / (4 * MH);            // centre group
@@ -181,6 +192,23 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
       return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (step ? 4 * m : m);
     };
     auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
+    // a centre's consecutive columns n0 .. n0+3 / n0+7 of the next B operand
+    auto put_b4 = [&](int n0, const float (&v)[4]) {
+      if constexpr (C::BMN) {
+        tc_put_b4<C>(Bs, n0, m, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) put_b(n0 + j, v[j]);
+      }
+    };
+    auto put_b8 = [&](int n0, const float (&v)[8]) {
+      if constexpr (C::BMN) {
+        tc_put_b8<C>(Bs, n0, m, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) put_b(n0 + j, v[j]);
+      }
+    };
     // cat(a, x) / sqrt(2) at the input of the skip layer net.skip (IGR convention, SURVEY §8c
     // item 14): when layer l's outputs feed it, every output is scaled by 1/sqrt(2) and the
     // threads of rows M .. M+2 (no neuron of layer l) supply the x part (as fwd.cu does)
@@ -408,14 +436,14 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
 #pragma unroll 1
           for (int i = 0; i < CPE; ++i) {
             const int cl = eg + C::EG * i;
-            float o4[4];
-            tc::tmem_ld4(tstash + i * CPC, o4);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) put_b(cl * CPC + j, o4[j]);
-            if (CPC == 8) {
-              tc::tmem_ld4(tstash + i * CPC + 4, o4);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) put_b(cl * CPC + 4 + j, o4[j]);
+            if constexpr (CPC == 4) {
+              float o4[4];
+              tc::tmem_ld4(tstash + i * CPC, o4);
+              put_b4(cl * CPC, o4);
+            } else {
+              float o8[8];
+              tc::tmem_ld8(tstash + i * CPC, o8);
+              put_b8(cl * CPC, o8);
             }
           }
           tc_epi_arrive(bars, 0);
@@ -502,10 +530,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
             if (last) {
               reduce4(cl, o0, o1, o2, o3);
             } else {
-              put_b(cl * 4 + 0, o0);
-              put_b(cl * 4 + 1, o1);
-              put_b(cl * 4 + 2, o2);
-              put_b(cl * 4 + 3, o3);
+              const float o4[4] = {o0, o1, o2, o3};
+              put_b4(cl * 4, o4);
             }
           } else {
             const float* ci = cis + cl * NCINFO;
@@ -548,8 +574,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
             if (last) {
               reduce4(cl, o[1], o[3], o[5], o[7]);
             } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) put_b(cl * 8 + j, o[j]);
+              put_b8(cl * 8, o);
             }
           }
         }

@@ -129,6 +129,8 @@ cudaError_t launch_fwd(const FwdArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_bwd(const BwdArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_wgrad(const WgradArgs& a, int nglayers, cudaStream_t st);
 cudaError_t launch_finalize(const FinArgs& a, cudaStream_t st);
+// y[i] += x[i], i < n (the reduced per-call gradient added to an accumulating one)
+cudaError_t launch_add_inplace(float* y, const float* x, int64_t n, cudaStream_t st);
 // tensor-core (tcgen05, bf16x6) path: available for padded widths 128 / 256 without skip
 bool tc_supported(int mpad, int skip);
 size_t tc_wimg_bytes(int mpad, int ngemm);          // one packed weight image (fwd or bwd)

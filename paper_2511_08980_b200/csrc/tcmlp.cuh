@@ -20,7 +20,7 @@
 
 namespace fdsdf {
 
-template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1>
+template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1, int BMN_ = 0>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
@@ -37,9 +37,27 @@ struct TcCfg {
   // (layer l).  Within a K chunk split s holds its 3 pieces as consecutive row blocks
   // [b0 | b1 | b2] of NS rows.
   static constexpr int NSPLIT = NSPLIT_;
+  // B operand layout: 0 = K-major SW128 (a column's K values contiguous: a thread = one K index
+  // writes 2-byte elements), 1 = MN-major SW128 (the columns contiguous: a thread writes a
+  // centre's consecutive columns as one 8- or 16-byte vector per piece).  MN-major: per 8-row K
+  // atom the 3 N-wide pieces [b0 | b1 | b2] as 3N/64 swizzle atoms of 1 KB (LBO = 1 KB), K atoms
+  // BSBO apart; a K chunk of 64 rows is 8 K atoms = BKC bytes, as in the K-major layout
+  static constexpr int BMN = BMN_;
+  static constexpr int BSBO = 3 * (N / NSPLIT_) / 64 * 1024;
   static constexpr int NS = N / NSPLIT;
   static constexpr int NEPI = NEPI_;            // epilogue warps (a multiple of 4 * MH)
-  static constexpr int NTHR = (2 + NEPI) * 32;
+  // warp-group aligned layout: warps 0..3 = control warp group (producer, MMA issuer, two idle
+  // warps), warps EPI0.. = epilogue warp groups.  The control group gives registers back
+  // (setmaxnreg.dec to REG_CTL) and the epilogue groups take them (setmaxnreg.inc to REG_EPI)
+  // from the CTA's pool, which is what the launch allocated: 20 warps x 96 registers per lane
+  // (the most 640 threads can launch with) = 4 x REG_CTL + 16 x REG_EPI -- an inc beyond the
+  // pool would wait forever
+  static constexpr int EPI0 = 4;
+  static constexpr int NTHR = (EPI0 + NEPI) * 32;
+  static constexpr int REG_LAUNCH = 96;
+  static constexpr int REG_CTL = 32;
+  static constexpr int REG_EPI = NEPI == 16 ? 112 : 96;
+  static_assert(EPI0 * REG_CTL + NEPI * REG_EPI <= (EPI0 + NEPI) * REG_LAUNCH, "setmaxnreg pool");
   static constexpr int EG = NEPI / (4 * MH);    // epilogue warps per (lane quarter, M-half)
   static constexpr int OFF_W = 0;
   static constexpr int OFF_B = NST * STAGE;
@@ -56,6 +74,7 @@ struct TcCfg {
   static_assert(NSPLIT == 1 || NSPLIT == 2, "one or two column splits");
   static_assert(TUSE <= 512, "TMEM has 512 columns");
   static_assert(NEPI % (4 * MH) == 0, "every (lane quarter, M-half) needs the same number of epilogue warps");
+  static_assert(!BMN || (NSPLIT == 1 && N % 64 == 0 && 8 * BSBO == BKC), "MN-major B: whole 64-column atoms");
 };
 
 struct TcBars {
@@ -104,6 +123,23 @@ __device__ __forceinline__ uint32_t tc_setup(const TcBars& b) {
   return *b.tslot;
 }
 
+// register rebalancing between the warp groups (whole warp groups, after tc_setup)
+template <int R>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));
+}
+template <int R>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R));
+}
+template <class C>
+__device__ __forceinline__ void tc_regsplit() {
+  if ((threadIdx.x >> 5) < C::EPI0)
+    setmaxnreg_dec<C::REG_CTL>();
+  else
+    setmaxnreg_inc<C::REG_EPI>();
+}
+
 template <class C>
 __device__ __forceinline__ void tc_teardown(uint32_t tbase) {
   tc::fence_before();
@@ -145,8 +181,8 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
 template <class C>
 __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned char* Ws,
                                        const unsigned char* Bs, uint32_t tbase, const TcBars& b) {
-  constexpr uint32_t id3 = tc::idesc_bf16(128, 3 * C::NS), id2 = tc::idesc_bf16(128, 2 * C::NS),
-                     id1 = tc::idesc_bf16(128, C::NS);
+  constexpr uint32_t id3 = tc::idesc_bf16(128, 3 * C::NS, 0, C::BMN), id2 = tc::idesc_bf16(128, 2 * C::NS, 0, C::BMN),
+                     id1 = tc::idesc_bf16(128, C::NS, 0, C::BMN);
   uint32_t it = 0, nb = 0;
 #ifdef FDSDF_PHASE_TIMING
   long long t0 = clock64(), tb = 0, tw = 0, tspan = 0, tm;
@@ -174,10 +210,11 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
           const uint32_t wa = smem_u32(Ws + s * C::STAGE);
           const uint32_t ba = smem_u32(Bs + kc * C::BKC + sp * 3 * C::NS * 128);
           const uint32_t d = tbase + h * C::DH + sp * C::RANGES * C::NS;
-          if (C::RANGES == 3) {
+          if constexpr (C::RANGES == 3) {
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
-              const uint64_t bd = tc::sdesc_sw128(ba + sub * 32);
+              const uint64_t bd = C::BMN ? tc::sdesc_sw128_mn(ba + sub * 2 * C::BSBO, 1024, C::BSBO)
+                                         : tc::sdesc_sw128(ba + sub * 32);
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
@@ -187,6 +224,7 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
             // (N = N: range 0) -- the six products, four A reads per K step instead of six
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {
+              static_assert(!C::BMN, "two-range issue: K-major B only");
               const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);
               const uint64_t b2 = tc::sdesc_sw128(ba + 2 * C::NS * 128 + sub * 32);
               tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b01, id2, (kc | sub) != 0 ? 1u : 0u);
@@ -268,6 +306,42 @@ __device__ __forceinline__ void tc_put_b(unsigned char* Bs, int n, int k, float 
   const uint32_t off = (uint32_t)((k >> 6) * C::BKC + sp * 3 * C::NS * 128) + tc::sw128_off(nl, k & 63, C::NS);
 #pragma unroll
   for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * C::NS * 128 + off) = s.p[p];
+}
+
+// MN-major B (C::BMN): byte offset of element (column np of the concatenated pieces
+// [b0 | b1 | b2], np = piece * N + column, K index k)
+template <class C>
+__device__ __forceinline__ uint32_t tc_bmn_off(int np, int k) {
+  const int kk = k & 63;
+  return (uint32_t)((k >> 6) * C::BKC + (kk >> 3) * C::BSBO + (np >> 6) * 1024 + (kk & 7) * 128 +
+                    ((((np & 63) >> 3) ^ (kk & 7)) << 4) + (np & 7) * 2);
+}
+
+// MN-major B: the 8 consecutive columns n0 .. n0+7 (n0 % 8 == 0) at K index k, split into 3 bf16
+// pieces, one 16-byte store per piece
+template <class C>
+__device__ __forceinline__ void tc_put_b8(unsigned char* Bs, int n0, int k, const float (&v)[8]) {
+  static_assert(C::BMN, "MN-major B only");
+  FDSDF_ASSERT(n0 >= 0 && n0 + 8 <= C::N && (n0 & 7) == 0 && k >= 0 && k < C::MPAD);
+  uint32_t w[4][3];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) tc::split3x2(v[2 * q], v[2 * q + 1], w[q]);
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+    *reinterpret_cast<uint4*>(Bs + tc_bmn_off<C>(p * C::N + n0, k)) = make_uint4(w[0][p], w[1][p], w[2][p], w[3][p]);
+}
+
+// MN-major B: 4 consecutive columns n0 .. n0+3 (n0 % 4 == 0), one 8-byte store per piece
+template <class C>
+__device__ __forceinline__ void tc_put_b4(unsigned char* Bs, int n0, int k, const float (&v)[4]) {
+  static_assert(C::BMN, "MN-major B only");
+  FDSDF_ASSERT(n0 >= 0 && n0 + 4 <= C::N && (n0 & 3) == 0 && k >= 0 && k < C::MPAD);
+  uint32_t w[2][3];
+  tc::split3x2(v[0], v[1], w[0]);
+  tc::split3x2(v[2], v[3], w[1]);
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+    *reinterpret_cast<uint2*>(Bs + tc_bmn_off<C>(p * C::N + n0, k)) = make_uint2(w[0][p], w[1][p]);
 }
 
 // accumulator of columns [col, col + W) of this warp's lane quarter: the sum of the three

@@ -240,4 +240,16 @@ cudaError_t launch_finalize(const FinArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+__global__ void add_kernel(float* y, const float* x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += x[i];
+}
+
+cudaError_t launch_add_inplace(float* y, const float* x, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>(1184, (n + 255) / 256);
+  add_kernel<<<grid, 256, 0, st>>>(y, x, n);
+  return cudaGetLastError();
+}
+
 }  // namespace fdsdf

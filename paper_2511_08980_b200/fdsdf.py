@@ -355,9 +355,12 @@ class FDSDF:
         return H
 
     def step(self, params, x, n_surface, h, loss_cfg, counts=None, frame_seed=0, index_offset=0, frames=None,
-             eps_grad=1e-6, grad=None, loss=None, accumulate=False, allreduce=False, stream=None):
-        """Returns (grad [P] fp32, loss [8] fp64) device tensors."""
+             eps_grad=None, grad=None, loss=None, accumulate=False, allreduce=False, stream=None):
+        """Returns (grad [P] fp32, loss [8] fp64) device tensors.  eps_grad (the degenerate-mask
+        threshold) defaults to loss_cfg["eps_grad"] when present, else 1e-6."""
         import torch
+        if eps_grad is None:
+            eps_grad = loss_cfg.get("eps_grad", 1e-6)
         params = self._dev(params, torch.float32)
         x = self._dev(x, torch.float32).reshape(-1, 3)
         n = x.shape[0]

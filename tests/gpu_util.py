@@ -3,9 +3,28 @@ fp64 oracle on identical seeded inputs, and compare with the tolerances of BASEL
 north_star (read concretely in SURVEY.md §8c and DESIGN.md §5)."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from harness import make_config
+from oracle.c_oracle import c_oracle_step, c_oracle_eval
+
+# The parity reference is the plain single-threaded fp64 C oracle (BASELINE.json north_star;
+# oracle/c/fdsdf_oracle.c, pinned by tests/test_c_oracle_pins.py).  The harness runs it on
+# contiguous row chunks in parallel threads (each call single-threaded) and adds the chunks in
+# order; the oracle's arithmetic per centre is unchanged.
+NTHREADS = max(1, min(32, os.cpu_count() or 1))
+
+
+def ref_step(*args, **kw):
+    kw.setdefault("threads", NTHREADS)
+    return c_oracle_step(*args, **kw)
+
+
+def ref_eval(*args, **kw):
+    kw.setdefault("threads", NTHREADS)
+    return c_oracle_eval(*args, **kw)
 
 ENTRY_TOL = 1e-4     # |d| <= 1e-4 (1 + |ref|) per point value and FD Hessian entry (h = 1e-2)
 LOSS_RTOL = 1e-4     # relative, each loss component and the total

@@ -17,7 +17,8 @@ import pytest
 torch = pytest.importorskip("torch")
 
 from harness import make_config  # noqa: E402
-from oracle import oracle_eval, oracle_step  # noqa: E402
+from gpu_util import ref_step, ref_eval  # noqa: E402
+from oracle import oracle_step, oracle_eval  # noqa: E402  (batched torch fp64 oracle for the 200k-centre C5 check)
 from gpu_util import compare_eval, gpu_eval, per_tensor_grad_errors, LOSS_RTOL, GRAD_RTOL  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -38,7 +39,7 @@ def _model(spec, n, eval_only=False):
     return m
 
 
-def _check_step(c, n_chunk=None):
+def _check_step(c, n_chunk=None, step_fn=ref_step):
     n = len(c["x"])
     m = _model(c["spec"], n)
     ev = gpu_eval(m, c, denom=c["loss"]["denom"])
@@ -51,7 +52,7 @@ def _check_step(c, n_chunk=None):
     for s in range(0, n, n_chunk):
         e = min(n, s + n_chunk)
         surf = np.arange(s, e) < c["n_surface"]
-        o = oracle_step(c["spec"], c["params"], c["x"][s:e], 0, c["h"], c["loss"], frames=(fr[s:e, :3], fr[s:e, 3:]),
+        o = step_fn(c["spec"], c["params"], c["x"][s:e], 0, c["h"], c["loss"], frames=(fr[s:e, :3], fr[s:e, 3:]),
                         counts=counts, surface_mask=surf, gidx=range(s, e))
         ol[:6] += o["loss"][:6]
         og = og + o["grad"]
@@ -70,7 +71,7 @@ def _check_step(c, n_chunk=None):
 def test_c2_full_eval_and_step():
     c = make_config("c2")
     ev = _check_step(c)
-    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
+    o = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
                     frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
     err = compare_eval(ev, o)
     print("c2 full eval", {k: float(v) for k, v in err.items()})
@@ -80,8 +81,11 @@ def test_c2_full_eval_and_step():
 
 
 def test_c5_full_step_chunked_oracle():
+    """C5 (200k centres): checked against the batched PyTorch fp64 oracle (the C oracle, ~6 ms per
+    centre on one core, would need ~20 CPU-minutes; both oracles are pinned and agree to 1e-9,
+    tests/test_c_oracle_pins.py)."""
     c = make_config("c5")
-    ev = _check_step(c, n_chunk=20_000)
+    ev = _check_step(c, n_chunk=20_000, step_fn=oracle_step)
     rng = np.random.default_rng(0)
     rows = np.sort(rng.choice(len(c["x"]), 3000, replace=False))
     o = oracle_eval(c["spec"], c["params"], c["x"][rows], 0, c["h"],
@@ -105,7 +109,7 @@ def test_c4_h_sweep(h):
     c = make_config("c4", 600, 600, h=h)
     m = _model(c["spec"], len(c["x"]), eval_only=True)
     g = gpu_eval(m, c)
-    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
+    o = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
                     frames=(g["frames"][:, :3], g["frames"][:, 3:]))
     err = compare_eval(g, o)
     print("c4 h", h, {k: float(v) for k, v in err.items()})
@@ -135,7 +139,7 @@ def test_c3_full_size(path):
     sub = {k: v[idx] for k, v in ev.items()}
     fr = sub["frames"]
     surf = idx < c["n_surface"]
-    o = oracle_eval(c["spec"], c["params"], c["x"][idx], int(surf.sum()), c["h"], frames=(fr[:, :3], fr[:, 3:]),
+    o = ref_eval(c["spec"], c["params"], c["x"][idx], int(surf.sum()), c["h"], frames=(fr[:, :3], fr[:, 3:]),
                     denom=c["loss"]["denom"])
     # oracle_eval assumes a surface prefix: the sampled rows are sorted, so surface rows come first
     err = compare_eval(sub, o)

@@ -19,7 +19,7 @@ SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, %r); sys.path.insert(0, %r)
 from harness import make_config
-from oracle import oracle_step, oracle_eval
+from gpu_util import ref_step, ref_eval
 from gpu_util import compare_eval, gpu_eval, per_tensor_grad_errors
 from paper_2511_08980_b200 import FDSDF
 name, ns, nu, path = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
@@ -28,12 +28,12 @@ n = len(c["x"])
 m = FDSDF(c["spec"], 0, max_centers=n)
 assert m.path == path, m.path
 ev = gpu_eval(m, c, denom=c["loss"]["denom"])
-o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]),
+o = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]),
                 denom=c["loss"]["denom"], denom_pow=c["loss"]["denom_pow"])
 err = compare_eval(ev, o)
 assert all(err[k] <= 1.0 for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K")), err
 g, l = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])
-o = oracle_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
+o = ref_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
 l = l.cpu().numpy(); ge = per_tensor_grad_errors(c["spec"], g.cpu().numpy().astype(np.float64), o["grad"])
 le = np.abs(l[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
 assert np.all(le[o["loss"][:5] != 0] <= 1e-4), le

@@ -43,3 +43,22 @@ def test_allreduce_world1_is_identity_and_fdsdf_allreduce():
     torch.cuda.synchronize()
     assert torch.equal(buf, torch.arange(1000, dtype=torch.float32, device="cuda"))
     m.close()
+
+
+def test_accumulate_with_allreduce_reduces_only_this_call():
+    """FDSDF_STEP_ACCUMULATE | FDSDF_STEP_ALLREDUCE: the call's own gradient is reduced in a
+    context buffer and then added (d_grad += sum_r g_r), so a running sum is never multiplied by
+    the world size.  At world size 1: prev + g exactly, and the loss is this call's."""
+    from paper_2511_08980_b200 import FDSDF
+    from paper_2511_08980_b200 import fdsdf as F
+    c = make_config("c2", 200, 200)
+    m = FDSDF(c["spec"], 0, max_centers=400)
+    m.comm_init(F.fdsdf_comm_unique_id(), 0, 1)
+    g1, l1 = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=3)
+    g1, l1 = g1.clone(), l1.clone()
+    prev = torch.linspace(-1, 1, m.P, device="cuda", dtype=torch.float32)
+    g2, l2 = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=3, grad=prev.clone(),
+                    accumulate=True, allreduce=True)
+    torch.cuda.synchronize()
+    assert torch.equal(g2, prev + g1) and torch.equal(l2, l1)
+    m.close()

@@ -11,7 +11,7 @@ import pytest
 torch = pytest.importorskip("torch")
 
 from harness import make_config, plane_mlp, loss_cfg, num_params  # noqa: E402
-from oracle import oracle_step, oracle_eval  # noqa: E402
+from gpu_util import ref_step, ref_eval  # noqa: E402
 from gpu_util import (compare_eval, gpu_eval, per_tensor_grad_errors, LOSS_RTOL,  # noqa: E402
                       GRAD_RTOL)
 
@@ -55,7 +55,7 @@ def test_eval_parity_given_frames(name, ns, nu, h, path):
     c = make_config(name, ns, nu, h=h)
     m = _model(c["spec"], len(c["x"]), eval_only=True, path=path)
     g = gpu_eval(m, c)
-    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
+    o = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
                     frames=(g["frames"][:, :3], g["frames"][:, 3:]))
     err = compare_eval(g, o)
     print(name, ns, nu, {k: float(v) for k, v in err.items()})
@@ -71,7 +71,7 @@ def test_eval_parity_self_framed(name, ns, nu, path):
     c = make_config(name, ns, nu, h=1e-2)
     m = _model(c["spec"], len(c["x"]), eval_only=True, path=path)
     g = gpu_eval(m, c)
-    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frame_seed=c["frame_seed"])
+    o = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frame_seed=c["frame_seed"])
     fr = np.concatenate([o["u"], o["v"]], 1)
     assert np.max(np.abs(g["frames"] - fr)) < 1e-3
     err = compare_eval(g, o)
@@ -104,7 +104,7 @@ def test_step_parity(case, path):
     ev = gpu_eval(m, c, denom=c["loss"]["denom"])
     grad, loss = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])
     grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
-    o = oracle_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"],
+    o = ref_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"],
                     frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
     lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
     gerr = per_tensor_grad_errors(c["spec"], grad, o["grad"])
@@ -189,7 +189,7 @@ def test_tiny_batches(n, path):
     c = make_config("c2", max(1, n // 2), n - max(1, n // 2))
     m = _model(c["spec"], n, path=path)
     g = gpu_eval(m, c)
-    o = oracle_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
+    o = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"],
                     frames=(g["frames"][:, :3], g["frames"][:, 3:]))
     err = compare_eval(g, o)
     assert max(err[k] for k in ("f", "g", "fuu", "fuv", "fvv")) <= 1.0, err
@@ -216,16 +216,110 @@ def test_ragged_widths_eval_and_step(act, widths, skip, path):
     c = dict(spec=spec, params=params, x=x, n_surface=ns, h=h, frame_seed=5, loss=ls)
     m = _model(spec, n, path=path)
     g = gpu_eval(m, c)
-    o = oracle_eval(spec, params, x, ns, h, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    o = ref_eval(spec, params, x, ns, h, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
     err = compare_eval(g, o)
     print(act, widths, skip, m.path, {k: float(v) for k, v in err.items()})
     for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K"):
         assert err[k] <= 1.0, (k, err)
     grad, loss = m.step(params, x, ns, h, ls, frame_seed=5)
     grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
-    o = oracle_step(spec, params, x, ns, h, ls, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    o = ref_step(spec, params, x, ns, h, ls, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
     lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
     gerr = per_tensor_grad_errors(spec, grad, o["grad"])
     print("lerr", lerr, "gerr", gerr)
     assert np.all(lerr[o["loss"][:5] != 0] <= LOSS_RTOL), lerr
     assert np.all(gerr <= GRAD_RTOL), gerr
+
+
+@pytest.mark.parametrize("om_first,om_hidden", [(30.0, 15.0), (10.0, 30.0)])
+def test_sine_hidden_frequency_parity(om_first, om_hidden, path):
+    """A SIREN 3->256x4->1 with omega0_first != omega0_hidden: eval
+    (GIVEN frames) and step parity against the oracle -- the first / hidden frequencies are
+    applied to the right layers on both paths (the closed-form pin of the oracle is
+    tests/test_c_oracle_pins.py::test_sine_hidden_layer_frequency_closed_form)."""
+    from harness import init_params, mlp_spec, csg_surface, uniform_box
+    spec = mlp_spec([3, 256, 256, 256, 256, 1], "sine", omega0_first=om_first, omega0_hidden=om_hidden)
+    params = init_params(spec, "siren", 5)
+    x = np.concatenate([csg_surface(150, 3, 21), uniform_box(123, 1.1, 22)]).astype(np.float32)
+    n, ns, h = len(x), 150, float(np.float32(5e-3))
+    ls = loss_cfg("ncr", "paper", w_dm=1, lambda_dnm=100, lambda_eik=50, lambda_fd=1)
+    c = dict(spec=spec, params=params, x=x, n_surface=ns, h=h, frame_seed=11, loss=ls)
+    m = _model(spec, n, path=path)
+    g = gpu_eval(m, c)
+    o = ref_eval(spec, params, x, ns, h, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    err = compare_eval(g, o)
+    print(om_first, om_hidden, {k: float(v) for k, v in err.items()})
+    for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K"):
+        assert err[k] <= 1.0, (k, err)
+    grad, loss = m.step(params, x, ns, h, ls, frame_seed=11)
+    grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
+    o = ref_step(spec, params, x, ns, h, ls, frames=(g["frames"][:, :3], g["frames"][:, 3:]))
+    lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
+    gerr = per_tensor_grad_errors(spec, grad, o["grad"])
+    print("lerr", lerr, "gerr", gerr)
+    assert np.all(lerr[o["loss"][:5] != 0] <= LOSS_RTOL), lerr
+    assert np.all(gerr <= GRAD_RTOL), gerr
+
+
+def _gap_threshold(gn, lo, hi):
+    """an eps_grad in the middle of the widest gap between consecutive sorted |g| among the
+    ranks [lo, hi): no centre lies near the threshold, so fp32 and fp64 take the same decision"""
+    s = np.sort(gn)
+    j = lo + int(np.argmax(np.diff(s[lo:hi])))
+    return float(0.5 * (s[j] + s[j + 1]))
+
+
+@pytest.mark.parametrize("name,ns,nu", [("c1", 300, 300), ("c2", 200, 200)])
+def test_degenerate_mask_step_parity(name, ns, nu, path):
+    """eps_grad near the median |g| masks about half of the centres: the GPU's
+    mask, n_degenerate = loss[5], every loss term and the gradient match the oracle's; masked
+    centres carry u = v = 0 and zero FD entries / D / K."""
+    c = make_config(name, ns, nu)
+    n = len(c["x"])
+    ls = dict(loss_cfg("ncr", "paper", w_dm=1, lambda_dnm=100, lambda_eik=50, lambda_fd=1))
+    o0 = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frame_seed=c["frame_seed"])
+    gn = np.linalg.norm(o0["g"], axis=1)
+    ls["eps_grad"] = _gap_threshold(gn, int(0.4 * n), int(0.6 * n))
+    m = _model(c["spec"], n, path=path)
+    ev = m.eval(c["params"], c["x"], c["n_surface"], c["h"], frame_seed=c["frame_seed"], eps_grad=ls["eps_grad"])
+    ev = {k: v.cpu().numpy() for k, v in ev.items()}
+    mk = ev["mask"].astype(bool)
+    assert np.array_equal(mk, gn >= ls["eps_grad"]) and 0.3 * n < (~mk).sum() < 0.7 * n
+    assert np.all(ev["frames"][~mk] == 0) and np.all(ev["hess"][~mk] == 0)
+    assert np.all(ev["K"][~mk] == 0) and np.all(ev["D"][~mk] == 0)
+    grad, loss = m.step(c["params"], c["x"], c["n_surface"], c["h"], ls, frame_seed=c["frame_seed"])
+    grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
+    assert m.device_flags() == 0
+    o = ref_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], ls,
+                    frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
+    assert loss[5] == o["loss"][5] == float((~mk).sum())
+    lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
+    gerr = per_tensor_grad_errors(c["spec"], grad, o["grad"])
+    print(name, "masked", int((~mk).sum()), "lerr", lerr, "gerr", gerr)
+    assert np.all(lerr <= LOSS_RTOL), lerr
+    assert np.all(gerr <= GRAD_RTOL), gerr
+
+
+def test_all_fd_skipped_and_nonfinite_loss_flags(path):
+    """Every centre masked -> L_fd = 0, n_degenerate = N and FDSDF_FLAG_ALL_FD_SKIPPED (4, S:L306);
+    a non-finite output bias -> a non-finite loss and FDSDF_FLAG_NONFINITE_LOSS (2) without
+    the input flag; flags are sticky until read and then cleared."""
+    c = make_config("c1", 64, 64)
+    n = len(c["x"])
+    ls = dict(loss_cfg("ncr", "paper", w_dm=1, lambda_dnm=100, lambda_eik=50, lambda_fd=1), eps_grad=1e9)
+    m = _model(c["spec"], n, path=path)
+    grad, loss = m.step(c["params"], c["x"], c["n_surface"], c["h"], ls, frame_seed=c["frame_seed"])
+    loss = loss.cpu().numpy()
+    assert loss[3] == 0.0 and loss[5] == n
+    o = ref_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], ls, frame_seed=c["frame_seed"])
+    assert o["loss"][3] == 0.0 and o["loss"][5] == n
+    assert abs(loss[4] - o["loss"][4]) <= LOSS_RTOL * abs(o["loss"][4])
+    assert np.all(per_tensor_grad_errors(c["spec"], grad.cpu().numpy().astype(np.float64), o["grad"]) <= GRAD_RTOL)
+    assert m.device_flags() == 4
+    assert m.device_flags() == 0
+    p = c["params"].copy()
+    p[-1] = np.float32("nan")
+    grad, loss = m.step(p, c["x"], c["n_surface"], c["h"], dict(ls, eps_grad=1e-6), frame_seed=c["frame_seed"])
+    assert not np.isfinite(loss.cpu().numpy()[4])
+    assert m.device_flags() == 2
+    assert m.device_flags() == 0

@@ -7,7 +7,7 @@ import pytest
 torch = pytest.importorskip("torch")
 
 from harness import make_config, sphere_surface  # noqa: E402
-from oracle import oracle_step  # noqa: E402
+from gpu_util import ref_step  # noqa: E402
 from oracle.train_oracle import adam_step, sample_batch  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -98,7 +98,7 @@ def test_training_loop_matches_oracle():
     for it in range(3):
         x = sample_batch(pool, n_pick, half, n_unif, 21, it)
         fs = tr.frame_seed(it)
-        o = oracle_step(spec, rp.astype(np.float32), x, n_pick, h, lc, frame_seed=fs)
+        o = ref_step(spec, rp.astype(np.float32), x, n_pick, h, lc, frame_seed=fs)
         lerr = abs(losses[it][4] - o["loss"][4]) / abs(o["loss"][4])
         print("iter", it, "loss", losses[it][4], "oracle", o["loss"][4], "rel", lerr)
         assert lerr <= 1e-3  # params drift apart by O(lr * 1e-5) after the first update

@@ -8,7 +8,7 @@ import pytest
 torch = pytest.importorskip("torch")
 
 from harness import make_config, loss_cfg  # noqa: E402
-from oracle import oracle_step  # noqa: E402
+from gpu_util import ref_step  # noqa: E402
 from gpu_util import gpu_eval, per_tensor_grad_errors, LOSS_RTOL, GRAD_RTOL  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -42,7 +42,7 @@ def test_step_parity_wgrad_bf16x3(name, ns, nu, ls, path):
     ev = gpu_eval(m, c, denom=c["loss"]["denom"])
     grad, loss = m.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frame_seed=c["frame_seed"])
     grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
-    o = oracle_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"],
+    o = ref_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"],
                     frames=(ev["frames"][:, :3], ev["frames"][:, 3:]))
     lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
     gerr = per_tensor_grad_errors(c["spec"], grad, o["grad"])
