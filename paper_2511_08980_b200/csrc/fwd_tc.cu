@@ -54,7 +54,7 @@ constexpr int fwd_tc_n(int mpad) { return mpad == 512 ? 32 : FWD_TC_N; }
 // MN-major B operand (a thread writes a centre's 4 / 8 consecutive columns as one vector store
 // per piece) wherever the tile is whole 64-column swizzle atoms: N = 64 (MPAD <= 256)
 #ifndef FWD_TC_BMN
-#define FWD_TC_BMN 0
+#define FWD_TC_BMN 1
 #endif
 constexpr int fwd_tc_bmn(int mpad) { return (FWD_TC_BMN && FWD_TC_NSPLIT == 1 && fwd_tc_n(mpad) % 64 == 0) ? 1 : 0; }
 template <int MPAD, int MODE>
