@@ -23,6 +23,11 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+// 1: the sine pair maps take the fast series form when the whole warp's arguments are small
+#ifndef FDSDF_PAIR_FAST
+#define FDSDF_PAIR_FAST 1
+#endif
+
 namespace fdsdf {
 
 template <int ACT>
@@ -69,14 +74,85 @@ struct Act<ACT_SINE> {
     *Aa = p.cy * p.sA;                           // (sin(y+A) - sin(y-A))/2
     *Sa = fmaf(-4.0f * p.sy, p.s2A, 2.0f * p.dys);  // sin(y+A)+sin(y-A)-2 sin z
   }
+
+  // Fast form of pre() for |A| <= FAST_A and |S| <= FAST_S (the whole warp, chosen per centre
+  // by pairs_fwd4 / pairs_bwd4 with a vote, so there is no divergent branch): sin A and
+  // sin^2(A/2), sin(S/2) and sin^2(S/4) straight from their Taylor series in A^2 and (S/2)^2 --
+  // no half-angle sincos, no range tests.  Truncation (first omitted term) relative to the
+  // value: sin A  A^10/11! <= 2.4e-11, sin^2(A/2)  A^10/(2 * 12!/...) <= 4e-12, sin(S/2) (S/2)^8/9!
+  // <= 2e-14, sin^2(S/4) (S/2)^6/20160 <= 2e-10 -- all below fp32 rounding, and every series
+  // keeps the RELATIVE precision of the small quantities.
+  static constexpr float FAST_A = 0.5f, FAST_S = 0.25f;
+  __device__ __forceinline__ static P2 pre_fast(const C& c, float A, float S) {
+    P2 p;
+    const float a2 = A * A;
+    float q = fmaf(a2, 2.7557319224e-6f, -1.9841269841e-4f);  // sin A = A (1 - A^2/6 + ... + A^8/9!)
+    q = fmaf(a2, q, 8.3333333333e-3f);
+    q = fmaf(a2, q, -1.6666666667e-1f);
+    p.sA = fmaf(A * a2, q, A);
+    float r = fmaf(a2, 1.3778659612e-7f, -1.2400793651e-5f);  // sin^2(A/2) = A^2/4 - A^4/48 + ... + A^10/7257600
+    r = fmaf(a2, r, 6.9444444444e-4f);
+    r = fmaf(a2, r, -2.0833333333e-2f);
+    r = fmaf(a2, r, 0.25f);
+    p.s2A = a2 * r;
+    p.cA = fmaf(-2.0f, p.s2A, 1.0f);
+    const float y = 0.5f * S, y2 = y * y;
+    float t = fmaf(y2, -1.9841269841e-4f, 8.3333333333e-3f);  // sin y, y = S/2
+    t = fmaf(y2, t, -1.6666666667e-1f);
+    const float sS2 = fmaf(y * y2, t, y);
+    float w = fmaf(y2, 6.9444444444e-4f, -2.0833333333e-2f);  // sin^2(y/2) = y^2/4 - y^4/48 + y^6/1440
+    w = fmaf(y2, w, 0.25f);
+    const float s2S = y2 * w;
+    p.dys = fmaf(sS2, c.cz, -2.0f * s2S * c.sz);   // sin y - sin z
+    p.dyc = fmaf(-sS2, c.sz, -2.0f * s2S * c.cz);  // cos y - cos z
+    p.sy = c.sz + p.dys;
+    p.cy = c.cz + p.dyc;
+    return p;
+  }
+  // all 4 pairs of a centre: o[2p] = A_a, o[2p+1] = S_a (warp-uniform choice of the fast form)
+  __device__ __forceinline__ static void pairs_fwd4(const C& c, const float (&A)[4], const float (&S)[4], float beta,
+                                                    float (&o)[8]) {
+    const float mA = fmaxf(fmaxf(fabsf(A[0]), fabsf(A[1])), fmaxf(fabsf(A[2]), fabsf(A[3])));
+    const float mS = fmaxf(fmaxf(fabsf(S[0]), fabsf(S[1])), fmaxf(fabsf(S[2]), fabsf(S[3])));
+    if (FDSDF_PAIR_FAST && __all_sync(0xffffffffu, mA <= FAST_A && mS <= FAST_S)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const P2 p = pre_fast(c, A[q], S[q]);
+        o[2 * q] = p.cy * p.sA;
+        o[2 * q + 1] = fmaf(-4.0f * p.sy, p.s2A, 2.0f * p.dys);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pair_fwd(c, A[q], S[q], beta, &o[2 * q], &o[2 * q + 1]);
+    }
+  }
   __device__ __forceinline__ static void pair_bwd(const C& c, float A, float S, float beta, float* Aa,
                                                   float* Sa, float* P, float* Dd, float* Z) {
     const P2 p = pre(c, A, S);
+    bwd_from(p, Aa, Sa, P, Dd, Z);
+  }
+  __device__ __forceinline__ static void bwd_from(const P2& p, float* Aa, float* Sa, float* P, float* Dd, float* Z) {
     *Aa = p.cy * p.sA;
     *Sa = fmaf(-4.0f * p.sy, p.s2A, 2.0f * p.dys);
     *P = p.cy * p.cA;
     *Dd = -p.sy * p.sA;
     *Z = fmaf(-4.0f * p.cy, p.s2A, 2.0f * p.dyc);
+  }
+  // all 4 pairs of a centre: t[5p .. 5p+4] = A_a, S_a, P, Dd, Z (warp-uniform fast form);
+  // `all` = every lane of the warp calls this (else the general form, no vote)
+  __device__ __forceinline__ static void pairs_bwd4(const C& c, const float (&A)[4], const float (&S)[4], float beta,
+                                                    float (&t)[20]) {
+    const float mA = fmaxf(fmaxf(fabsf(A[0]), fabsf(A[1])), fmaxf(fabsf(A[2]), fabsf(A[3])));
+    const float mS = fmaxf(fmaxf(fabsf(S[0]), fabsf(S[1])), fmaxf(fabsf(S[2]), fabsf(S[3])));
+    if (FDSDF_PAIR_FAST && __all_sync(0xffffffffu, mA <= FAST_A && mS <= FAST_S)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        bwd_from(pre_fast(c, A[q], S[q]), &t[5 * q], &t[5 * q + 1], &t[5 * q + 2], &t[5 * q + 3], &t[5 * q + 4]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        pair_bwd(c, A[q], S[q], beta, &t[5 * q], &t[5 * q + 1], &t[5 * q + 2], &t[5 * q + 3], &t[5 * q + 4]);
+    }
   }
 };
 
@@ -125,6 +201,17 @@ struct Act<ACT_SOFTPLUS> {
                                                   float* Sa) {
     const P2 p = pre(c, A, S, beta);
     fwd_from(c, p, beta, Aa, Sa);
+  }
+  __device__ __forceinline__ static void pairs_fwd4(const C& c, const float (&A)[4], const float (&S)[4], float beta,
+                                                    float (&o)[8]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) pair_fwd(c, A[q], S[q], beta, &o[2 * q], &o[2 * q + 1]);
+  }
+  __device__ __forceinline__ static void pairs_bwd4(const C& c, const float (&A)[4], const float (&S)[4], float beta,
+                                                    float (&t)[20]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      pair_bwd(c, A[q], S[q], beta, &t[5 * q], &t[5 * q + 1], &t[5 * q + 2], &t[5 * q + 3], &t[5 * q + 4]);
   }
   __device__ __forceinline__ static void pair_bwd(const C& c, float A, float S, float beta, float* Aa,
                                                   float* Sa, float* P, float* Dd, float* Z) {

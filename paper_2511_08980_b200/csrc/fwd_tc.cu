@@ -313,12 +313,13 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           *zg4(c, 0, 2) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
         }
         float o[8];
-#pragma unroll
-        for (int p = 0; p < 8; ++p) o[p] = 0.f;
-        if (mok) {
+        {  // every lane (the pair maps vote on their fast form); rows past the width give 0
           const typename AF::C cc = AF::centre(z0, beta);
+          AF::pairs_fwd4(cc, Av, Sv, beta, o);
+          if (!mok) {
 #pragma unroll
-          for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &o[2 * p], &o[2 * p + 1]);
+            for (int p = 0; p < 8; ++p) o[p] = 0.f;
+          }
         }
         skip_pairs(0, ci, o);
         float o4[4] = {o[0], o[1], o[2], o[3]};
@@ -563,12 +564,13 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               *zg4(c, l, 2) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
             }
             float o[8];
-#pragma unroll
-            for (int p = 0; p < 8; ++p) o[p] = 0.f;
-            if (mok) {
+            {  // every lane (the pair maps vote on their fast form); rows past the width give 0
               const typename AF::C cc = AF::centre(z0, beta);
+              AF::pairs_fwd4(cc, Av, Sv, beta, o);
+              if (!mok) {
 #pragma unroll
-              for (int p = 0; p < 4; ++p) AF::pair_fwd(cc, Av[p], Sv[p], beta, &o[2 * p], &o[2 * p + 1]);
+                for (int p = 0; p < 8; ++p) o[p] = 0.f;
+              }
             }
             skip_pairs(l, ci, o);
             if (last) {

@@ -23,9 +23,11 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
     const uint32_t a = smem_u32(base);
     base += (1024 - (a & 1023)) & 1023;
   }
+  // MN-major: N may be a partial swizzle atom (N % 64 != 0): the B pieces take whole 64-column atoms
+  const int NA = mn ? (N + 63) / 64 * 64 : N;
   unsigned char* As = base;
   unsigned char* Bs = As + 3 * M * 128;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + 3 * N * 128);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + 3 * NA * 128);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
   const int tid = threadIdx.x, warp = tid >> 5;
   const int MH = M / 128;
@@ -43,7 +45,7 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
   const uint32_t tbase = *tslot;
   const uint32_t idesc = mn ? tc::idesc_bf16(128, N, 1, 1) : tc::idesc_bf16(128, N);
   // MN-major strides: atoms along MN are 1024 B apart, along K (M/64)*1024 resp. (N/64)*1024
-  const uint32_t a_mn = 1024, a_k = (uint32_t)(M / 64) * 1024, b_mn = 1024, b_k = (uint32_t)(N / 64) * 1024;
+  const uint32_t a_mn = 1024, a_k = (uint32_t)(M / 64) * 1024, b_mn = 1024, b_k = (uint32_t)(NA / 64) * 1024;
   const int q0 = nprod == 1 ? 5 : (nprod == 3 ? 3 : 0);
 
   for (int kc = 0; kc < K / 64; ++kc) {
@@ -58,9 +60,9 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
     for (int i = tid; i < N * 64; i += 256) {
       const int r = i >> 6, k = i & 63;
       const tc::Bf3 s = tc::split3(B[(size_t)r * K + kc * 64 + k]);
-      const uint32_t o = mn ? tc::sw128mn_off(r, k, N) : tc::sw128_off(r, k, N);
+      const uint32_t o = mn ? tc::sw128mn_off(r, k, NA) : tc::sw128_off(r, k, N);
 #pragma unroll
-      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * N * 128 + o) = s.p[p];
+      for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(Bs + p * NA * 128 + o) = s.p[p];
     }
     fence_proxy_async();
     __syncthreads();
@@ -72,11 +74,11 @@ __global__ void __launch_bounds__(256, 1) tcprobe_kernel(const float* __restrict
             uint64_t ad, bd;
             if (!mn) {
               ad = tc::sdesc_sw128(smem_u32(As + tc::prod_a(q) * M * 128 + h * 128 * 128 + s * 32));
-              bd = tc::sdesc_sw128(smem_u32(Bs + tc::prod_b(q) * N * 128 + s * 32));
+              bd = tc::sdesc_sw128(smem_u32(Bs + tc::prod_b(q) * NA * 128 + s * 32));
             } else {
               // K step s = 16 K = 2 atoms along K; M-half h = 2 atoms along M
               const uint32_t aa = smem_u32(As + tc::prod_a(q) * M * 128 + 2 * s * a_k + 2 * h * a_mn);
-              const uint32_t bb = smem_u32(Bs + tc::prod_b(q) * N * 128 + 2 * s * b_k);
+              const uint32_t bb = smem_u32(Bs + tc::prod_b(q) * NA * 128 + 2 * s * b_k);
               ad = tc::sdesc_sw128_mn(aa, a_mn, a_k);
               bd = tc::sdesc_sw128_mn(bb, b_mn, b_k);
             }
@@ -110,8 +112,8 @@ extern "C" fdsdf_status fdsdf_selftest_mma(const float* d_W, const float* d_B, f
   if (!d_W || !d_B || !d_D) return FDSDF_E_INVALID;
   if (M < 128 || M > 256 || M % 128 || N < 16 || N > 256 || N % 16 || K < 64 || K % 64) return FDSDF_E_INVALID;
   if (nprod != 1 && nprod != 3 && nprod != 6) return FDSDF_E_INVALID;
-  if (mn_major < 0 || mn_major > 1 || (mn_major && (N % 64))) return FDSDF_E_INVALID;
-  const size_t smem = 3 * (size_t)(M + N) * 128 + 64 + 1024;
+  if (mn_major < 0 || mn_major > 1) return FDSDF_E_INVALID;
+  const size_t smem = 3 * (size_t)(M + (N + 63) / 64 * 64) * 128 + 64 + 1024;
   cudaError_t e = cudaFuncSetAttribute(tcprobe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return FDSDF_E_CUDA;
   tcprobe_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(d_W, d_B, d_D, M, N, K, nprod, mn_major);

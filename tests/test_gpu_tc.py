@@ -64,10 +64,12 @@ def test_mma_bf16x6_is_fp32_accurate(M, N, K):
     assert err1 > 100.0
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (128, 64, 64), (256, 128, 256), (128, 192, 128)])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (128, 64, 64), (256, 128, 256), (128, 192, 128),
+                                   (128, 80, 128), (256, 160, 128), (128, 240, 64), (128, 16, 64)])
 def test_mma_mn_major(M, N, K):
     """MN-major operands (LBO = stride between swizzle atoms along M/N, SBO = along K), the
-    layout of the weight-gradient kernel."""
+    layout of the weight-gradient kernel and of the forward kernels' B operand; N not a multiple
+    of the 64-column swizzle atom (a partial last atom) is the backward's N = 80 / 160."""
     D, ref, scale = _run(M, N, K, 6, seed=7, mn=1)
     err = np.max(np.abs(D - ref) / (scale * 2.0 ** -24))
     print("mn-major", M, N, K, "err ulps", err)
