@@ -166,8 +166,7 @@ enum {
                                 /* an FFMA-only network -> FDSDF_E_UNSUPPORTED.               */
 };
 /* Environment read at create time: FDSDF_MAX_SM=k (k >= 2) caps the persistent grids at k
- * SMs (GPU sharing; the tests use it to run many tiles per CTA at oracle-sized inputs);
- * FDSDF_PAIR=1 selects the CTA-pair forward kernels.                        */
+ * SMs (GPU sharing; the tests use it to run many tiles per CTA at oracle-sized inputs).    */
 fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_centers,
                           uint32_t flags, fdsdf_ctx** out);
 

@@ -10,8 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfdsdf.so")
 BUILD = os.path.join(ROOT, "build")
-SOURCES = ["api.cu", "fwd.cu", "bwd.cu", "wgrad.cu", "tcprobe.cu", "fwd_tc.cu", "bwd_tc.cu", "wgrad_tc.cu", "train.cu", "fwd_tc2.cu"]
-HEADERS = ["common.cuh", "act.cuh", "tile.cuh", "kernels.cuh", "tc.cuh", "fdepi.cuh", "tcmlp.cuh", "tcpair.cuh"]
+SOURCES = ["api.cu", "fwd.cu", "bwd.cu", "wgrad.cu", "tcprobe.cu", "fwd_tc.cu", "bwd_tc.cu", "wgrad_tc.cu", "train.cu"]
+HEADERS = ["common.cuh", "act.cuh", "tile.cuh", "kernels.cuh", "tc.cuh", "fdepi.cuh", "tcmlp.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("FDSDF_NVCC_EXTRA", "").split()  # debug builds only (e.g. -DFDSDF_PHASE_TIMING)
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -92,7 +92,6 @@ struct fdsdf_ctx {
   unsigned* dflags = nullptr;
   // tensor-core (tcgen05 bf16x6) forward
   bool tc = false;
-  bool pair = false;              // CTA-pair (cta_group::2) forward kernels
   bool tcf = false;               // tensor-core forward (fwd_tc.cu): the tensor path, or the
                                   // hybrid path of 512-wide / skip-layer networks
   bool tcw = false;               // tensor-core weight gradient (wgrad_tc.cu): ditto
@@ -276,12 +275,6 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     if (ok_tc && !(flags & FDSDF_CREATE_FFMA)) {
       c->tc = true;
       c->mpad = mp_tc;
-      // CTA-pair forward kernels (fwd_tc2.cu): opt-in with FDSDF_PAIR=1 in the environment.
-      // They overlap the MMA phase of one half-tile with the epilogue of the other, but the
-      // cross-CTA operand hand-off (cluster-scope proxy fence + release per slot-layer, remote
-      // st.shared::cluster) costs more than the overlap saves on B200 today.
-      const char* ev = getenv("FDSDF_PAIR");
-      c->pair = mp_tc == 256 && c->L >= 3 && ev && ev[0] == '1';
     }
     // networks the full tensor path does not cover (512-wide layers, the skip layer) still run
     // their forward and weight gradient on the tensor cores when the padded width is a tcgen05
@@ -445,17 +438,6 @@ static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t str
   a.wimg = c->fimg;
   a.cinfo = c->cinfo;
   const int64_t n = a.n;
-  if (c->pair) {  // CTA-pair kernels: two half-tile slots in flight per pair
-    a.ntiles = (n + fwd_tc2_tile_centres(1) - 1) / fwd_tc2_tile_centres(1);
-    const int g1 = 2 * (int)std::min<int64_t>(c->nsm / 2, a.ntiles);
-    cudaError_t e = pairs_only ? cudaSuccess
-                               : run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc2(a, 1, g1, strm); });
-    if (e != cudaSuccess) return e;
-    a.ntiles = (n + fwd_tc2_tile_centres(2) - 1) / fwd_tc2_tile_centres(2);
-    const int g2 = 2 * (int)std::min<int64_t>(c->nsm / 2, a.ntiles);
-    c->last_fgrid = g2;
-    return run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd_tc2(a, 2, g2, strm); });
-  }
   a.ntiles = (n + fwd_tc_tile_centres(1, c->mpad) - 1) / fwd_tc_tile_centres(1, c->mpad);
   const int g1 = (int)std::min<int64_t>(c->nsm, a.ntiles);
   cudaError_t e = pairs_only ? cudaSuccess

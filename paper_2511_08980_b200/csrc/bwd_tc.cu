@@ -30,6 +30,13 @@ namespace fdsdf {
 #ifndef BWD_TC_NEPI
 #define BWD_TC_NEPI 16
 #endif
+// unroll of the per-centre loops of phases A and B: 1 keeps them rolled (the per-centre carry
+// arrays then live in local memory); CPE (4) unrolls them, so the carries stay in registers and
+// the loads of later centres can be hoisted
+#ifndef BWD_TC_UNROLL
+#define BWD_TC_UNROLL 1
+#endif
+constexpr int kBwdUnroll = BWD_TC_UNROLL;
 // B / D column of (centre cl, adjoint column j) = 8 j + cl: the SW128 row group of column j is
 // j itself, so each thread writes a centre's ten B columns at one base offset plus compile-time
 // offsets j * 1024 (no per-element swizzle arithmetic)
@@ -289,9 +296,10 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       for (int l = pipe_top ? L - 3 : L - 2; l >= 0; --l) {
         const bool top = (l == L - 2);
         const int M = net.width[l + 1];
-        const float om = net.omega[l];
         const bool mok = m < M;
-        const float wl = (top && mok) ? wlast : 0.f;
+        // omega_l: in the image of the GEMM that produced X (pack_tc_kernel), or (top layer without
+        // an MMA) in its last-layer weight
+        const float wl = (top && mok) ? wlast * net.omega[l] : 0.f;
         float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
         const float db_l = r_db[l];  // local-memory read issued here, consumed after phase B
         constexpr bool CARRY = BWD_TC_CARRY;
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
         };
         {
           Zq qn = ldq(0);
-#pragma unroll 1
+#pragma unroll kBwdUnroll
           for (int i = 0; i < CPE; ++i) {
             const Zq q = qn;
             qn = ldq(i + 1);
@@ -439,7 +447,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
           ++nd;
           tc::fence_after();
         }
-#pragma unroll 1
+#pragma unroll kBwdUnroll
         for (int i = 0; i < CPE; ++i) {
           const int cl = eg + EG * i;
           const int64_t c = c0 + cl;
@@ -498,8 +506,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             for (int p = 0; p < 4; ++p) {
               const float P = t[5 * p + 2], Dd = t[5 * p + 3], Z = t[5 * p + 4];
               const float XA = X[2 + 2 * p], XS = X[3 + 2 * p];
-              const float dA = om * fmaf(XA, P, 2.0f * XS * Dd);
-              const float dS = om * fmaf(0.5f * XA, Dd, XS * P);
+              const float dA = fmaf(XA, P, 2.0f * XS * Dd);
+              const float dS = fmaf(0.5f * XA, Dd, XS * P);
               zbar = fmaf(XA, Dd, fmaf(XS, Z, zbar));
               dl[2 + 2 * p] = dA;
               dl[3 + 2 * p] = dS;
@@ -514,8 +522,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
             }
             const float Xc = X[0], Xt = X[1];
             const float zb = fmaf(Xc, s1, fmaf(s2tr, Xt, zbar));
-            dl[0] = om * zb;
-            dl[1] = om * s1 * Xt;
+            dl[0] = zb;
+            dl[1] = s1 * Xt;
             if (l == 0) {  // a^{-1}: centre -> x0, tangent -> r
               w0p[0] = fmaf(dl[0], sd[16], fmaf(dl[1], r0, w0p[0]));
               w0p[1] = fmaf(dl[0], sd[17], fmaf(dl[1], r1, w0p[1]));

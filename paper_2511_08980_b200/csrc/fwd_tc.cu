@@ -36,6 +36,11 @@ namespace fdsdf {
 #ifndef FWD_TC_NEPI
 #define FWD_TC_NEPI 16
 #endif
+// unroll of the per-centre epilogue loop (1 = rolled)
+#ifndef FWD_TC_UNROLL
+#define FWD_TC_UNROLL 1
+#endif
+constexpr int kFwdUnroll = FWD_TC_UNROLL;
 // GEMM columns per tile (mode 1: N/4 centres, mode 2: N/8 centres); with FWD_TC_NEPI the
 // epilogue warps (a multiple of 4 x M-halves whose centre groups divide the tile)
 #ifndef FWD_TC_N
@@ -87,8 +92,12 @@ size_t tc_wimg_bytes(int mpad, int ngemm) { return (size_t)(ngemm > 0 ? ngemm : 
 int fwd_tc_tile_centres(int mode, int mpad) { return mode == 1 ? fwd_tc_n(mpad) / 4 : fwd_tc_n(mpad) / 8; }
 
 // ----------------------------------------------------------------------------- weight images
-// image[g][kc][h][piece < WP][sw128 128 rows x 64 k]: forward A operand = W_l (rows = output
-// neuron m, K = input neuron k); backward A operand = W_l^T (rows = k, K = m).
+// image[g][kc][h][piece < WP][sw128 128 rows x 64 k]: forward A operand = omega_l W_l (rows =
+// output neuron m, K = input neuron k); backward A operand = omega_{l-1} W_l^T (rows = k, K = m),
+// l = g + 1.  The SIREN frequency of the layer whose pre-activation the GEMM produces (forward:
+// z_l = omega_l (W_l a + b_l); backward: delta_{l-1} = omega_{l-1} (...) (W_l^T delta_l)) is folded
+// into the image (one fp32 rounding of omega W, <= 2^-24 relative), so the epilogues never scale
+// the accumulator; omega = 1 for softplus.
 __global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char* bimg) {
   const int mp = net.mpad;
   const int KC = mp / 64, MH = mp / 128;
@@ -103,13 +112,13 @@ __global__ void pack_tc_kernel(const Net net, unsigned char* fimg, unsigned char
     const int h = r >> 7, rr = r & 127, kc = k >> 6, kk = k & 63;
     const size_t off = (size_t)g * per_layer + ((size_t)kc * MH + h) * (tc::WP * 16384) + tc::sw128_off(rr, kk, 128);
     {
-      const float v = (r < M && k < K) ? W[(size_t)r * K + k] : 0.f;  // forward: W[m = r][k]
+      const float v = (r < M && k < K) ? net.omega[l] * W[(size_t)r * K + k] : 0.f;  // forward: W[m = r][k]
       const tc::Bf3 s = tc::split3(v);
 #pragma unroll
       for (int p = 0; p < tc::WP; ++p) *reinterpret_cast<__nv_bfloat16*>(fimg + off + p * 16384) = s.p[p];
     }
     if (bimg) {
-      const float v = (k < M && r < K) ? W[(size_t)k * K + r] : 0.f;  // backward: W^T[k = r][m = k]
+      const float v = (k < M && r < K) ? net.omega[g] * W[(size_t)k * K + r] : 0.f;  // backward: W^T[k = r][m = k]
       const tc::Bf3 s = tc::split3(v);
 #pragma unroll
       for (int p = 0; p < tc::WP; ++p) *reinterpret_cast<__nv_bfloat16*>(bimg + off + p * 16384) = s.p[p];
@@ -407,7 +416,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
         const float om = net.omega[l];
         const bool mok = m < M;
         const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
-        const float bias_l = (MODE == 1 && l > 0 && mok) ? net.b[l][m] : 0.f;  // once per layer
+        // omega_l b_l (the image carries omega_l W_l), once per layer
+        const float bias_l = (MODE == 1 && l > 0 && mok) ? om * net.b[l][m] : 0.f;
         // last layer: sum over this warp's 32 neurons of w_L[m] * out_j, one slot per centre
         auto reduce4 = [&](int cl, float p0, float p1, float p2, float p3) {
           float pv[4] = {wl * p0, wl * p1, wl * p2, wl * p3};
@@ -475,7 +485,7 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
           ptimer.after_wait();
           tc::fence_after();
         }
-#pragma unroll 1
+#pragma unroll kFwdUnroll
         for (int i = 0; i < CPEs; ++i) {
           const int cl = sp * CPSPL + eg + C::EG * i;  // centre slot in the tile
           const int64_t c = c0 + cl;
@@ -506,10 +516,10 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               // register selects, not a runtime index (which would put v in local memory)
               const bool hi = (cl & 1) != 0;
               if (mok) {
-                z = om * ((hi ? v[4] : v[0]) + bias_l);
-                t0 = om * (hi ? v[5] : v[1]);
-                t1 = om * (hi ? v[6] : v[2]);
-                t2 = om * (hi ? v[7] : v[3]);
+                z = (hi ? v[4] : v[0]) + bias_l;
+                t0 = hi ? v[5] : v[1];
+                t1 = hi ? v[6] : v[2];
+                t2 = hi ? v[7] : v[3];
               }
             }
             if (valid) {
@@ -554,8 +564,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
               if (mok) {
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
-                  Av[p] = om * v[2 * p];
-                  Sv[p] = om * v[2 * p + 1];
+                  Av[p] = v[2 * p];
+                  Sv[p] = v[2 * p + 1];
                 }
               }
             }

@@ -138,9 +138,6 @@ cudaError_t launch_pack_tc(const Net& net, unsigned char* fwd_img, unsigned char
 cudaError_t launch_fwd_tc(const FwdArgs& a, int mode, int grid, cudaStream_t st);
 int fwd_tc_tile_centres(int mode, int mpad);        // mode 1: N/4, mode 2: N/8 centres
 bool tc_fwd_supported(int mpad);                    // tensor forward (fwd_tc.cu) for this width
-// CTA-pair variants (fwd_tc2.cu): mpad 256, L >= 3; grid = 2 x clusters
-cudaError_t launch_fwd_tc2(const FwdArgs& a, int mode, int grid, cudaStream_t st);
-int fwd_tc2_tile_centres(int mode);                 // 32 (mode 1) / 16 (mode 2) per pair tile
 cudaError_t launch_bwd_tc(const BwdArgs& a, int grid, cudaStream_t st);
 int bwd_tc_tile_centres();                          // 8
 int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
