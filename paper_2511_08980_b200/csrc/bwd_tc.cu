@@ -25,7 +25,7 @@ namespace fdsdf {
 // L2 prefetch of the stored forward pre-activations: 1 = one layer of one tile (8 x 12 KB bulk
 // prefetches) issued one MMA pass before phase A reads it; 0 = none
 #ifndef BWD_TC_PREFETCH
-#define BWD_TC_PREFETCH 1
+#define BWD_TC_PREFETCH 0
 #endif
 #ifndef BWD_TC_NEPI
 #define BWD_TC_NEPI 16
@@ -37,6 +37,17 @@ namespace fdsdf {
 #define BWD_TC_UNROLL 1
 #endif
 constexpr int kBwdUnroll = BWD_TC_UNROLL;
+// stores of delta / the layer activations (read once, by the weight-gradient kernel after the
+// whole backward): 1 = streaming (st.global.cs, evict-first), 0 = default caching
+#ifndef BWD_TC_STCS
+#define BWD_TC_STCS 1
+#endif
+__device__ __forceinline__ void bwd_st(float* p, float v) {
+  if (BWD_TC_STCS)
+    __stcs(p, v);
+  else
+    *p = v;
+}
 // B / D column of (centre cl, adjoint column j) = 8 j + cl: the SW128 row group of column j is
 // j itself, so each thread writes a centre's ten B columns at one base offset plus compile-time
 // offsets j * 1024 (no per-element swizzle arithmetic)
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
       FDSDF_ASSERT(c >= 0 && c < a.n && ltop >= 0 && ltop < nh);
       float* dp = a.del + ((size_t)ltop * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
-      for (int j = 0; j < NCOLB; ++j) dp[j * MPAD] = dl[j];
+      for (int j = 0; j < NCOLB; ++j) bwd_st(dp + j * MPAD, dl[j]);
       float v = 0.f;
 #pragma unroll
       for (int j = 0; j < NCOLB; ++j) v = fmaf(dL[j], pv[j], v);
@@ -380,7 +391,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
                 FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
                 float* ap = a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
-                for (int j = 0; j < NCOLB; ++j) ap[j * MPAD] = pv[j];
+                for (int j = 0; j < NCOLB; ++j) bwd_st(ap + j * MPAD, pv[j]);
               }
               if (top) {
                 const float* sd = sds + cl * 20;
@@ -535,7 +546,7 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
               FDSDF_ASSERT(c >= 0 && c < a.n && l >= 1 && l < nh);
               float* dp = a.del + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
-              for (int j = 0; j < NCOLB; ++j) dp[j * MPAD] = dl[j];
+              for (int j = 0; j < NCOLB; ++j) bwd_st(dp + j * MPAD, dl[j]);
             }
           }
           if (l >= 1) put_b10(cl, dl);

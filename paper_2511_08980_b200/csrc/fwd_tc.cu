@@ -510,16 +510,13 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
                 t2 = om * w2;
               }
             } else {
-              float v[8];
-              tc_ld_sum8<C>(taddr, (cl >> 1) * 8, v);
-              // centre cl's 4 columns are the half (cl & 1) of the 8 loaded (warp-uniform):
-              // register selects, not a runtime index (which would put v in local memory)
-              const bool hi = (cl & 1) != 0;
+              float v[4];
+              tc_ld_sum4<C>(taddr, cl * 4, v);  // centre cl's 4 columns
               if (mok) {
-                z = (hi ? v[4] : v[0]) + bias_l;
-                t0 = hi ? v[5] : v[1];
-                t1 = hi ? v[6] : v[2];
-                t2 = hi ? v[7] : v[3];
+                z = v[0] + bias_l;
+                t0 = v[1];
+                t1 = v[2];
+                t2 = v[3];
               }
             }
             if (valid) {

@@ -18,6 +18,10 @@
 
 #include "tc.cuh"
 
+#ifndef FDSDF_WPIECES_PER_STAGE
+#define FDSDF_WPIECES_PER_STAGE 1
+#endif
+
 namespace fdsdf {
 
 template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1, int BMN_ = 0>
@@ -27,9 +31,14 @@ struct TcCfg {
   static constexpr int MH = MPAD / 128;         // tcgen05 M-halves (M = 128 each)
   static constexpr int KC = MPAD / 64;          // K chunks (one 128-byte swizzle row each)
   // weight stage (kc, h): the three bf16 pieces of 128 rows x 64 K (48 KB), 2-deep ring
-  static constexpr int IMGSTAGE = tc::WP * 128 * 128;  // stage stride in the packed image
-  static constexpr int STAGE = IMGSTAGE;               // weight stage in shared memory
-  static constexpr int NST = 2;
+  static constexpr int IMGSTAGE = tc::WP * 128 * 128;  // (kc, h) block stride in the packed image
+  // weight ring: WPS pieces per stage (3: a whole (kc, h) block of 48 KB, 2-deep; 1: one 16 KB
+  // piece, 6-deep -- the same 96 KB, but a stage is refilled as soon as its piece's MMAs are done
+  // instead of after all three, so more of the L2 -> smem weight stream is in flight)
+  static constexpr int WPS = FDSDF_WPIECES_PER_STAGE;
+  static constexpr int STAGE = WPS * 128 * 128;        // weight stage in shared memory
+  static constexpr int NST = 6 / WPS;
+  static_assert(WPS == 1 || WPS == 3, "whole blocks or single pieces");
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
   static constexpr int BKC = 3 * N * 128;       // one K chunk of B
   // column splits: the tile's N columns are NSPLIT independent MMA passes of NS columns each,
@@ -157,14 +166,16 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
     for (int gi = 0; gi < ngemm * C::NSPLIT; ++gi) {  // each layer once per column split
       const int g = reverse ? ngemm - 1 - gi / C::NSPLIT : gi / C::NSPLIT;
       for (int kc = 0; kc < C::KC; ++kc)
-        for (int h = 0; h < C::MH; ++h, ++it) {
-          const int s = (int)(it % C::NST);
-          const uint32_t ph = (it / C::NST) & 1u;
-          mbar_wait_backoff(&b.wempty[s], ph ^ 1u);
-          mbar_arrive_expect_tx(&b.wfull[s], C::STAGE);
-          bulk_g2s(Ws + s * C::STAGE, img + (((size_t)g * C::KC + kc) * C::MH + h) * C::IMGSTAGE, C::STAGE,
-                   &b.wfull[s]);
-        }
+        for (int h = 0; h < C::MH; ++h)
+          for (int p = 0; p < tc::WP; p += C::WPS, ++it) {
+            const int s = (int)(it % C::NST);
+            const uint32_t ph = (it / C::NST) & 1u;
+            mbar_wait_backoff(&b.wempty[s], ph ^ 1u);
+            mbar_arrive_expect_tx(&b.wfull[s], C::STAGE);
+            bulk_g2s(Ws + s * C::STAGE,
+                     img + (((size_t)g * C::KC + kc) * C::MH + h) * C::IMGSTAGE + (size_t)p * 16384, C::STAGE,
+                     &b.wfull[s]);
+          }
     }
 }
 
@@ -202,38 +213,54 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
 #endif
       tc::fence_after();
       for (int kc = 0; kc < C::KC; ++kc)
-        for (int h = 0; h < C::MH; ++h, ++it) {
-          const int s = (int)(it % C::NST);
-          const uint32_t ph = (it / C::NST) & 1u;
-          TC_MMA_T(tw, mbar_wait(&b.wfull[s], ph));
-          tc::fence_after();
-          const uint32_t wa = smem_u32(Ws + s * C::STAGE);
+        for (int h = 0; h < C::MH; ++h) {
           const uint32_t ba = smem_u32(Bs + kc * C::BKC + sp * 3 * C::NS * 128);
           const uint32_t d = tbase + h * C::DH + sp * C::RANGES * C::NS;
-          if constexpr (C::RANGES == 3) {
+          // piece-major within the (kc, h) block: all K steps of a0, then of a1, then of a2 (the
+          // first product into every range is a0's at kc = sub = 0, which overwrites)
 #pragma unroll
-            for (int sub = 0; sub < 4; ++sub) {
-              const uint64_t bd = C::BMN ? tc::sdesc_sw128_mn(ba + sub * 2 * C::BSBO, 1024, C::BSBO)
-                                         : tc::sdesc_sw128(ba + sub * 32);
-              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), bd, id3, (kc | sub) != 0 ? 1u : 0u);
-              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), bd, id2, 1u);
-              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), bd, id1, 1u);
+          for (int p = 0; p < tc::WP; ++p) {
+            uint32_t wa;
+            int s = 0;
+            if (C::WPS == 1 || p == 0) {
+              s = (int)(it % C::NST);
+              const uint32_t ph = (it / C::NST) & 1u;
+              TC_MMA_T(tw, mbar_wait(&b.wfull[s], ph));
+              tc::fence_after();
+              ++it;
+            } else {
+              s = (int)((it - 1) % C::NST);
             }
-          } else {
-            // a0 . [b0|b1] and a1 . [b0|b1] (N = 2N: ranges 0, 1), then a0 . b2 and a2 . b0
-            // (N = N: range 0) -- the six products, four A reads per K step instead of six
+            wa = smem_u32(Ws + s * C::STAGE) + (C::WPS == 1 ? 0 : p * 16384);
+            if constexpr (C::RANGES == 3) {
+              // a0 . [b0|b1|b2] (N = 3N: ranges 0, 1, 2), a1 . [b0|b1] (ranges 0, 1), a2 . b0 (range 0)
+              const uint32_t id = p == 0 ? id3 : (p == 1 ? id2 : id1);
 #pragma unroll
-            for (int sub = 0; sub < 4; ++sub) {
+              for (int sub = 0; sub < 4; ++sub) {
+                const uint64_t bd = C::BMN ? tc::sdesc_sw128_mn(ba + sub * 2 * C::BSBO, 1024, C::BSBO)
+                                           : tc::sdesc_sw128(ba + sub * 32);
+                tc::mma_bf16_w(d, tc::sdesc_sw128(wa + sub * 32), bd, id, (p | kc | sub) != 0 ? 1u : 0u);
+              }
+            } else {
+              // a0 . [b0|b1] (N = 2N: ranges 0, 1) and a0 . b2, a1 . [b0|b1], a2 . b0 (range 0): the
+              // six products, four A reads per K step instead of six
               static_assert(!C::BMN, "two-range issue: K-major B only");
-              const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);
-              const uint64_t b2 = tc::sdesc_sw128(ba + 2 * C::NS * 128 + sub * 32);
-              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b01, id2, (kc | sub) != 0 ? 1u : 0u);
-              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 1 * 16384 + sub * 32), b01, id2, 1u);
-              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 0 * 16384 + sub * 32), b2, id1, 1u);
-              tc::mma_bf16_w(d, tc::sdesc_sw128(wa + 2 * 16384 + sub * 32), b01, id1, 1u);
+#pragma unroll
+              for (int sub = 0; sub < 4; ++sub) {
+                const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);
+                const uint64_t a = tc::sdesc_sw128(wa + sub * 32);
+                if (p == 0) {
+                  tc::mma_bf16_w(d, a, b01, id2, (kc | sub) != 0 ? 1u : 0u);
+                  tc::mma_bf16_w(d, a, tc::sdesc_sw128(ba + 2 * C::NS * 128 + sub * 32), id1, 1u);
+                } else if (p == 1) {
+                  tc::mma_bf16_w(d, a, b01, id2, 1u);
+                } else {
+                  tc::mma_bf16_w(d, a, b01, id1, 1u);
+                }
+              }
             }
+            if (C::WPS == 1 || p == tc::WP - 1) tc::mma_commit_w(&b.wempty[s]);
           }
-          tc::mma_commit_w(&b.wempty[s]);
         }
       tc::mma_commit_w(&b.dfull[sp]);
 #ifdef FDSDF_PHASE_TIMING
@@ -353,11 +380,21 @@ __device__ __forceinline__ void tc_ld_sum8(uint32_t taddr, int col, float (&v)[8
   float r1[8], r2[8];
   const int sp = col / C::NS, nl = col % C::NS;  // 8 columns never straddle a split
   const uint32_t t0 = taddr + sp * 3 * C::NS + nl;
-  tc::tmem_ld8(t0, v);
-  tc::tmem_ld8(t0 + C::NS, r1);
-  tc::tmem_ld8(t0 + 2 * C::NS, r2);
+  tc::tmem_ld8x3(t0, t0 + C::NS, t0 + 2 * C::NS, v, r1, r2);
 #pragma unroll
   for (int j = 0; j < 8; ++j) v[j] += r1[j] + r2[j];
+}
+
+template <class C>
+__device__ __forceinline__ void tc_ld_sum4(uint32_t taddr, int col, float (&v)[4]) {
+  FDSDF_ASSERT(col >= 0 && col + 4 <= C::NSPLIT * C::NS);
+  static_assert(C::RANGES == 3, "three accumulator ranges");
+  float r1[4], r2[4];
+  const int sp = col / C::NS, nl = col % C::NS;  // 4 columns never straddle a split
+  const uint32_t t0 = taddr + sp * 3 * C::NS + nl;
+  tc::tmem_ld4x3(t0, t0 + C::NS, t0 + 2 * C::NS, v, r1, r2);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] += r1[j] + r2[j];
 }
 
 template <class C>

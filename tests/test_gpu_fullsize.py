@@ -157,3 +157,31 @@ def test_c3_full_size(path):
     assert np.isfinite(l1).all() and np.isfinite(g1).all()
     assert np.array_equal(g1, g2.cpu().numpy()) and np.array_equal(l1, l2.cpu().numpy())
     m.close()
+
+
+def test_c3_step_parity_first_rows():
+    """C3's loss (FD-NSH, (1, 100, 50, 1), den 1, h = 1e-2) and weight gradient on the first 1024
+    surface + 1024 uniform rows of the C3 batch against the fp64 C oracle, on the
+    default (hybrid) path and the FFMA path, with the frames the GPU drew (GIVEN mode for both
+    GPU steps and the oracle)."""
+    from paper_2511_08980_b200 import FDSDF
+    c = make_config("c3", 1024, 1024)
+    n = len(c["x"])
+    m = FDSDF(c["spec"], 0, max_centers=n)
+    assert m.path == "hybrid", m.path
+    ev = gpu_eval(m, c, denom=c["loss"]["denom"])
+    fr = ev["frames"]
+    o = ref_step(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frames=(fr[:, :3], fr[:, 3:]))
+    for path in (None, "ffma"):
+        mm = m if path is None else FDSDF(c["spec"], 0, max_centers=n, path=path)
+        grad, loss = mm.step(c["params"], c["x"], c["n_surface"], c["h"], c["loss"], frames=fr)
+        grad, loss = grad.cpu().numpy().astype(np.float64), loss.cpu().numpy()
+        lerr = np.abs(loss[:5] - o["loss"][:5]) / np.maximum(np.abs(o["loss"][:5]), 1e-30)
+        gerr = per_tensor_grad_errors(c["spec"], grad, o["grad"])
+        print("c3 first rows", mm.path, "lerr", lerr, "gerr max", gerr.max())
+        assert np.all(lerr[o["loss"][:5] != 0] <= LOSS_RTOL), lerr
+        assert loss[5] == o["loss"][5]
+        assert np.all(gerr <= GRAD_RTOL), gerr
+        if path is not None:
+            mm.close()
+    m.close()
