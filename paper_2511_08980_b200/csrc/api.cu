@@ -434,17 +434,24 @@ static void fill_fwd(fdsdf_ctx* c, FwdArgs& a, const float* d_x, int64_t n, cons
 // FD epilogue).  Sets a.ntiles per launch; records the mode-2 grid in c->last_fgrid.
 // pairs_only: skip mode 1 and reuse the centre info / centre pre-activations a previous call
 // left in the workspace (fdsdf_eval_hessian's 2nd and 3rd frame passes)
+// persistent grid of the tensor-core kernels: one CTA per SM, at most one per tile, and even
+// (they run as clusters of 2 sharing the weight stream, tcmlp.cuh FDSDF_WMC)
+static int tc_grid(const fdsdf_ctx* c, int64_t ntiles) {
+  const int64_t g = std::min<int64_t>(c->nsm, ntiles);
+  return (int)std::min<int64_t>(c->nsm & ~1, (g + 1) & ~1);
+}
+
 static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t strm, bool pairs_only = false) {
   a.wimg = c->fimg;
   a.cinfo = c->cinfo;
   const int64_t n = a.n;
   a.ntiles = (n + fwd_tc_tile_centres(1, c->mpad) - 1) / fwd_tc_tile_centres(1, c->mpad);
-  const int g1 = (int)std::min<int64_t>(c->nsm, a.ntiles);
+  const int g1 = tc_grid(c, a.ntiles);
   cudaError_t e = pairs_only ? cudaSuccess
                              : run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc(a, 1, g1, strm); });
   if (e != cudaSuccess) return e;
   a.ntiles = (n + fwd_tc_tile_centres(2, c->mpad) - 1) / fwd_tc_tile_centres(2, c->mpad);
-  const int g2 = (int)std::min<int64_t>(c->nsm, a.ntiles);
+  const int g2 = tc_grid(c, a.ntiles);
   c->last_fgrid = g2;
   return run_slot(c, FDSDF_KSLOT_FWD, strm, [&] { return launch_fwd_tc(a, 2, g2, strm); });
 }
@@ -662,7 +669,7 @@ static fdsdf_status step_impl(fdsdf_ctx* c, const float* d_params, const float* 
   if (c->tc) {
     b.wimg = c->bimg;
     b.ntiles = (n + bwd_tc_tile_centres() - 1) / bwd_tc_tile_centres();
-    bgrid = (int)std::min<int64_t>(c->nsm, b.ntiles);
+    bgrid = tc_grid(c, b.ntiles);
     nbslots = bgrid * bwd_tc_acc_slots(c->mpad);
     e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwd_tc(b, bgrid, strm); });
   } else {

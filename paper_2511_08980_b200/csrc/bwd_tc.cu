@@ -80,7 +80,7 @@ int bwd_tc_tile_centres() { return 8; }
 int bwd_tc_acc_slots(int mpad) { return BWD_TC_NEPI / (4 * (mpad / 128)); }  // accumulator slots per CTA (EG)
 
 template <int ACT, int MPAD>
-__global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const BwdArgs a) {
+__global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const BwdArgs a) {
   using C = BtcCfg<MPAD>;
   using AF = Act<ACT>;
   constexpr int N = C::N, MH = C::MH, CT = C::CT, EG = C::EG;
@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const Bwd
 #ifdef FDSDF_PHASE_TIMING
     long long t_tstart = 0, t_tstart_n = 0, t_top = 0, t_pa = 0;
 #endif
-    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, spar ^= 1u) {
+    const int64_t tend = tc_tile_end<C>(a.ntiles);
+    for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x, spar ^= 1u) {
       const int64_t c0 = tile * CT;
       // this tile's first MMA pass reads layer L-3; the next tile's top layer (computed during
       // this tile's passes) reads layer L-2 of that tile

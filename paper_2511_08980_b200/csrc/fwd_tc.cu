@@ -62,13 +62,18 @@ constexpr int fwd_tc_n(int mpad) { return mpad == 512 ? 32 : FWD_TC_N; }
 #define FWD_TC_BMN 1
 #endif
 constexpr int fwd_tc_bmn(int mpad) { return (FWD_TC_BMN && FWD_TC_NSPLIT == 1 && fwd_tc_n(mpad) % 64 == 0) ? 1 : 0; }
+// weight ring depth (16 KB single-piece stages): one more than the backward's 6 fits next to the
+// forward's 96 KB B operand
+#ifndef FWD_TC_NST
+#define FWD_TC_NST 6
+#endif
 template <int MPAD, int MODE>
 struct FtcCfg : TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
-                      FWD_TC_NSPLIT, fwd_tc_bmn(MPAD)> {
+                      FWD_TC_NSPLIT, fwd_tc_bmn(MPAD), FWD_TC_NST> {
   // TMEM stash (FWD_PIPE0): the next tile's layer-0 outputs, (MH x EG thread groups) x CPE x
   // columns per centre = MH x N columns
   using B = TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
-                  FWD_TC_NSPLIT, fwd_tc_bmn(MPAD)>;
+                  FWD_TC_NSPLIT, fwd_tc_bmn(MPAD), FWD_TC_NST>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
@@ -79,6 +84,7 @@ struct FtcCfg : TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n
   static constexpr int OFF_LV = OFF_CI + 2 * CI_N * 4;              // double [MAXC][NLOSS]
   static constexpr int OFF_BAR = OFF_LV + MAXC * NLOSS * 8;         // mbarriers + TMEM slot
   static constexpr int BYTES = OFF_BAR + tc_bars_bytes<B>() + 1024; // + alignment slack
+  static_assert(BYTES <= 232448, "shared memory per CTA");
 };
 
 bool tc_supported(int mpad, int skip) { return (mpad == 128 || mpad == 256) && skip < 0; }
@@ -137,7 +143,7 @@ cudaError_t launch_pack_tc(const Net& net, unsigned char* fimg, unsigned char* b
 // ----------------------------------------------------------------------------- the kernel
 
 template <int ACT, int MPAD, int MODE>
-__global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(const FwdArgs a) {
+__global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(const FwdArgs a) {
   using C = FtcCfg<MPAD, MODE>;
   using AF = Act<ACT>;
   constexpr int N = C::N, MH = C::MH;
@@ -401,7 +407,8 @@ __global__ void __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) fwd_tc_kernel(con
       }
     };
     if (MODE == 2) load_cinfo(blockIdx.x, cis0, et, C::NEPI * 32);
-    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, tpar ^= 1u) {
+    const int64_t tend = tc_tile_end<C>(a.ntiles);
+    for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x, tpar ^= 1u) {
       const int64_t c0 = tile * CT;
       float* red = red0 + tpar * C::RED_N;
       float* cis = cis0 + tpar * C::CI_N;

@@ -21,10 +21,52 @@
 #ifndef FDSDF_WPIECES_PER_STAGE
 #define FDSDF_WPIECES_PER_STAGE 1
 #endif
+// 1: the kernels run as clusters of 2 CTAs that share the weight stream -- each CTA bulk-copies
+// every other stage with .multicast::cluster into BOTH CTAs' rings, and every MMA issuer frees a
+// stage in both CTAs (multicast tcgen05.commit), so each SM pulls half the weight bytes from L2
+#ifndef FDSDF_WMC
+#define FDSDF_WMC 0
+#endif
+#if FDSDF_WMC
+#define FDSDF_TC_CLUSTER __cluster_dims__(2, 1, 1)
+#else
+#define FDSDF_TC_CLUSTER
+#endif
 
 namespace fdsdf {
 
-template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1, int BMN_ = 0>
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// every thread of every CTA of the cluster
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// bulk copy global -> the same shared-memory offset in every CTA of `mask`, complete_tx on the
+// mbarrier at the same offset in each of them
+__device__ __forceinline__ void bulk_g2s_mc(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
+                                            uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// whole-warp: arrive on the mbarrier at `bar`'s offset in every CTA of `mask` once the MMAs
+// issued so far are complete
+__device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1, int BMN_ = 0,
+          int NST_ = 6>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
@@ -37,8 +79,9 @@ struct TcCfg {
   // instead of after all three, so more of the L2 -> smem weight stream is in flight)
   static constexpr int WPS = FDSDF_WPIECES_PER_STAGE;
   static constexpr int STAGE = WPS * 128 * 128;        // weight stage in shared memory
-  static constexpr int NST = 6 / WPS;
+  static constexpr int NST = WPS == 1 ? NST_ : 2;  // ring depth in stages
   static_assert(WPS == 1 || WPS == 3, "whole blocks or single pieces");
+  static constexpr int MC = FDSDF_WMC ? 2 : 1;  // CTAs sharing the weight stream (cluster size)
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
   static constexpr int BKC = 3 * N * 128;       // one K chunk of B
   // column splits: the tile's N columns are NSPLIT independent MMA passes of NS columns each,
@@ -117,7 +160,7 @@ __device__ __forceinline__ uint32_t tc_setup(const TcBars& b) {
   if (tid == 0) {
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(&b.wfull[s], 1);
-      mbar_init(&b.wempty[s], 1);
+      mbar_init(&b.wempty[s], C::MC);  // freed by the MMA issuer of every CTA of the cluster
     }
     for (int s = 0; s < C::NSPLIT; ++s) {
       mbar_init(&b.bfull[s], C::NEPI);
@@ -128,6 +171,7 @@ __device__ __forceinline__ uint32_t tc_setup(const TcBars& b) {
   if (warp == 1) tc::tmem_alloc(b.tslot, C::TCOLS);
   tc::fence_before();
   __syncthreads();
+  if (C::MC > 1) cluster_sync_all();  // the peer's barriers are initialised before any multicast
   tc::fence_after();
   return *b.tslot;
 }
@@ -153,7 +197,19 @@ template <class C>
 __device__ __forceinline__ void tc_teardown(uint32_t tbase) {
   tc::fence_before();
   __syncthreads();
+  if (C::MC > 1) cluster_sync_all();  // no multicast copy / commit still targets this CTA
   if ((threadIdx.x >> 5) == 1) tc::tmem_dealloc(tbase, C::TCOLS);
+}
+
+// End of this CTA's tile loop (tile = blockIdx.x, + gridDim.x, ...): with a shared weight stream
+// both CTAs of a cluster must run the same number of tiles, so the odd CTA may get one tile index
+// >= ntiles (a tile of invalid centres: every store of the kernels checks c < n)
+template <class C>
+__device__ __forceinline__ int64_t tc_tile_end(int64_t ntiles) {
+  if (C::MC == 1) return ntiles;
+  const int64_t b0 = blockIdx.x & ~1u;
+  const int64_t iters = ntiles > b0 ? (ntiles - b0 + gridDim.x - 1) / gridDim.x : 0;
+  return b0 + iters * (int64_t)gridDim.x;
 }
 
 // Producer (one thread): stages of GEMM g, chunk kc, half h for every tile this CTA owns.
@@ -162,7 +218,9 @@ template <class C>
 __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm, int reverse, int64_t ntiles,
                                             unsigned char* Ws, const TcBars& b) {
   uint32_t it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+  const int64_t tend = tc_tile_end<C>(ntiles);
+  const uint32_t rank = C::MC > 1 ? cluster_ctarank() : 0u;
+  for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x)
     for (int gi = 0; gi < ngemm * C::NSPLIT; ++gi) {  // each layer once per column split
       const int g = reverse ? ngemm - 1 - gi / C::NSPLIT : gi / C::NSPLIT;
       for (int kc = 0; kc < C::KC; ++kc)
@@ -172,9 +230,11 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
             const uint32_t ph = (it / C::NST) & 1u;
             mbar_wait_backoff(&b.wempty[s], ph ^ 1u);
             mbar_arrive_expect_tx(&b.wfull[s], C::STAGE);
-            bulk_g2s(Ws + s * C::STAGE,
-                     img + (((size_t)g * C::KC + kc) * C::MH + h) * C::IMGSTAGE + (size_t)p * 16384, C::STAGE,
-                     &b.wfull[s]);
+            const unsigned char* src = img + (((size_t)g * C::KC + kc) * C::MH + h) * C::IMGSTAGE + (size_t)p * 16384;
+            if (C::MC == 1)
+              bulk_g2s(Ws + s * C::STAGE, src, C::STAGE, &b.wfull[s]);
+            else if ((it & 1u) == rank)  // this CTA's half of the stages, into both rings
+              bulk_g2s_mc(Ws + s * C::STAGE, src, C::STAGE, &b.wfull[s], (uint16_t)0x3);
           }
     }
 }
@@ -204,7 +264,8 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
 #else
 #define TC_MMA_T(acc, stmt) stmt;
 #endif
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+  const int64_t tend = tc_tile_end<C>(ntiles);
+  for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x)
     for (int gs = 0; gs < ngemm * C::NSPLIT; ++gs, ++nb) {
       const int sp = gs % C::NSPLIT;  // column split of this pass
       TC_MMA_T(tb, mbar_wait_backoff(&b.bfull[sp], (nb / C::NSPLIT) & 1u));
@@ -259,7 +320,12 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
                 }
               }
             }
-            if (C::WPS == 1 || p == tc::WP - 1) tc::mma_commit_w(&b.wempty[s]);
+            if (C::WPS == 1 || p == tc::WP - 1) {
+              if (C::MC == 1)
+                tc::mma_commit_w(&b.wempty[s]);
+              else
+                mma_commit_mc_w(&b.wempty[s], (uint16_t)0x3);  // the stage is free in both CTAs
+            }
           }
         }
       tc::mma_commit_w(&b.dfull[sp]);
