@@ -204,6 +204,46 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* ctx, const float* d_params, const float* d_x,
 fdsdf_status fdsdf_eval_hessian(fdsdf_ctx* ctx, const float* d_params, const float* d_x, int64_t n, float h,
                                 float* d_H, float* d_f, float* d_grad, void* stream);
 
+/* f and grad f at n points (no stencil): the query of a trained SDF, e.g. on the grid of a mesh
+ * extraction.  d_f [n] / d_grad [n][3] fp32 device buffers, either NULL (not
+ * written, not both).  On the tensor / hybrid paths only the centre pass runs (4 columns per
+ * point); the FFMA path runs its fused eval.  Errors: as fdsdf_eval (n > max_centers ->
+ * FDSDF_E_INVALID: query large grids in chunks). */
+fdsdf_status fdsdf_eval_field(fdsdf_ctx* ctx, const float* d_params, const float* d_x, int64_t n, float* d_f,
+                              float* d_grad, void* stream);
+
+/* ---- evaluation side (PAPER.md L157 metrics; DESIGN.md §2 items 17-21) ----
+ * Context-free helpers on device buffers; synchronous where they return host values.          */
+/* Grid points x_q = origin + spacing (i, j, k), q = i + nx (j + ny k): d_x [nx*ny*nz][3]. */
+fdsdf_status fdsdf_grid_points(int nx, int ny, int nz, float ox, float oy, float oz, float spacing, float* d_x,
+                               void* stream);
+/* Device workspace (bytes) fdsdf_mesh_extract needs for an nx x ny x nz grid (0: invalid). */
+size_t fdsdf_mesh_work_bytes(int nx, int ny, int nz);
+/* Zero level set of the grid values d_f [nz][ny][nx] (x fastest, the order of
+ * fdsdf_grid_points) by marching tetrahedra: the 6 Kuhn tetrahedra of every cell, a vertex on
+ * every sign-changing edge by linear interpolation, inside = f < 0, triangles oriented from
+ * inside to outside, deterministic order (cells x-fastest, tetrahedra, triangles).  Writes
+ * *h_ntris (host) and, if it fits in max_tris, the triangles d_tris [*h_ntris][3][3] fp32.
+ * Synchronises `stream`.  Errors: NULL pointers, a dimension < 2, spacing <= 0, workspace too
+ * small, or *h_ntris > max_tris (the size needed is still returned) -> FDSDF_E_INVALID. */
+fdsdf_status fdsdf_mesh_extract(const float* d_f, int nx, int ny, int nz, float ox, float oy, float oz,
+                                float spacing, float* d_tris, int64_t max_tris, int64_t* h_ntris, void* d_work,
+                                size_t work_bytes, void* stream);
+/* Device workspace (bytes) fdsdf_mesh_metrics needs. */
+size_t fdsdf_metrics_work_bytes(int64_t ntris, int64_t nsample, int64_t ngt);
+/* The paper's reconstruction metrics between the mesh d_tris [ntris][3][3] and ground-truth
+ * surface samples d_gt [ngt][3] with unit normals d_gt_normals [ngt][3]: nsample points
+ * area-weighted on the mesh (counter-based SplitMix64 randoms of `seed`) with their face normals;
+ * nearest neighbours both ways (brute force, ties -> lowest index).  h_out [6] (host, fp64):
+ * CD = (mean_p d(p,G) + mean_g d(g,P))/2, F1 = 2PR/(P+R) at threshold tau (strict d < tau),
+ * NC = (mean_p |n_p.n_nn| + mean_g |n_g.n_nn|)/2, Hausdorff, precision P, recall R -- unscaled
+ * (the paper reports CD x10^3, F1 and NC x10^2).  Synchronises `stream`.  Errors: ntris == 0 ->
+ * FDSDF_E_EMPTY; NULL pointers, counts < 1 or > 2^31-1, tau <= 0, workspace too small ->
+ * FDSDF_E_INVALID. */
+fdsdf_status fdsdf_mesh_metrics(const float* d_tris, int64_t ntris, const float* d_gt, const float* d_gt_normals,
+                                int64_t ngt, int64_t nsample, uint64_t seed, float tau, double* h_out, void* d_work,
+                                size_t work_bytes, void* stream);
+
 /* One training step: the loss of Eq. (1) and its gradient with respect to every parameter.
  * d_grad [P] fp32 (overwritten, or accumulated with FDSDF_STEP_ACCUMULATE);
  * d_loss [8] fp64 = (L_DM, L_DNM, L_eik, L_fd, total, n_degenerate, 0, 0), each term
@@ -273,9 +313,11 @@ const char* fdsdf_last_error(const fdsdf_ctx* ctx);
 /* Returns and clears the sticky device flags (synchronises the context's device). */
 fdsdf_status fdsdf_get_device_flags(fdsdf_ctx* ctx, uint32_t* out);
 /* Which contraction path the context runs (-1: NULL): FDSDF_PATH_FFMA; FDSDF_PATH_TENSOR (every
- * contraction on the tensor cores); FDSDF_PATH_HYBRID (networks with 512-wide layers or the
- * skip layer, default flags: the forward -- centre and stencil passes -- and the weight
- * gradient on the tensor cores, the backward on the FFMA kernel). */
+ * contraction on the tensor cores, fused layer-sequential kernels); FDSDF_PATH_HYBRID (networks
+ * with 512-wide layers or the skip layer, default flags: every contraction on the tensor cores
+ * too -- the fused forward kernels, the backward as one GEMM + adjoint launch per hidden layer,
+ * the weight gradient; FDSDF_HYBRID_FFMA_BWD=1 in the environment at create time keeps the
+ * backward on the FFMA kernel). */
 enum { FDSDF_PATH_FFMA = 0, FDSDF_PATH_TENSOR = 1, FDSDF_PATH_HYBRID = 2 };
 int32_t fdsdf_path(const fdsdf_ctx* ctx);
 /* Number of kernel launches enqueued by the last eval/step call on this context. */

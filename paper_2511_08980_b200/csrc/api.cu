@@ -98,6 +98,7 @@ struct fdsdf_ctx {
   bool wgrad3 = false;            // FDSDF_CREATE_WGRAD_BF16X3: the weight gradient's 3-product form
   unsigned char* fimg = nullptr;  // packed forward weight image
   unsigned char* bimg = nullptr;  // packed backward (W^T) weight image
+  bool tcbl = false;              // hybrid path: layer-wise tensor-core backward (bwdl_tc.cu)
   float* cinfo = nullptr;    // [max_centers][16]
   float* zev = nullptr;      // eval-only contexts: [max_centers][nh][mpad] centre pre-activations
   float* hframes = nullptr;  // fdsdf_eval_hessian: [max_centers][6] axis frames
@@ -282,6 +283,12 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     // actv layouts)
     c->tcf = c->tc || (!(flags & FDSDF_CREATE_FFMA) && c->mpad >= 128 && tc_fwd_supported(c->mpad));
     c->tcw = c->tcf && wgrad_tc_supported(c->mpad);
+    // hybrid path: the backward on the tensor cores too (one GEMM + adjoint-map launch per
+    // layer, bwdl_tc.cu); FDSDF_HYBRID_FFMA_BWD=1 keeps the FFMA backward (A/B, validation)
+    {
+      const char* ev = getenv("FDSDF_HYBRID_FFMA_BWD");
+      c->tcbl = !c->tc && c->tcf && bwdl_tc_supported(c->mpad) && !(ev && ev[0] == '1');
+    }
     c->wgrad3 = (flags & FDSDF_CREATE_WGRAD_BF16X3) != 0;
     if (c->wgrad3 && !c->tcw) {  // only the tensor-core weight gradient has the 3-product form
       delete c;
@@ -350,7 +357,9 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     ok = ok && alloc((void**)&c->seed, (size_t)max_centers * NSEED * sizeof(float));
     ok = ok && alloc((void**)&c->del, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
     ok = ok && alloc((void**)&c->actv, (size_t)c->nh * max_centers * NCOLB * mp * sizeof(float));
-    const size_t bslots = c->tc ? (size_t)c->nsm * bwd_tc_acc_slots(mp) : (size_t)c->bgrid;
+    const size_t bslots = c->tc     ? (size_t)c->nsm * bwd_tc_acc_slots(mp)
+                          : c->tcbl ? (size_t)c->nsm * bwdl_tc_acc_slots(mp)
+                                    : (size_t)c->bgrid;
     ok = ok && alloc((void**)&c->bacc, std::max<size_t>(bslots, c->bgrid) * c->nacc * sizeof(float));
     const int nsplit_max = c->tcw ? std::max(c->nsplit, c->nsm) : c->nsplit;
     ok = ok && alloc((void**)&c->part, (size_t)std::max(0, c->ngemm) * nsplit_max * mp * mp * sizeof(float));
@@ -359,7 +368,7 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     ok = ok && alloc((void**)&c->fimg, tc_wimg_bytes(mp, c->ngemm));
     ok = ok && alloc((void**)&c->cinfo, (size_t)max_centers * 16 * sizeof(float));
     if (c->eval_only) ok = ok && alloc((void**)&c->zev, (size_t)max_centers * c->nh * mp * sizeof(float));
-    if (c->tc && !c->eval_only) ok = ok && alloc((void**)&c->bimg, tc_wimg_bytes(mp, c->ngemm));
+    if ((c->tc || c->tcbl) && !c->eval_only) ok = ok && alloc((void**)&c->bimg, tc_wimg_bytes(mp, c->ngemm));
   }
   if (ok) ok = cudaMemset(c->dflags, 0, sizeof(unsigned)) == cudaSuccess;
   cudaSetDevice(prev);
@@ -441,7 +450,8 @@ static int tc_grid(const fdsdf_ctx* c, int64_t ntiles) {
   return (int)std::min<int64_t>(c->nsm & ~1, (g + 1) & ~1);
 }
 
-static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t strm, bool pairs_only = false) {
+static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t strm, bool pairs_only = false,
+                                      bool centre_only = false) {
   a.wimg = c->fimg;
   a.cinfo = c->cinfo;
   const int64_t n = a.n;
@@ -449,7 +459,7 @@ static cudaError_t launch_fwd_tc_pair(fdsdf_ctx* c, FwdArgs& a, cudaStream_t str
   const int g1 = tc_grid(c, a.ntiles);
   cudaError_t e = pairs_only ? cudaSuccess
                              : run_slot(c, FDSDF_KSLOT_FWD_CENTRE, strm, [&] { return launch_fwd_tc(a, 1, g1, strm); });
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || centre_only) return e;
   a.ntiles = (n + fwd_tc_tile_centres(2, c->mpad) - 1) / fwd_tc_tile_centres(2, c->mpad);
   const int g2 = tc_grid(c, a.ntiles);
   c->last_fgrid = g2;
@@ -461,7 +471,7 @@ extern "C" {
 // the body of fdsdf_eval (arguments already validated); pairs_only: see launch_fwd_tc_pair
 static fdsdf_status eval_run(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n,
                              const fdsdf_stencil* st, const fdsdf_eval_out* out, cudaStream_t strm,
-                             bool pairs_only);
+                             bool pairs_only, bool centre_only = false);
 
 fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, const fdsdf_stencil* st,
                         const fdsdf_eval_out* out, void* stream) {
@@ -470,11 +480,29 @@ fdsdf_status fdsdf_eval(fdsdf_ctx* c, const float* d_params, const float* d_x, i
   return eval_run(c, d_params, d_x, n, st, out, (cudaStream_t)stream, false);
 }
 
+fdsdf_status fdsdf_eval_field(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n, float* d_f,
+                              float* d_grad, void* stream) {
+  if (!c) return FDSDF_E_INVALID;
+  if (!d_f && !d_grad && n > 0) return fail(c, FDSDF_E_INVALID, "no output requested");
+  fdsdf_stencil st{};
+  st.h = 1e-2f;  // unused by the centre pass (the tensor path runs only that pass)
+  st.frame_mode = FDSDF_FRAME_RANDOM;
+  st.eps_grad = 0.f;
+  st.denom = FDSDF_DENOM_ONE;
+  st.denom_pow = 4;
+  fdsdf_status s = check_common(c, d_params, d_x, n, &st);
+  if (s != FDSDF_OK) return s;
+  fdsdf_eval_out out{};
+  out.d_f = d_f;
+  out.d_grad = d_grad;
+  return eval_run(c, d_params, d_x, n, &st, &out, (cudaStream_t)stream, false, true);
+}
+
 }  // extern "C"
 
 static fdsdf_status eval_run(fdsdf_ctx* c, const float* d_params, const float* d_x, int64_t n,
                              const fdsdf_stencil* st, const fdsdf_eval_out* out, cudaStream_t strm,
-                             bool pairs_only) {
+                             bool pairs_only, bool centre_only) {
   pairs_only = pairs_only && c->tcf;  // the FFMA forward is one fused kernel
   int prev = 0;
   cudaGetDevice(&prev);
@@ -509,7 +537,7 @@ static fdsdf_status eval_run(fdsdf_ctx* c, const float* d_params, const float* d
   if (c->tcf) {
     a.zf = c->eval_only ? c->zev : c->zf;
     a.zcols = c->eval_only ? 1 : NCOLF;
-    e = launch_fwd_tc_pair(c, a, strm, pairs_only);
+    e = launch_fwd_tc_pair(c, a, strm, pairs_only, centre_only);
     if (prev != c->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(c, e, "fwd_tc_kernel");
     return FDSDF_OK;
@@ -625,7 +653,7 @@ static fdsdf_status step_impl(fdsdf_ctx* c, const float* d_params, const float* 
   }
   if (c->tcf && c->ngemm > 0)  // tensor forward image (and, on the tensor path, the backward's)
     e = run_slot(c, FDSDF_KSLOT_PACK_TC, strm, [&] { return launch_pack_tc(c->net, c->fimg, c->bimg, strm); });
-  if (e == cudaSuccess && !c->tc && c->ngemm > 0)  // FFMA backward / weight gradient
+  if (e == cudaSuccess && !c->tc && !(c->tcbl && c->tcw) && c->ngemm > 0)  // FFMA backward / weight gradient
     e = run_slot(c, FDSDF_KSLOT_PACK, strm, [&] { return launch_pack(c->net, c->wt, c->wb, strm); });
   if (e != cudaSuccess) return done(cuda_fail(c, e, "pack_tc"));
 
@@ -672,6 +700,13 @@ static fdsdf_status step_impl(fdsdf_ctx* c, const float* d_params, const float* 
     bgrid = tc_grid(c, b.ntiles);
     nbslots = bgrid * bwd_tc_acc_slots(c->mpad);
     e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwd_tc(b, bgrid, strm); });
+  } else if (c->tcbl) {
+    b.wimg = c->bimg;
+    b.ntiles = (n + bwdl_tc_tile_centres() - 1) / bwdl_tc_tile_centres();
+    bgrid = (int)std::min<int64_t>(c->nsm, b.ntiles);
+    nbslots = bgrid * bwdl_tc_acc_slots(c->mpad);
+    e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwdl_tc(b, bgrid, strm); });
+    c->launches += c->L - 2;  // one launch per hidden layer
   } else {
     b.ntiles = (n + c->btile - 1) / c->btile;
     bgrid = (int)std::min<int64_t>(c->bgrid, b.ntiles);

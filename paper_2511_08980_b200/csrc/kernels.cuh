@@ -141,6 +141,12 @@ bool tc_fwd_supported(int mpad);                    // tensor forward (fwd_tc.cu
 cudaError_t launch_bwd_tc(const BwdArgs& a, int grid, cudaStream_t st);
 int bwd_tc_tile_centres();                          // 8
 int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
+// hybrid path (512-wide layers, the skip layer): the backward as one tensor-core GEMM + adjoint
+// launch per hidden layer (bwdl_tc.cu); mpad 256 / 512
+bool bwdl_tc_supported(int mpad);
+cudaError_t launch_bwdl_tc(const BwdArgs& a, int grid, cudaStream_t st);
+int bwdl_tc_tile_centres();                         // 8
+int bwdl_tc_acc_slots(int mpad);                    // accumulator slots per CTA
 cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, bool bf16x3, cudaStream_t st);
 int wgrad_tc_splits(int nsm, int64_t rows, int mpad);  // split-K factor of the tensor wgrad
 bool wgrad_tc_supported(int mpad);                      // MPAD 128 / 256 / 512

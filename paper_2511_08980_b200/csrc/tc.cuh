@@ -235,6 +235,24 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
 
 
 
+// 10 consecutive columns as five 2-column loads, one wait
+__device__ __forceinline__ void tmem_ld10(uint32_t ta, float (&v)[10]) {
+  uint32_t r[10];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%10];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%2,%3}, [%11];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%4,%5}, [%12];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%6,%7}, [%13];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%8,%9}, [%14];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9])
+      : "r"(ta), "r"(ta + 2), "r"(ta + 4), "r"(ta + 6), "r"(ta + 8)
+      : "memory");
+#pragma unroll
+  for (int j = 0; j < 10; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 // three 8-column loads (the three accumulator ranges of one column group), one wait
 __device__ __forceinline__ void tmem_ld8x3(uint32_t ta, uint32_t tb, uint32_t tc_, float (&a)[8], float (&b)[8],
                                            float (&c)[8]) {

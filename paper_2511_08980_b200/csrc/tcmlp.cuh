@@ -195,6 +195,7 @@ __device__ __forceinline__ void tc_regsplit() {
 
 template <class C>
 __device__ __forceinline__ void tc_teardown(uint32_t tbase) {
+  __syncwarp();  // warp 0 diverged (lane 0 = the producer): reconverge before the aligned barrier
   tc::fence_before();
   __syncthreads();
   if (C::MC > 1) cluster_sync_all();  // no multicast copy / commit still targets this CTA
