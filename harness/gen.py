@@ -23,7 +23,7 @@ import numpy as np
 
 __all__ = [
     "mlp_spec", "layer_shapes", "num_params", "init_params", "plane_mlp",
-    "sphere_surface", "uniform_box", "csg_shape", "csg_surface", "csg_bbox_diag",
+    "sphere_surface", "uniform_box", "csg_shape", "csg_surface", "csg_surface_normals", "csg_bbox_diag",
     "add_noise", "csg_cutout_surface", "loss_cfg", "frame_seed", "make_config",
     "CONFIG_NAMES",
 ]
@@ -137,8 +137,8 @@ def _area(p):
     return 2.0 * math.pi * p["r"] * 2.0 * p["hh"] + 2.0 * math.pi * p["r"] ** 2
 
 
-def _sample_prim(p, m, rng):
-    """m points uniform (by area) on the surface, local frame."""
+def _sample_prim(p, m, rng, normals=False):
+    """m points uniform (by area) on the surface, local frame (and their outward unit normals)."""
     if p["kind"] == "box":
         h = p["half"]
         face_area = np.array([h[1] * h[2], h[0] * h[2], h[0] * h[1]])
@@ -146,6 +146,10 @@ def _sample_prim(p, m, rng):
         sgn = np.where(rng.uniform(size=m) < 0.5, -1.0, 1.0)
         loc = rng.uniform(-1.0, 1.0, (m, 3)) * h
         loc[np.arange(m), axis] = sgn * h[axis]
+        if normals:
+            nrm = np.zeros((m, 3))
+            nrm[np.arange(m), axis] = sgn
+            return loc, nrm
         return loc
     r, hh = p["r"], p["hh"]
     lat = 2.0 * math.pi * r * 2.0 * hh
@@ -154,7 +158,12 @@ def _sample_prim(p, m, rng):
     ang = rng.uniform(0, 2 * math.pi, m)
     rad = np.where(part == 0, r, r * np.sqrt(rng.uniform(size=m)))
     z = np.where(part == 0, rng.uniform(-hh, hh, m), np.where(part == 1, hh, -hh))
-    return np.stack([rad * np.cos(ang), rad * np.sin(ang), z], axis=1)
+    loc = np.stack([rad * np.cos(ang), rad * np.sin(ang), z], axis=1)
+    if normals:
+        nrm = np.stack([np.where(part == 0, np.cos(ang), 0.0), np.where(part == 0, np.sin(ang), 0.0),
+                        np.where(part == 0, 0.0, np.where(part == 1, 1.0, -1.0))], axis=1)
+        return loc, nrm
+    return loc
 
 
 def _strictly_inside(p, x):
@@ -164,23 +173,29 @@ def _strictly_inside(p, x):
     return (loc[:, 0] ** 2 + loc[:, 1] ** 2 < p["r"] ** 2) & (np.abs(loc[:, 2]) < p["hh"])
 
 
-def _raw_surface(prims, n, rng):
+def _raw_surface(prims, n, rng, normals=False):
     areas = np.array([_area(p) for p in prims])
-    out = []
+    out, outn = [], []
     have = 0
     while have < n:
         m = max(2 * (n - have), 1024)
         which = rng.choice(len(prims), size=m, p=areas / areas.sum())
         pts = np.empty((m, 3))
+        nrm = np.empty((m, 3))
         for i, p in enumerate(prims):
             sel = which == i
             if sel.any():
-                pts[sel] = _sample_prim(p, int(sel.sum()), rng) @ p["R"].T + p["c"]
+                loc, ln = _sample_prim(p, int(sel.sum()), rng, normals=True)
+                pts[sel] = loc @ p["R"].T + p["c"]
+                nrm[sel] = ln @ p["R"].T
         keep = np.ones(m, bool)
         for i, p in enumerate(prims):
             keep &= ~(_strictly_inside(p, pts) & (which != i))
         out.append(pts[keep])
+        outn.append(nrm[keep])
         have += int(keep.sum())
+    if normals:
+        return np.concatenate(out)[:n], np.concatenate(outn)[:n]
     return np.concatenate(out)[:n]
 
 
@@ -199,6 +214,14 @@ def csg_surface(n, shape_seed, pts_seed):
     prims, centre, scale, _ = _normaliser(shape_seed)
     raw = _raw_surface(prims, n, np.random.default_rng(pts_seed))
     return ((raw - centre) * scale).astype(np.float32)
+
+
+def csg_surface_normals(n, shape_seed, pts_seed):
+    """csg_surface's points (the same draw) and their outward unit normals: the ground truth of the
+    reconstruction metrics (normals of the union's primitives, rotated)."""
+    prims, centre, scale, _ = _normaliser(shape_seed)
+    raw, nrm = _raw_surface(prims, n, np.random.default_rng(pts_seed), normals=True)
+    return ((raw - centre) * scale).astype(np.float32), nrm.astype(np.float32)
 
 
 def csg_bbox_diag(shape_seed):

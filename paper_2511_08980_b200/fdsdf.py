@@ -120,6 +120,21 @@ def lib():
         L.fdsdf_selftest_mma_pair.restype = C.c_int
         L.fdsdf_version.argtypes = []
         L.fdsdf_version.restype = C.c_char_p
+        L.fdsdf_eval_field.argtypes = [vp, vp, vp, i64, vp, vp, vp]
+        L.fdsdf_eval_field.restype = C.c_int
+        f32 = C.c_float
+        L.fdsdf_grid_points.argtypes = [C.c_int, C.c_int, C.c_int, f32, f32, f32, f32, vp, vp]
+        L.fdsdf_grid_points.restype = C.c_int
+        L.fdsdf_mesh_work_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.fdsdf_mesh_work_bytes.restype = C.c_size_t
+        L.fdsdf_mesh_extract.argtypes = [vp, C.c_int, C.c_int, C.c_int, f32, f32, f32, f32, vp, i64,
+                                         C.POINTER(i64), vp, C.c_size_t, vp]
+        L.fdsdf_mesh_extract.restype = C.c_int
+        L.fdsdf_metrics_work_bytes.argtypes = [i64, i64, i64]
+        L.fdsdf_metrics_work_bytes.restype = C.c_size_t
+        L.fdsdf_mesh_metrics.argtypes = [vp, i64, vp, vp, i64, i64, C.c_uint64, f32, C.POINTER(C.c_double), vp,
+                                         C.c_size_t, vp]
+        L.fdsdf_mesh_metrics.restype = C.c_int
         _lib = L
     return _lib
 
@@ -216,6 +231,48 @@ def make_loss(cfg: dict, counts):
 def fdsdf_eval_hessian(ctx, params, x, n, h, H, f=None, g=None, stream=None):
     _check(lib().fdsdf_eval_hessian(ctx, _ptr(params), _ptr(x), int(n), float(h), _ptr(H), _ptr(f), _ptr(g),
                                     _stream(stream)), ctx)
+
+
+def fdsdf_eval_field(ctx, params, x, n, f, g, stream=None):
+    _check(lib().fdsdf_eval_field(ctx, _ptr(params), _ptr(x), int(n), _ptr(f), _ptr(g), _stream(stream)), ctx)
+
+
+def fdsdf_grid_points(nx, ny, nz, origin, spacing, x, stream=None):
+    _check(lib().fdsdf_grid_points(int(nx), int(ny), int(nz), *(float(o) for o in origin), float(spacing), _ptr(x),
+                                   _stream(stream)))
+
+
+def fdsdf_mesh_extract(f_grid, origin, spacing, stream=None):
+    """Triangles [T, 3, 3] (device fp32) of the zero level set of the grid values f_grid [nz, ny, nx]
+    (include/fdsdf.h fdsdf_mesh_extract); the workspace and output are allocated here."""
+    import torch
+    nz, ny, nx = (int(d) for d in f_grid.shape)
+    work = torch.empty(int(lib().fdsdf_mesh_work_bytes(nx, ny, nz)), dtype=torch.uint8, device=f_grid.device)
+    nt = C.c_int64(0)
+    args = (_ptr(f_grid.contiguous()), nx, ny, nz, *(float(o) for o in origin), float(spacing))
+    st = lib().fdsdf_mesh_extract(*args, None, 0, C.byref(nt), _ptr(work), work.numel(), _stream(stream))
+    if st not in (0, 1):
+        _check(st)
+    tris = torch.empty(max(nt.value, 1), 3, 3, dtype=torch.float32, device=f_grid.device)
+    _check(lib().fdsdf_mesh_extract(*args, _ptr(tris), tris.shape[0], C.byref(nt), _ptr(work), work.numel(),
+                                    _stream(stream)))
+    return tris[:nt.value]
+
+
+def fdsdf_mesh_metrics(tris, gt, gt_normals, nsample=100_000, seed=0, tau=0.005, stream=None):
+    """dict(cd, f1, nc, hausdorff, precision, recall) -- unscaled (include/fdsdf.h fdsdf_mesh_metrics)."""
+    import torch
+    tris = tris.contiguous()
+    gt = gt.contiguous()
+    gt_normals = gt_normals.contiguous()
+    nt, ng = int(tris.shape[0]), int(gt.shape[0])
+    work = torch.empty(max(1, int(lib().fdsdf_metrics_work_bytes(nt, int(nsample), ng))), dtype=torch.uint8,
+                       device=tris.device)
+    out = (C.c_double * 6)()
+    _check(lib().fdsdf_mesh_metrics(_ptr(tris), nt, _ptr(gt), _ptr(gt_normals), ng, int(nsample),
+                                    C.c_uint64(int(seed) & ((1 << 64) - 1)), float(tau), out, _ptr(work),
+                                    work.numel(), _stream(stream)))
+    return dict(zip(("cd", "f1", "nc", "hausdorff", "precision", "recall"), list(out)))
 
 
 def fdsdf_eval(ctx, params, x, n, stencil: Stencil, out: EvalOut, stream=None):
@@ -353,6 +410,32 @@ class FDSDF:
             H = torch.empty(n, 6, device=self.device, dtype=torch.float32)
         fdsdf_eval_hessian(self.ctx, params, x, n, h, H, f, g, stream)
         return H
+
+    def eval_field(self, params, x, f=None, g=None, stream=None):
+        """f [n] and grad f [n, 3] (device tensors) at points x (no stencil): fdsdf_eval_field, in
+        chunks of max_centers."""
+        import torch
+        params = self._dev(params, torch.float32)
+        x = self._dev(x, torch.float32).reshape(-1, 3)
+        n = x.shape[0]
+        if f is None:
+            f = torch.empty(n, device=self.device, dtype=torch.float32)
+        if g is None:
+            g = torch.empty(n, 3, device=self.device, dtype=torch.float32)
+        for a in range(0, n, self.max_centers):
+            b = min(n, a + self.max_centers)
+            fdsdf_eval_field(self.ctx, params, x[a:b], b - a, f[a:b], g[a:b], stream)
+        return f, g
+
+    def extract_mesh(self, params, res, lo=-1.0, hi=1.0, stream=None):
+        """The zero level set of f on a res^3 grid over [lo, hi]^3: (triangles [T,3,3], grid f)."""
+        import torch
+        sp = (hi - lo) / (res - 1)
+        x = torch.empty(res ** 3, 3, device=self.device, dtype=torch.float32)
+        fdsdf_grid_points(res, res, res, (lo, lo, lo), sp, x, stream)
+        f, _ = self.eval_field(params, x, stream=stream)
+        fg = f.reshape(res, res, res)
+        return fdsdf_mesh_extract(fg, (lo, lo, lo), sp, stream), fg
 
     def step(self, params, x, n_surface, h, loss_cfg, counts=None, frame_seed=0, index_offset=0, frames=None,
              eps_grad=None, grad=None, loss=None, accumulate=False, allreduce=False, stream=None):
