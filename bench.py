@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the train-iteration and eval measurements")
     ap.add_argument("--no-eval-sweep", action="store_true",
                     help="skip C5e: fdsdf_eval throughput for 1e4 .. 1e7 centres (N = 1 only, 'eval_sweep')")
+    ap.add_argument("--recon-iters", type=int, default=3000,
+                    help="training iterations of the reconstruction extra (N = 1; 0 = skip)")
     ap.add_argument("--no-c5", action="store_true",
                     help="skip the C5 block (BASELINE configs[4]: 200k centres per GPU, every N)")
     ap.add_argument("--path", choices=("default", "ffma", "tensor"), default="default",
@@ -381,6 +383,50 @@ def measure_c5(args, spec, local, rank, world, dev, stream, flush, barrier):
             "unit": UNIT, "finite_loss": ok, "collective": coll}
 
 
+def measure_recon(args, model, cfg, stream):
+    """The paper's experiment in kind (§4) on the synthetic CSG shape: train the
+    SIREN (Trainer: 20k of a 30k surface pool + 20k box points per iteration, FD-NCR + eikonal +
+    Dirichlet, Adam 5e-5) for --recon-iters iterations, then extract the zero level set on a 128^3
+    grid (fdsdf_eval_field + marching tetrahedra) and score it against 30k held-out ground-truth
+    samples with normals: CD x10^3, F1 x10^2 (tau = 0.005), NC x10^2 -- at init and after training."""
+    import torch
+    from harness import csg_surface, csg_surface_normals
+    from paper_2511_08980_b200.fdsdf import Trainer, fdsdf_mesh_metrics
+    dev = model.device
+    ns = cfg["n_surface"]
+    pool = csg_surface(int(ns * 1.5), 3, 100).astype(np.float32)
+    G, Gn = csg_surface_normals(30_000, 3, 77)
+    G, Gn = torch.from_numpy(G).to(dev), torch.from_numpy(Gn).to(dev)
+    # the full Eq. (1) with SPEC's defaults (S:L327): the non-manifold term keeps the untrained SIREN
+    # from leaving zero crossings in free space (the headline C2 step uses BASELINE's loss list)
+    lc = dict(cfg["loss"], lambda_dnm=100.0)
+    tr = Trainer(model, cfg["params"], pool, ns, len(cfg["x"]) - ns, 1.1, cfg["h"], lc, seed=4)
+    res = 128
+
+    def score():
+        t0 = time.perf_counter()
+        tris, _ = model.extract_mesh(tr.params, res, stream=stream)
+        mm = fdsdf_mesh_metrics(tris, G, Gn, nsample=100_000, seed=1, tau=0.005, stream=stream)
+        torch.cuda.synchronize()
+        return {"cd_x1e3": mm["cd"] * 1e3, "f1_x1e2": mm["f1"] * 1e2, "nc_x1e2": mm["nc"] * 1e2,
+                "hausdorff": mm["hausdorff"], "triangles": int(tris.shape[0]),
+                "extract_and_score_s": time.perf_counter() - t0}
+
+    init = score()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.recon_iters):
+        tr.iterate(stream)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    final = score()
+    return {"iterations": args.recon_iters, "wall_s": dt, "ms_per_iteration_wall": dt * 1e3 / args.recon_iters,
+            "grid": f"{res}^3 over [-1,1]^3", "metrics_at_init": init, "metrics_after": final,
+            "ground_truth": "30k held-out CSG surface samples with normals (harness.csg_surface_normals)",
+            "note": "synthetic CSG stand-in for the ABC meshes (DESIGN.md §3); the paper trains ~5-9k iterations "
+                    "with CD-based early stopping (P:L153)"}
+
+
 def setup_comm(model, world, rank, dev):
     """The library's own NCCL communicator (the in-step allreduce of FDSDF_STEP_ALLREDUCE): rank 0
     draws the unique id, torch.distributed broadcasts it.  Should loading / initialising it fail
@@ -605,6 +651,10 @@ def main():
             "wgrad_ms": kt3["wgrad"][0] / max(kt3["wgrad"][1], 1),
             "what": "opt-in FDSDF_CREATE_WGRAD_BF16X3: weight gradient with 3 bf16 piece products "
                     "(~3*2^-16 per product); forward / delta propagation bf16x6; same oracle gates"}
+
+    # ------------------------------------------------------------------ reconstruction (NEXT-4)
+    if not args.no_extras and world == 1 and args.recon_iters > 0:
+        extras["reconstruction"] = measure_recon(args, model, cfg, stream)
 
     # ------------------------------------------------------------------ C5 (BASELINE configs[4])
     c5 = None

@@ -530,6 +530,11 @@ class Trainer:
         self.n_pick, self.n_uniform, self.box_half, self.h = int(n_pick), int(n_uniform), float(box_half), float(h)
         self.loss_cfg, self.seed, self.lr, self.betas, self.eps = loss_cfg, int(seed), lr, betas, eps
         n = self.n_pick + self.n_uniform
+        if allreduce and counts is None:
+            # the summed loss / gradient of a data-parallel step is the global mean only with the
+            # global counts; each rank also needs its own `seed` (the sampler draws the box points
+            # from (seed, iteration, row) alone) and index_offset (frames from the global index)
+            raise ValueError("Trainer(allreduce=True) needs the global counts (N_s, N_u, N)")
         self.counts = counts if counts is not None else (self.n_pick, self.n_uniform, n)
         self.index_offset, self.allreduce = int(index_offset), bool(allreduce)
         self.x = torch.empty(n, 3, device=model.device, dtype=torch.float32)

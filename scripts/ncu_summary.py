@@ -25,10 +25,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 TAG = ""
 OURS = re.compile(r"(fwd_kernel|bwd_kernel|wgrad_kernel|finalize_kernel|pack_kernel|fwd_tc_kernel|bwd_tc_kernel|"
-                  r"wgrad_tc_kernel|pack_tc_kernel)")
+                  r"wgrad_tc_kernel|pack_tc_kernel|bwdl_tc_kernel)")
 FWD_TC_MODE = re.compile(r"fwd_tc_kernel<\s*(?:\(int\))?\d+,\s*(?:\(int\))?\d+,\s*(?:\(int\))?([12])>")
 # kernel -> the bench's timing slot name (bench.py kernel_ms keys)
-TC_SLOT = {"bwd_tc_kernel": "bwd", "wgrad_tc_kernel": "wgrad", "pack_tc_kernel": "pack_tc"}
+TC_SLOT = {"bwd_tc_kernel": "bwd", "wgrad_tc_kernel": "wgrad", "pack_tc_kernel": "pack_tc", "bwdl_tc_kernel": "bwd"}
 
 FULL_METRICS = [
     ("gpu__time_duration.sum", "duration"),
@@ -115,7 +115,11 @@ def full(rep, rnd):
             out.append(f"| {h[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]} | "
                        + " | ".join(f"{v:.2f}" for v in vals) + " |")
     open(os.path.join(PROF, f"r{rnd:02d}{TAG}_ncu_full.md"), "w").write("\n".join(out) + "\n")
-    json.dump(dram, open(os.path.join(PROF, "ncu_dram_per_launch.json"), "w"), indent=1)
+    import sys
+    sys.path.insert(0, ROOT)
+    from bench import source_hash  # the build tag bench.py checks before it reports roofline.traffic
+    json.dump({"build": source_hash(), "capture": os.path.basename(rep), "per_launch": dram},
+              open(os.path.join(PROF, "ncu_dram_per_launch.json"), "w"), indent=1)
     print("\n".join(out))
 
 
