@@ -37,6 +37,10 @@ namespace fdsdf {
 #define BWD_TC_UNROLL 1
 #endif
 constexpr int kBwdUnroll = BWD_TC_UNROLL;
+// 1: phase A's pair maps take act.cuh's warp-uniform fast series form (pairs_bwd4)
+#ifndef BWD_TC_FASTPAIR
+#define BWD_TC_FASTPAIR 0
+#endif
 // stores of delta / the layer activations (read once, by the weight-gradient kernel after the
 // whole backward): 1 = streaming (st.global.cs, evict-first), 0 = default caching
 #ifndef BWD_TC_STCS
@@ -361,12 +365,27 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
 #pragma unroll
             for (int j = 0; j < NCOLB; ++j) pv[j] = 0.f;
             float cs1 = 0.f, cs2tr = 0.f;
+#if BWD_TC_FASTPAIR
+            typename AF::C ccf{};
+            if (valid) {  // every lane of the warp: the pair maps vote on their fast series form
+              ccf = AF::centre(q.z, beta);
+              AF::pairs_bwd4(ccf, q.A, q.S, beta, t);
+              if (!mok) {
+#pragma unroll
+                for (int j = 0; j < 20; ++j) t[j] = 0.f;
+              }
+            }
+#endif
             if (mok && valid) {
+#if BWD_TC_FASTPAIR
+              const typename AF::C cc = ccf;
+#else
               const typename AF::C cc = AF::centre(q.z, beta);
 #pragma unroll
               for (int p = 0; p < 4; ++p)
                 AF::pair_bwd(cc, q.A[p], q.S[p], beta, &t[5 * p], &t[5 * p + 1], &t[5 * p + 2], &t[5 * p + 3],
                              &t[5 * p + 4]);
+#endif
               {  // the layer's activations (wgrad operand) are X-independent: stored here
                 const float* sd = sds + cl * 20;
                 const float tr = fmaf(sd[5], q.t0, fmaf(sd[6], q.t1, sd[7] * q.t2));
