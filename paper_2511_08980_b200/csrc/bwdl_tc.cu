@@ -31,6 +31,13 @@
 #define BWDL_PF 0
 #endif
 
+// M-half passes per tile: 2 = the MMAs of the second half of the output neurons run while the
+// epilogue warps of the first half consume theirs (and the next tile's first pass overlaps the
+// second half's epilogue); each pass re-stages the tile's delta chunks (L2 hits)
+#ifndef BWDL_PASSES
+#define BWDL_PASSES 2
+#endif
+
 namespace fdsdf {
 
 template <int MPAD>
@@ -40,6 +47,8 @@ struct BlCfg {
   static constexpr int EPI0 = 4, NEPI = 16;             // warps 0..3 control, 4..19 epilogue
   static constexpr int NTHR = (EPI0 + NEPI) * 32;
   static constexpr int NSTGT = 64;                      // stager threads (warps 2, 3)
+  static constexpr int NPASS = BWDL_PASSES;            // M-half passes per tile
+  static constexpr int HPP = MH / NPASS, WPP = NEPI / NPASS;  // halves / epilogue warps per pass
   static constexpr int EG = NEPI / (4 * MH);            // centre groups
   static constexpr int CPE = CT / EG;                   // centres per epilogue thread
   static constexpr int WSTAGE = 16384, NWST = 6;        // weight ring: single-piece stages
@@ -51,16 +60,17 @@ struct BlCfg {
   static constexpr int OFF_W = 0;
   static constexpr int OFF_B = NWST * WSTAGE;
   static constexpr int OFF_R = OFF_B + NBST * BSTAGE;
-  static constexpr int OFF_SD = OFF_R + NRST * RSTAGE;  // float [2][CT][20]: seeds + x
-  static constexpr int OFF_BAR = OFF_SD + 2 * CT * 20 * 4;
-  // wfull, wempty, bfull, bempty, rfull, rempty, dfull, dfree
-  static constexpr int NBAR = 2 * NWST + 2 * NBST + 2 * NRST + 2;
+  static constexpr int OFF_SD = OFF_R + NRST * RSTAGE;  // float [NPASS][2][CT][20]: seeds + x
+  static constexpr int OFF_BAR = OFF_SD + NPASS * 2 * CT * 20 * 4;
+  // wfull, wempty, bfull, bempty, rfull, rempty, dfull[NPASS], dfree[NPASS]
+  static constexpr int NBAR = 2 * NWST + 2 * NBST + 2 * NRST + 2 * NPASS;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;
   static constexpr uint32_t TCOLS = MH * NT <= 128 ? 128 : (MH * NT <= 256 ? 256 : 512);
   static constexpr int REG_LAUNCH = 96, REG_CTL = 56, REG_EPI = 104;
   static_assert(EPI0 * REG_CTL + NEPI * REG_EPI <= (EPI0 + NEPI) * REG_LAUNCH, "setmaxnreg pool");
   static_assert(MH * NT <= 512 && BYTES <= 232448, "TMEM / shared memory");
   static_assert(EG >= 1 && CT % EG == 0, "centre groups");
+  static_assert(NPASS >= 1 && MH % NPASS == 0 && WPP % 4 == 0, "passes");
 };
 
 int bwdl_tc_tile_centres() { return 8; }
@@ -86,8 +96,8 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
   uint64_t* rfull = bempty + C::NBST;
   uint64_t* rempty = rfull + C::NRST;
   uint64_t* dfull = rempty + C::NRST;
-  uint64_t* dfree = dfull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfree + 1);
+  uint64_t* dfree = dfull + C::NPASS;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfree + C::NPASS);
 
   const Net& net = a.net;
   const int L = net.L;
@@ -109,8 +119,10 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
       mbar_init(&rfull[s], 1);
       mbar_init(&rempty[s], C::NSTGT / 32);
     }
-    mbar_init(dfull, 1);
-    mbar_init(dfree, C::NEPI);
+    for (int p = 0; p < C::NPASS; ++p) {
+      mbar_init(&dfull[p], 1);
+      mbar_init(&dfree[p], C::WPP);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tslot, C::TCOLS);
@@ -131,8 +143,9 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
         const unsigned char* img = a.wimg + (size_t)l * MPAD * MPAD * 2 * tc::WP;  // image g = l: omega_l W_{l+1}^T
         uint32_t it = 0, ir = 0;
         for (int64_t tile = lane == 0 ? blockIdx.x : a.ntiles; tile < a.ntiles; tile += gridDim.x)
+          for (int ps = 0; ps < C::NPASS; ++ps)
           for (int kc = 0; kc < C::KC; ++kc) {
-            if (BWDL_PF && kc == 0) {  // the next tile's zf blocks (layer l) -> L2
+            if (BWDL_PF && kc == 0 && ps == 0) {  // the next tile's zf blocks (layer l) -> L2
               const int64_t nxt = tile + gridDim.x;
               for (int cl = 0; cl < CT && nxt < a.ntiles; ++cl) {
                 const int64_t c = nxt * CT + cl;
@@ -153,7 +166,7 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
                   : "memory");
               ++ir;
             }
-            for (int h = 0; h < MH; ++h)
+            for (int h = ps * C::HPP; h < (ps + 1) * C::HPP; ++h)
               for (int p = 0; p < tc::WP; ++p, ++it) {
                 const int s = (int)(it % C::NWST);
                 mbar_wait_backoff(&wempty[s], ((it / C::NWST) & 1u) ^ 1u);
@@ -175,15 +188,17 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
 #else
 #define BL_T(acc, stmt) stmt;
 #endif
-        for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++nt) {
-          BL_T(t_d, mbar_wait_backoff(dfree, (nt & 1u) ^ 1u));  // the epilogue has read the previous tile's D
+        for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++nt)
+          for (int ps = 0; ps < C::NPASS; ++ps) {
+          // the pass's epilogue warps have read the previous tile's D of these halves
+          BL_T(t_d, mbar_wait_backoff(&dfree[ps], (nt & 1u) ^ 1u));
           tc::fence_after();
           for (int kc = 0; kc < C::KC; ++kc, ++ib) {
             const int sb = (int)(ib % C::NBST);
             BL_T(t_b, mbar_wait(&bfull[sb], (ib / C::NBST) & 1u));
             tc::fence_after();
             const uint32_t bb = smem_u32(Bs + sb * C::BSTAGE);
-            for (int h = 0; h < MH; ++h)
+            for (int h = ps * C::HPP; h < (ps + 1) * C::HPP; ++h)
 #pragma unroll
               for (int p = 0; p < tc::WP; ++p, ++it) {
                 const int s = (int)(it % C::NWST);
@@ -201,8 +216,8 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
               }
             tc::mma_commit_w(&bempty[sb]);
           }
-          tc::mma_commit_w(dfull);
-          if (lane == 0) BL_TRACE("[l%d] mma committed dfull tile %u\n", l, nt);
+          tc::mma_commit_w(&dfull[ps]);
+          if (lane == 0) BL_TRACE("[l%d] mma committed dfull tile %u pass %d\n", l, nt, ps);
         }
         if (lane == 0) BL_TRACE("[l%d] mma done\n", l);
 #ifdef FDSDF_PHASE_TIMING
@@ -218,6 +233,7 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
         const int st = tid - 64;
         uint32_t ib = 0;
         for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x)
+          for (int ps = 0; ps < C::NPASS; ++ps)
           for (int kc = 0; kc < C::KC; ++kc, ++ib) {
             const int sb = (int)(ib % C::NBST), sr = (int)(ib % C::NRST);
             mbar_wait(&rfull[sr], (ib / C::NRST) & 1u);
@@ -258,10 +274,11 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
     setmaxnreg_inc<C::REG_EPI>();
 #endif
     // ------------------------------------------------------------------ epilogue warps
-    const int ew = warp - C::EPI0, et = tid - 32 * C::EPI0;
+    const int ew = warp - C::EPI0;
+    const int ps = ew / C::WPP, et = tid - 32 * (C::EPI0 + ps * C::WPP);  // pass group, thread in it
     const int q4 = warp & 3;
-    const int hh = (ew >> 2) % MH;
-    const int eg = ew / (4 * MH);
+    const int hh = ps * C::HPP + ((ew % C::WPP) >> 2) % C::HPP;
+    const int eg = ((ew % C::WPP) >> 2) / C::HPP;
     const int m = hh * 128 + 32 * q4 + lane;  // neuron of layer l
     const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * NT;
     const int M = net.width[l + 1];
@@ -276,8 +293,8 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
     uint32_t nt = 0;
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++nt) {
       const int64_t c0 = tile * CT;
-      float* sds = sds0 + (nt & 1u) * CT * 20;
-      for (int i = et; i < CT * 20; i += C::NEPI * 32) {
+      float* sds = sds0 + (ps * 2 + (nt & 1u)) * CT * 20;
+      for (int i = et; i < CT * 20; i += C::WPP * 32) {
         const int cl = i / 20, q = i % 20;
         const int64_t c = c0 + cl;
         float v = 0.f;
@@ -285,7 +302,7 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
         else if (c < a.n && q >= 16 && q < 19) v = a.x[c * 3 + (q - 16)];
         sds[i] = v;
       }
-      bar_named(1, C::NEPI * 32);
+      bar_named(1 + ps, C::WPP * 32);
       if (et == 0) BL_TRACE("[l%d] epilogue tile %u\n", l, nt);
       // this thread's stored forward pre-activations (z, t | A, S pairs) of centre i, loaded one
       // centre ahead of its use
@@ -302,8 +319,8 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
       float4 gn[3];
       ldz(0, gn);
       if (!top) {
-        if (ew == 0) mbar_wait(dfull, nt & 1u);
-        bar_named(2, C::NEPI * 32);
+        if (et < 32) mbar_wait(&dfull[ps], nt & 1u);
+        bar_named(1 + C::NPASS + ps, C::WPP * 32);
         tc::fence_after();
       }
 #pragma unroll 1
@@ -392,9 +409,9 @@ __global__ void __launch_bounds__(BlCfg<MPAD>::NTHR, 1)
       if (!top) {
         tc::fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(dfree);
+        if (lane == 0) mbar_arrive(&dfree[ps]);
       }
-      bar_named(1, C::NEPI * 32);  // the seeds buffer of this parity is free again
+      bar_named(1 + ps, C::WPP * 32);  // the seeds buffer of this parity is free again
     }
     if (et == 0) BL_TRACE("[l%d] epilogue done\n", l);
     // this thread's rows of its (CTA, centre group) slot: db_l, and dW_last / db_last (top) or
