@@ -702,8 +702,8 @@ static fdsdf_status step_impl(fdsdf_ctx* c, const float* d_params, const float* 
     e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwd_tc(b, bgrid, strm); });
   } else if (c->tcbl) {
     b.wimg = c->bimg;
-    b.ntiles = (n + bwdl_tc_tile_centres() - 1) / bwdl_tc_tile_centres();
-    bgrid = (int)std::min<int64_t>(c->nsm, b.ntiles);
+    b.ntiles = (n + bwdl_tc_tile_centres(c->mpad) - 1) / bwdl_tc_tile_centres(c->mpad);
+    bgrid = bwdl_tc_grid(c->nsm, b.ntiles, c->mpad);
     nbslots = bgrid * bwdl_tc_acc_slots(c->mpad);
     e = run_slot(c, FDSDF_KSLOT_BWD, strm, [&] { return launch_bwdl_tc(b, bgrid, strm); });
     c->launches += c->L - 2;  // one launch per hidden layer

@@ -145,7 +145,8 @@ int bwd_tc_acc_slots(int mpad);                     // accumulator slots per CTA
 // launch per hidden layer (bwdl_tc.cu); mpad 256 / 512
 bool bwdl_tc_supported(int mpad);
 cudaError_t launch_bwdl_tc(const BwdArgs& a, int grid, cudaStream_t st);
-int bwdl_tc_tile_centres();                         // 8
+int bwdl_tc_tile_centres(int mpad);                 // 16 (CTA pairs, mpad 512) or 8
+int bwdl_tc_grid(int nsm, int64_t ntiles, int mpad); // CTAs (even for CTA pairs)
 int bwdl_tc_acc_slots(int mpad);                    // accumulator slots per CTA
 cudaError_t launch_wgrad_tc(const WgradArgs& a, int nglayers, bool bf16x3, cudaStream_t st);
 int wgrad_tc_splits(int nsm, int64_t rows, int mpad);  // split-K factor of the tensor wgrad
