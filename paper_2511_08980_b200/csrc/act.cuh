@@ -160,14 +160,22 @@ struct Act<ACT_SINE> {
 // sigma(z) = sp(beta z)/beta, sp(t) = log(1 + e^t); s(t) = logistic.
 template <>
 struct Act<ACT_SOFTPLUS> {
+  // s(t) and 1 - s(t) = s(-t) from ONE exponential: e = exp(-|t|) <= 1, r = 1 / (1 + e);
+  // the larger of the two is r, the smaller e r (both with fp32 relative precision)
+  __device__ __forceinline__ static void logistic2(float t, float* s, float* sm) {
+    const float e = expf(-fabsf(t));
+    const float r = __fdividef(1.0f, 1.0f + e);
+    const float lo = e * r;
+    *s = t >= 0.0f ? r : lo;
+    *sm = t >= 0.0f ? lo : r;
+  }
   struct C {
     float t, s0, s0m;  // beta z, s(t), 1 - s(t)
   };
   __device__ __forceinline__ static C centre(float z, float beta) {
     C c;
     c.t = beta * z;
-    c.s0 = logistic_acc(c.t);
-    c.s0m = logistic_acc(-c.t);
+    logistic2(c.t, &c.s0, &c.s0m);
     return c;
   }
   __device__ __forceinline__ static float value(const C& c, float beta) { return softplus_acc(c.t) / beta; }
@@ -175,25 +183,27 @@ struct Act<ACT_SOFTPLUS> {
   __device__ __forceinline__ static float d2(const C& c, float beta) { return beta * c.s0 * c.s0m; }
 
   struct P2 {
-    float sy, ps, ea, ema, E, em_d;
+    float sy, sym, ps, ea, ema, ima, E, em_d;
   };
   __device__ __forceinline__ static P2 pre(const C& c, float A, float S, float beta) {
     P2 p;
     const float a = beta * A;
     const float d = 0.5f * beta * S;
     const float ty = c.t + d;
-    p.sy = logistic_acc(ty);
-    p.ps = p.sy * logistic_acc(-ty);       // s(ty)(1 - s(ty))
+    logistic2(ty, &p.sy, &p.sym);          // s(ty), 1 - s(ty)
+    p.ps = p.sy * p.sym;                   // s(ty)(1 - s(ty))
     p.ea = expm1f(a);                      // e^a - 1
-    p.ema = -p.ea / (1.0f + p.ea);         // e^-a - 1
+    p.ima = __fdividef(1.0f, 1.0f + p.ea); // e^-a
+    p.ema = -p.ea * p.ima;                 // e^-a - 1
     p.E = p.ea * (-p.ema);                 // e^a - 2 + e^-a = 4 sinh^2(a/2) >= 0
     p.em_d = expm1f(d);
     return p;
   }
   __device__ __forceinline__ static void fwd_from(const C& c, const P2& p, float beta, float* Aa, float* Sa) {
     const float ib = 1.0f / beta;
-    // sp(ty+a) - sp(ty-a) = log1p(s ea) - log1p(s ema)       (terms of opposite sign)
-    *Aa = 0.5f * ib * (log1pf(p.sy * p.ea) - log1pf(p.sy * p.ema));
+    // sp(ty+a) - sp(ty-a) = log((1 + s ea) / (1 + s ema)) = log1p(s (ea - ema) / (1 + s ema)),
+    // 1 + s ema = (1 - s) + s e^-a  (sums of positive terms only)
+    *Aa = 0.5f * ib * log1pf(p.sy * (p.ea - p.ema) / fmaf(p.sy, p.ima, p.sym));
     // sp(ty+a)+sp(ty-a)-2sp(ty) = log1p(s(1-s) E);  sp(ty)-sp(t) = log1p(s0 expm1(d))
     *Sa = ib * (log1pf(p.ps * p.E) + 2.0f * log1pf(c.s0 * p.em_d));
   }
@@ -217,14 +227,14 @@ struct Act<ACT_SOFTPLUS> {
                                                   float* Sa, float* P, float* Dd, float* Z) {
     const P2 p = pre(c, A, S, beta);
     fwd_from(c, p, beta, Aa, Sa);
-    const float den = 1.0f / fmaf(p.ps, p.E, 1.0f);
-    const float one_m_2s = -tanhf(0.5f * (c.t + 0.5f * beta * S));  // 1 - 2 s(ty)
+    const float den = __fdividef(1.0f, fmaf(p.ps, p.E, 1.0f));
+    const float one_m_2s = p.sym - p.sy;                              // 1 - 2 s(ty)
     const float even = p.E * p.ps * one_m_2s * den;                   // s(ty+a)+s(ty-a)-2s(ty)
     const float odd = (p.ea - p.ema) * p.ps * den;                    // s(ty+a)-s(ty-a)
     *P = 0.5f * (2.0f * p.sy + even);
     *Dd = 0.5f * odd;
-    // s(ty) - s(t) = -s(ty)(1-s(t)) expm1(-d)
-    const float dsy = -p.sy * c.s0m * expm1f(-0.5f * beta * S);
+    // s(ty) - s(t) = -s(ty)(1-s(t)) expm1(-d),  expm1(-d) = -expm1(d) / (1 + expm1(d))
+    const float dsy = p.sy * c.s0m * (p.em_d / (1.0f + p.em_d));
     *Z = even + 2.0f * dsy;
   }
 };
