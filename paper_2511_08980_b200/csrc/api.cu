@@ -276,6 +276,9 @@ fdsdf_status fdsdf_create(const fdsdf_mlp_spec* spec, int device, int64_t max_ce
     if (ok_tc && !(flags & FDSDF_CREATE_FFMA)) {
       c->tc = true;
       c->mpad = mp_tc;
+      // FDSDF_FORCE_HYBRID=1 (A/B only): a 256-wide network on the hybrid path's layer-wise backward
+      const char* fh = getenv("FDSDF_FORCE_HYBRID");
+      if (fh && fh[0] == '1' && c->mpad == 256 && !(flags & FDSDF_CREATE_TENSOR)) c->tc = false;
     }
     // networks the full tensor path does not cover (512-wide layers, the skip layer) still run
     // their forward and weight gradient on the tensor cores when the padded width is a tcgen05

@@ -63,6 +63,11 @@ __device__ __forceinline__ void bwd_st(float* p, float v) {
 #endif
 // 1: phase A hands sigma'(z) and sigma''(z) (r . t) of each centre to phase B
 // in a small per-thread array, instead of phase B reloading z, t and recomputing sincos(z)
+// 1: one epilogue warp polls "D full", the others wait in a named barrier (no spinning warps
+// beside the ones still in phase A)
+#ifndef BWD_TC_POLL1
+#define BWD_TC_POLL1 1
+#endif
 #ifndef BWD_TC_CARRY
 #define BWD_TC_CARRY 1
 #endif
@@ -260,8 +265,14 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
     long long t_tstart = 0, t_tstart_n = 0, t_top = 0, t_pa = 0;
 #endif
     const int64_t tend = tc_tile_end<C>(a.ntiles);
+    // centre / layer strides of zf and of the delta / activation rows (floats): per tile one
+    // 64-bit product, per centre and layer 32-bit offsets
+    constexpr int ZCS_L = NCOLF * MPAD;
+    const int zcs = nh * ZCS_L;
     for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x, spar ^= 1u) {
       const int64_t c0 = tile * CT;
+      const float* const zt = a.zf + (size_t)c0 * zcs;       // zf block of the tile's first centre
+      const size_t drow0 = (size_t)c0 * NCOLB * MPAD + m;    // its first delta / activation row, + m
       // this tile's first MMA pass reads layer L-3; the next tile's top layer (computed during
       // this tile's passes) reads layer L-2 of that tile
       prefetch_layer(tile, L - 3);
@@ -332,7 +343,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
           const int64_t c = c0 + eg + EG * i;
           if (i < CPE && c < a.n && mok) {
             FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
-            const float4* zq = reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD) + m;
+            const float4* zq = reinterpret_cast<const float4*>(zt + (eg + EG * i) * zcs + l * ZCS_L) + m;
+            FDSDF_ASSERT((const float*)zq == a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + 4 * m);
             const float4 g0 = __ldg(zq), g1 = __ldg(zq + MPAD), g2 = __ldg(zq + 2 * MPAD);
             q.z = g0.x;
             q.t0 = g0.y;
@@ -409,7 +421,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
             {
               if (valid && l <= L - 3) {
                 FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
-                float* ap = a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
+                float* ap = a.actv + (size_t)l * nrows * MPAD + drow0 + cl * (NCOLB * MPAD);
+                FDSDF_ASSERT(ap == a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m);
 #pragma unroll
                 for (int j = 0; j < NCOLB; ++j) bwd_st(ap + j * MPAD, pv[j]);
               }
@@ -460,7 +473,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
           const int64_t c = c0 + eg + EG * i;
           z4[0] = z4[1] = z4[2] = z4[3] = 0.f;
           if (!CARRY && i < CPE && c < a.n && mok) {
-            const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD) + m);
+            const float4 g0 = __ldg(reinterpret_cast<const float4*>(zt + (eg + EG * i) * zcs + l * ZCS_L) + m);
             z4[0] = g0.x;
             z4[1] = g0.y;
             z4[2] = g0.z;
@@ -473,7 +486,12 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
         float cs1n = CARRY ? c_s1[0] : 0.f, cs2n = CARRY ? c_s2tr[0] : 0.f;
         if (!top) {
           ptimer.before_wait();
-          mbar_wait(bars.dfull, nd & 1u);
+          if (BWD_TC_POLL1) {  // one warp polls, the others sleep in a hardware named barrier
+            if (et < 32) mbar_wait(bars.dfull, nd & 1u);
+            bar_named(2, C::NEPI * 32);
+          } else {
+            mbar_wait(bars.dfull, nd & 1u);
+          }
           ptimer.after_wait();
           ++nd;
           tc::fence_after();
@@ -564,7 +582,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
           if (valid) {
             if (l >= 1) {
               FDSDF_ASSERT(c >= 0 && c < a.n && l >= 1 && l < nh);
-              float* dp = a.del + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m;
+              float* dp = a.del + (size_t)l * nrows * MPAD + drow0 + cl * (NCOLB * MPAD);
+              FDSDF_ASSERT(dp == a.del + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m);
 #pragma unroll
               for (int j = 0; j < NCOLB; ++j) bwd_st(dp + j * MPAD, dl[j]);
             }

@@ -88,10 +88,13 @@ struct BlCfg {
   static_assert(NPASS >= 1 && WPP % 4 == 0 && (PAIR ? MH % 2 == 0 : MH % NPASS == 0), "passes");
 };
 
-static constexpr bool bwdl_pair(int mpad) { return BWDL_PAIR && mpad == 512; }
+#ifndef BWDL_PAIR256
+#define BWDL_PAIR256 0
+#endif
+static constexpr bool bwdl_pair(int mpad) { return BWDL_PAIR && (mpad == 512 || (BWDL_PAIR256 && mpad == 256)); }
 int bwdl_tc_tile_centres(int mpad) { return bwdl_pair(mpad) ? 16 : 8; }
 int bwdl_tc_acc_slots(int mpad) {
-  return mpad == 512 ? BlCfg<512, bwdl_pair(512)>::EG : BlCfg<256, false>::EG;
+  return mpad == 512 ? BlCfg<512, bwdl_pair(512)>::EG : BlCfg<256, bwdl_pair(256)>::EG;
 }
 bool bwdl_tc_supported(int mpad) { return mpad == 256 || mpad == 512; }
 int bwdl_tc_grid(int nsm, int64_t ntiles, int mpad) {

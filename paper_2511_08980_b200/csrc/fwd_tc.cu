@@ -30,8 +30,9 @@
 
 namespace fdsdf {
 
-#ifndef FWD_TC_NSPLIT
-#define FWD_TC_NSPLIT 1
+// M-half pipelining of the 256-wide layers (tcmlp.cuh TcCfg::HP): 1 = on
+#ifndef FWD_TC_HP
+#define FWD_TC_HP 1
 #endif
 #ifndef FWD_TC_NEPI
 #define FWD_TC_NEPI 16
@@ -52,7 +53,7 @@ constexpr int kFwdUnroll = FWD_TC_UNROLL;
 #ifndef FWD_TC_PIPE0
 #define FWD_TC_PIPE0 1
 #endif
-constexpr bool FWD_PIPE0 = FWD_TC_PIPE0 && FWD_TC_NSPLIT == 1;
+constexpr bool FWD_PIPE0 = FWD_TC_PIPE0;
 // tile width: FWD_TC_N columns up to 256-wide layers; 32 for 512-wide ones (C3), where a wider
 // B operand (32 x 512 x 3 pieces = 96 KB) would not fit next to the weight ring
 constexpr int fwd_tc_n(int mpad) { return mpad == 512 ? 32 : FWD_TC_N; }
@@ -61,19 +62,20 @@ constexpr int fwd_tc_n(int mpad) { return mpad == 512 ? 32 : FWD_TC_N; }
 #ifndef FWD_TC_BMN
 #define FWD_TC_BMN 1
 #endif
-constexpr int fwd_tc_bmn(int mpad) { return (FWD_TC_BMN && FWD_TC_NSPLIT == 1 && fwd_tc_n(mpad) % 64 == 0) ? 1 : 0; }
+constexpr int fwd_tc_bmn(int mpad) { return (FWD_TC_BMN && fwd_tc_n(mpad) % 64 == 0) ? 1 : 0; }
+constexpr int fwd_tc_hp(int mpad) { return (FWD_TC_HP && mpad == 256) ? 1 : 0; }
 // weight ring depth (16 KB single-piece stages): one more than the backward's 6 fits next to the
 // forward's 96 KB B operand
 #ifndef FWD_TC_NST
 #define FWD_TC_NST 6
 #endif
 template <int MPAD, int MODE>
-struct FtcCfg : TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
-                      FWD_TC_NSPLIT, fwd_tc_bmn(MPAD), FWD_TC_NST> {
+struct FtcCfg : TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0, 1,
+                      fwd_tc_bmn(MPAD), FWD_TC_NST, fwd_tc_hp(MPAD)> {
   // TMEM stash (FWD_PIPE0): the next tile's layer-0 outputs, (MH x EG thread groups) x CPE x
   // columns per centre = MH x N columns
-  using B = TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0,
-                  FWD_TC_NSPLIT, fwd_tc_bmn(MPAD), FWD_TC_NST>;
+  using B = TcCfg<MPAD, fwd_tc_n(MPAD), FWD_TC_NEPI, 3, FWD_PIPE0 ? fwd_tc_n(MPAD) * (MPAD / 128) : 0, 1,
+                  fwd_tc_bmn(MPAD), FWD_TC_NST, fwd_tc_hp(MPAD)>;
   static constexpr int MAXC = 16;                                   // max centres per tile
   // last-layer partial sums and the tile's centre info are double-buffered by tile parity:
   // the per-centre epilogue of tile t runs during the first MMA phase of tile t+1
@@ -182,10 +184,27 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
     const int ew = warp - C::EPI0;  // 0 .. NEPI-1
     const int et = tid - 32 * C::EPI0;  // 0 .. NEPI*32-1
     const int q4 = warp & 3;                 // TMEM lane quarter
-    const int hh = (ew >> 2) % MH;           // M-half
-    const int eg = ew / (4 * MH);            // centre group
-    const int m = hh * 128 + 32 * q4 + lane; // output neuron of this thread
-    const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * C::DH;
+    // M-blocks: without M-half pipelining every warp owns one M-half and EG centre groups split
+    // the tile; with it (C::HP) every warp walks both M-halves in turn (half 0, then half 1 of
+    // each layer) and NEPI / 4 centre groups split the tile
+    constexpr bool HP = C::HP;
+    constexpr int NBLK = HP ? MH : 1;        // M-blocks per layer and thread
+    constexpr int EGX = HP ? C::NEPI / 4 : C::EG;  // centre groups
+    constexpr int CPX = CT / EGX;            // centres per thread and M-block
+    static_assert(CT % EGX == 0, "centre groups divide the tile");
+    const int hh0 = HP ? 0 : (ew >> 2) % MH;
+    const int egx = HP ? (ew >> 2) : ew / (4 * MH);  // centre group
+    auto half_of = [&](int blk) { return HP ? blk : hh0; };
+    auto neuron = [&](int blk) { return half_of(blk) * 128 + 32 * q4 + lane; };  // output neuron of this thread
+    auto taddr_of = [&](int blk) -> uint32_t {
+      return tbase + ((uint32_t)(32 * q4) << 16) + half_of(blk) * C::DH;
+    };
+    // this thread's stash columns of M-block blk: CPX centres x CPC values (FWD_PIPE0)
+    auto tstash_of = [&](int blk) -> uint32_t {
+      return tbase + ((uint32_t)(32 * q4) << 16) + MH * C::DH + (half_of(blk) * EGX + egx) * CPX * CPC;
+    };
+    // slot of this warp's last-layer partial sums of M-block blk (finish() sums the slots)
+    auto rslot = [&](int blk) { return HP ? blk * 4 + q4 : ew; };
     const float beta = net.beta;
     const float h = a.h;
     const bool step = a.step != 0;
@@ -196,39 +215,44 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
 #pragma unroll
     for (int q = 0; q < NLOSS; ++q) lacc[q] = 0.0;
 
-    // this thread's stored pre-activations of layer l, centre c (kernels.cuh zf layout): float4
-    // group g (step), the centre value z (step: in group 0; eval: z only, contiguous over m)
-    auto zg4 = [&](int64_t c, int l, int g) -> float4* {
+    // this thread's stored pre-activations of layer l, centre c, neuron m (kernels.cuh zf
+    // layout): float4 group g (step), the centre value z (step: in group 0; eval: z only,
+    // contiguous over m)
+    // `zb` = the centre's block of zf (zrow(c)): one 64-bit product per centre, the rest in 32 bits
+    const int zcs = nh * a.zcols * MPAD, zls = a.zcols * MPAD;  // centre / layer strides (floats)
+    auto zrow = [&](int64_t c) -> float* { return a.zf + (size_t)c * zcs; };
+    auto zg4 = [&](const float* zb, int64_t c, int l, int g, int m) -> float4* {
       FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && g >= 0 && g < ZG && a.zcols == NCOLF && m < MPAD);
-      return reinterpret_cast<float4*>(a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + (size_t)g * 4 * MPAD) + m;
+      FDSDF_ASSERT(zb == a.zf + (size_t)c * zcs);
+      return reinterpret_cast<float4*>(const_cast<float*>(zb) + l * zls + g * 4 * MPAD) + m;
     };
-    auto zc = [&](int64_t c, int l) -> float* {
+    auto zc = [&](const float* zb, int64_t c, int l, int m) -> float* {
       FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh && m < MPAD);
-      return a.zf + ((size_t)c * nh + l) * a.zcols * MPAD + (step ? 4 * m : m);
+      FDSDF_ASSERT(zb == a.zf + (size_t)c * zcs);
+      return const_cast<float*>(zb) + l * zls + (step ? 4 * m : m);
     };
-    auto put_b = [&](int n, float v) { tc_put_b<C>(Bs, n, m, v); };
-    // a centre's consecutive columns n0 .. n0+3 / n0+7 of the next B operand
-    auto put_b4 = [&](int n0, const float (&v)[4]) {
+    // a centre's consecutive columns n0 .. n0+3 / n0+7 of the next B operand (K index m)
+    auto put_b4 = [&](int n0, int m, const float (&v)[4]) {
       if constexpr (C::BMN) {
         tc_put_b4<C>(Bs, n0, m, v);
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) put_b(n0 + j, v[j]);
+        for (int j = 0; j < 4; ++j) tc_put_b<C>(Bs, n0 + j, m, v[j]);
       }
     };
-    auto put_b8 = [&](int n0, const float (&v)[8]) {
+    auto put_b8 = [&](int n0, int m, const float (&v)[8]) {
       if constexpr (C::BMN) {
         tc_put_b8<C>(Bs, n0, m, v);
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) put_b(n0 + j, v[j]);
+        for (int j = 0; j < 8; ++j) tc_put_b<C>(Bs, n0 + j, m, v[j]);
       }
     };
     // cat(a, x) / sqrt(2) at the input of the skip layer net.skip (IGR convention, SURVEY §8c
     // item 14): when layer l's outputs feed it, every output is scaled by 1/sqrt(2) and the
     // threads of rows M .. M+2 (no neuron of layer l) supply the x part (as fwd.cu does)
     constexpr float RSQ2 = 0.70710678118654752f;
-    auto skip_centre = [&](int l, int64_t c, bool valid, float& o0, float& o1, float& o2, float& o3) {
+    auto skip_centre = [&](int l, int m, int64_t c, bool valid, float& o0, float& o1, float& o2, float& o3) {
       if (l + 1 != net.skip) return;
       const int M = net.width[l + 1];
       if (m >= M && m < M + 3) {  // value x_d, tangents e_d
@@ -243,7 +267,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
       o2 *= RSQ2;
       o3 *= RSQ2;
     };
-    auto skip_pairs = [&](int l, const float* ci, float (&o)[8]) {
+    auto skip_pairs = [&](int l, int m, const float* ci, float (&o)[8]) {
       if (l + 1 != net.skip) return;
       const int M = net.width[l + 1];
       if (m >= M && m < M + 3) {  // odd part of x0 +- h d_p = h d_p, even part 0
@@ -258,24 +282,33 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
 #pragma unroll
       for (int p = 0; p < 8; ++p) o[p] *= RSQ2;
     };
-    // this thread's stash columns: CPE centres x CPC values (FWD_PIPE0)
-    const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + MH * C::DH + (hh * C::EG + eg) * CPE * CPC;
     const bool pipe0 = FWD_PIPE0 && ngemm > 0;
-    FDSDF_ASSERT(!FWD_PIPE0 || (MH * C::DH + (hh * C::EG + eg + 1) * CPE * CPC) <= (int)C::TCOLS);
-    // this thread's layer-0 weight row and bias (fan-in 3; constant over the kernel, loaded once
-    // instead of before every centre's layer-0 arithmetic)
-    const bool mok0 = m < net.width[1];
-    const float w0r0 = mok0 ? net.W[0][m * 3 + 0] : 0.f, w0r1 = mok0 ? net.W[0][m * 3 + 1] : 0.f,
-                w0r2 = mok0 ? net.W[0][m * 3 + 2] : 0.f, b0r = (MODE == 1 && mok0) ? net.b[0][m] : 0.f;
-    // layer 0 of centre i of tile tl (centre info cis_t): pre-activations -> zf, activations ->
-    // this thread's stash columns (exactly the l == 0 arithmetic of the epilogue below)
-    auto layer0_centre = [&](int64_t tl, int i, const float* cis_t) {
+    FDSDF_ASSERT(!FWD_PIPE0 || (MH * C::DH + MH * EGX * CPX * CPC) <= (int)C::TCOLS);
+    // this thread's layer-0 weight rows and biases, one per M-block (fan-in 3; constant over the
+    // kernel, loaded once instead of before every centre's layer-0 arithmetic)
+    float w0r[NBLK][3], b0r[NBLK];
+#pragma unroll
+    for (int blk = 0; blk < NBLK; ++blk) {
+      const int m = neuron(blk);
+      const bool mok0 = m < net.width[1];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) w0r[blk][j] = mok0 ? net.W[0][m * 3 + j] : 0.f;
+      b0r[blk] = (MODE == 1 && mok0) ? net.b[0][m] : 0.f;
+    }
+    // compile-time indexed (a runtime index would put the arrays in local memory)
+    auto w0of = [&](int blk, int j) -> float { return (NBLK > 1 && blk) ? w0r[NBLK - 1][j] : w0r[0][j]; };
+    auto b0of = [&](int blk) -> float { return (NBLK > 1 && blk) ? b0r[NBLK - 1] : b0r[0]; };
+    // layer 0 of centre i of M-block blk of tile tl (centre info cis_t): pre-activations -> zf,
+    // activations -> this thread's stash columns (exactly the l == 0 arithmetic of the epilogue)
+    auto layer0_centre = [&](int64_t tl, int blk, int i, const float* cis_t) {
       if (tl >= a.ntiles) return;
-      const int cl = eg + C::EG * i;
+      const int cl = egx + EGX * i;
       const int64_t c = tl * CT + cl;
       const bool valid = c < a.n;
       const float om = net.omega[0];
+      const int m = neuron(blk);
       const bool mok = m < net.width[1];
+      const uint32_t tstash = tstash_of(blk);
       if (MODE == 1) {
         float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
         float x0 = 0.f, x1 = 0.f, x2 = 0.f;
@@ -286,17 +319,17 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
           if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
         }
         if (mok) {
-          const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
-          z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0r);
+          const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
+          z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0of(blk));
           t0 = om * w0;
           t1 = om * w1;
           t2 = om * w2;
         }
         if (valid) {
           if (step)
-            *zg4(c, 0, 0) = make_float4(z, t0, t1, t2);
+            *zg4(zrow(c), c, 0, 0, m) = make_float4(z, t0, t1, t2);
           else
-            *zc(c, 0) = z;
+            *zc(zrow(c), c, 0, m) = z;
         }
         float o[4] = {0.f, 0.f, 0.f, 0.f};
         if (mok) {
@@ -307,14 +340,15 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
           o[2] = s1 * t1;
           o[3] = s1 * t2;
         }
-        skip_centre(0, c, valid, o[0], o[1], o[2], o[3]);
+        skip_centre(0, m, c, valid, o[0], o[1], o[2], o[3]);
         tc::tmem_st4(tstash + i * CPC, o);
       } else {
         const float* ci = cis_t + cl * NCINFO;
-        const float z0 = valid ? __ldg(zc(c, 0)) : 0.f;
+        const float* zb = zrow(c);
+        const float z0 = valid ? __ldg(zc(zb, c, 0, m)) : 0.f;
         float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
         if (mok) {
-          const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
+          const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
           const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
           const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
           const float hs = om * h;
@@ -324,8 +358,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
           Av[3] = hs * (du - dv);
         }
         if (step && valid) {
-          *zg4(c, 0, 1) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
-          *zg4(c, 0, 2) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
+          *zg4(zb, c, 0, 1, m) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
+          *zg4(zb, c, 0, 2, m) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
         }
         float o[8];
         {  // every lane (the pair maps vote on their fast form); rows past the width give 0
@@ -336,7 +370,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
             for (int p = 0; p < 8; ++p) o[p] = 0.f;
           }
         }
-        skip_pairs(0, ci, o);
+        skip_pairs(0, m, ci, o);
         float o4[4] = {o[0], o[1], o[2], o[3]};
         tc::tmem_st4(tstash + i * CPC, o4);
         o4[0] = o[4];
@@ -362,8 +396,12 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float v = 0.f;
-          for (int w = 0; w < C::NEPI; ++w)
-            if ((w / (4 * MH)) == (cl % C::EG)) v += red[(w * C::MAXC + cl) * 4 + j];
+          if (HP) {  // slots blk * 4 + q4: every one holds a partial sum of every centre
+            for (int w = 0; w < 4 * MH; ++w) v += red[(w * C::MAXC + cl) * 4 + j];
+          } else {
+            for (int w = 0; w < C::NEPI; ++w)
+              if ((w / (4 * MH)) == (cl % C::EG)) v += red[(w * C::MAXC + cl) * 4 + j];
+          }
           tot[j] = v;
         }
         if (MODE == 1) {
@@ -410,6 +448,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
     const int64_t tend = tc_tile_end<C>(a.ntiles);
     for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x, tpar ^= 1u) {
       const int64_t c0 = tile * CT;
+      float* const zt = zrow(c0);  // the tile's first centre's block of zf
       float* red = red0 + tpar * C::RED_N;
       float* cis = cis0 + tpar * C::CI_N;
       if (MODE == 2) {
@@ -421,12 +460,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
         const bool last = (l == L - 2);
         const int M = net.width[l + 1];
         const float om = net.omega[l];
-        const bool mok = m < M;
-        const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
-        // omega_l b_l (the image carries omega_l W_l), once per layer
-        const float bias_l = (MODE == 1 && l > 0 && mok) ? om * net.b[l][m] : 0.f;
         // last layer: sum over this warp's 32 neurons of w_L[m] * out_j, one slot per centre
-        auto reduce4 = [&](int cl, float p0, float p1, float p2, float p3) {
+        auto reduce4 = [&](int blk, int cl, float wl, float p0, float p1, float p2, float p3) {
           float pv[4] = {wl * p0, wl * p1, wl * p2, wl * p3};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -436,171 +471,198 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
             v += __shfl_xor_sync(0xffffffffu, v, 4);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
             v += __shfl_xor_sync(0xffffffffu, v, 1);
-            if (lane == 0) red[(ew * C::MAXC + cl) * 4 + j] = v;
+            if (lane == 0) red[(rslot(blk) * C::MAXC + cl) * 4 + j] = v;
           }
         };
-        // the tile's centres are processed split by split (C::NSPLIT column splits): as soon as
-        // this split's part of the next B operand is written, its MMA pass for layer l+1 runs
-        // while the epilogue continues with the next split of layer l
-        constexpr int CPSPL = CT / C::NSPLIT;   // centres per split
-        constexpr int CPEs = CPE / C::NSPLIT;   // centres per thread per split
         if (l == 0 && pipe0) {
           // B operand of layer 1 from the parked layer-0 outputs (computed here only for the
-          // CTA's first tile)
+          // CTA's first tile), M-block by M-block
           if (tile == blockIdx.x) {
-            for (int i = 0; i < CPE; ++i) layer0_centre(tile, i, cis);
+            for (int blk = 0; blk < NBLK; ++blk)
+              for (int i = 0; i < CPX; ++i) layer0_centre(tile, blk, i, cis);
+            tc::tmem_wait_st();
+          }
+#pragma unroll
+          for (int blk = 0; blk < NBLK; ++blk) {
+            const int m = neuron(blk);
+            const uint32_t tstash = tstash_of(blk);
+#pragma unroll 1
+            for (int i = 0; i < CPX; ++i) {
+              const int cl = egx + EGX * i;
+              if constexpr (CPC == 4) {
+                float o4[4];
+                tc::tmem_ld4(tstash + i * CPC, o4);
+                put_b4(cl * CPC, m, o4);
+              } else {
+                float o8[8];
+                tc::tmem_ld8(tstash + i * CPC, o8);
+                put_b8(cl * CPC, m, o8);
+              }
+            }
+            tc_epi_arrive(bars, HP ? blk : 0);
+          }
+        } else {
+          if (pipe0 && l >= l0first) {  // the next tile's layer 0, spread over this tile's MMA phases
+            if (MODE == 2 && l == l0first) {
+              if (ew == 0) cp_async_wait_all();
+              bar_named(1, C::NEPI * 32);  // the next tile's centre info is in
+            }
+#pragma unroll 1
+            for (int k = l - l0first; k < NBLK * CPX; k += L - 1 - l0first)
+              layer0_centre(tile + gridDim.x, k / CPX, k % CPX, cis0 + (tpar ^ 1u) * C::CI_N);
             tc::tmem_wait_st();
           }
 #pragma unroll 1
-          for (int i = 0; i < CPE; ++i) {
-            const int cl = eg + C::EG * i;
-            if constexpr (CPC == 4) {
-              float o4[4];
-              tc::tmem_ld4(tstash + i * CPC, o4);
-              put_b4(cl * CPC, o4);
-            } else {
-              float o8[8];
-              tc::tmem_ld8(tstash + i * CPC, o8);
-              put_b8(cl * CPC, o8);
+          for (int blk = 0; blk < NBLK; ++blk) {
+            const int m = neuron(blk);
+            const bool mok = m < M;
+            const float wl = (last && mok) ? net.W[L - 1][m] : 0.f;
+            // omega_l b_l (the image carries omega_l W_l), once per layer and M-block
+            const float bias_l = (MODE == 1 && l > 0 && mok) ? om * net.b[l][m] : 0.f;
+            const uint32_t taddr = taddr_of(blk);
+            // mode 2: the centre pre-activation of this neuron at centre slot cl (prefetched one
+            // centre ahead; this thread's first centre before the MMA wait)
+            auto ldz = [&](int cl) -> float {
+              const int64_t c = c0 + cl;
+              return (MODE == 2 && cl < CT && c < a.n) ? __ldg(zc(zt + cl * zcs, c, l, m)) : 0.f;
+            };
+            float z0n = ldz(egx);
+            if (l > 0) {
+              ptimer.before_wait();
+              // one warp polls the mbarrier, the others sleep in a hardware named barrier (no
+              // spin instructions competing with the MMA warp for issue slots)
+              if (ew == 0) mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
+              bar_named(2, C::NEPI * 32);
+              ptimer.after_wait();
+              tc::fence_after();
             }
-          }
-          tc_epi_arrive(bars, 0);
-        } else
-        for (int sp = 0; sp < C::NSPLIT; ++sp) {
-        // mode 2: the centre pre-activation of this neuron, prefetched one centre ahead
-        auto ldz = [&](int i) -> float {
-          const int64_t c = c0 + sp * CPSPL + eg + C::EG * i;
-          return (MODE == 2 && i < CPEs && c < a.n) ? __ldg(zc(c, l)) : 0.f;
-        };
-        float z0n = ldz(0);
-        if (pipe0 && l >= l0first) {  // the next tile's layer 0, spread over this tile's MMA phases
-          if (MODE == 2 && l == l0first) {
-            if (ew == 0) cp_async_wait_all();
-            bar_named(1, C::NEPI * 32);  // the next tile's centre info is in
-          }
-#pragma unroll 1
-          for (int i = l - l0first; i < CPE; i += L - 1 - l0first)
-            layer0_centre(tile + gridDim.x, i, cis0 + (tpar ^ 1u) * C::CI_N);
-          tc::tmem_wait_st();
-        }
-        if (l > 0) {
-          ptimer.before_wait();
-          // one warp polls the mbarrier, the others sleep in a hardware named barrier (no
-          // spin instructions competing with the MMA warp for issue slots)
-          if (ew == 0) mbar_wait(&bars.dfull[sp], nd & 1u);
-          bar_named(2, C::NEPI * 32);
-          ptimer.after_wait();
-          tc::fence_after();
-        }
-#pragma unroll kFwdUnroll
-        for (int i = 0; i < CPEs; ++i) {
-          const int cl = sp * CPSPL + eg + C::EG * i;  // centre slot in the tile
-          const int64_t c = c0 + cl;
-          const bool valid = c < a.n;
-          const float z0 = z0n;
-          z0n = ldz(i + 1);
-          if constexpr (MODE == 1) {
-            float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
-            if (l == 0) {
-              float x0 = 0.f, x1 = 0.f, x2 = 0.f;
-              if (valid) {
-                x0 = a.x[c * 3 + 0];
-                x1 = a.x[c * 3 + 1];
-                x2 = a.x[c * 3 + 2];
-                if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
-              }
-              if (mok) {
-                const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
-                z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0r);
-                t0 = om * w0;
-                t1 = om * w1;
-                t2 = om * w2;
-              }
-            } else {
-              float v[4];
-              tc_ld_sum4<C>(taddr, cl * 4, v);  // centre cl's 4 columns
-              if (mok) {
-                z = v[0] + bias_l;
-                t0 = v[1];
-                t1 = v[2];
-                t2 = v[3];
-              }
-            }
-            if (valid) {
-              if (step)
-                *zg4(c, l, 0) = make_float4(z, t0, t1, t2);
-              else
-                *zc(c, l) = z;
-            }
-            float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-            if (mok) {
-              const typename AF::C cc = AF::centre(z, beta);
-              const float s1 = AF::d1(cc, beta);
-              o0 = AF::value(cc, beta);
-              o1 = s1 * t0;
-              o2 = s1 * t1;
-              o3 = s1 * t2;
-            }
-            skip_centre(l, c, valid, o0, o1, o2, o3);
-            if (last) {
-              reduce4(cl, o0, o1, o2, o3);
-            } else {
-              const float o4[4] = {o0, o1, o2, o3};
-              put_b4(cl * 4, o4);
-            }
-          } else {
-            const float* ci = cis + cl * NCINFO;
-            float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
-            if (l == 0) {
-              if (mok) {
-                const float w0 = w0r0, w1 = w0r1, w2 = w0r2;
-                const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
-                const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
-                const float hs = om * h;
-                Av[0] = hs * du;
-                Av[1] = hs * dv;
-                Av[2] = hs * (du + dv);
-                Av[3] = hs * (du - dv);
-              }
-            } else {
-              float v[8];
-              tc_ld_sum8<C>(taddr, cl * 8, v);
-              if (mok) {
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                  Av[p] = v[2 * p];
-                  Sv[p] = v[2 * p + 1];
+            // HP: the B rows of K half 0 may still be read by the layer's (1, 0) MMA group --
+            // wait for "B free" before this M-block's first B store
+            bool need_free = HP && blk == 0 && l > 0 && !last;
+            auto centre_body = [&](const int cl, const float z0) {
+              const int64_t c = c0 + cl;
+              const bool valid = c < a.n;
+                if constexpr (MODE == 1) {
+                float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
+                if (l == 0) {
+                  float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+                  if (valid) {
+                    x0 = a.x[c * 3 + 0];
+                    x1 = a.x[c * 3 + 1];
+                    x2 = a.x[c * 3 + 2];
+                    if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
+                  }
+                  if (mok) {
+                    const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
+                    z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0of(blk));
+                    t0 = om * w0;
+                    t1 = om * w1;
+                    t2 = om * w2;
+                  }
+                } else {
+                  float v[4];
+                  tc_ld_sum4<C>(taddr, cl * 4, v);  // centre cl's 4 columns
+                  if (mok) {
+                    z = v[0] + bias_l;
+                    t0 = v[1];
+                    t1 = v[2];
+                    t2 = v[3];
+                  }
+                }
+                if (valid) {
+                  if (step)
+                    *zg4(zt + cl * zcs, c, l, 0, m) = make_float4(z, t0, t1, t2);
+                  else
+                    *zc(zt + cl * zcs, c, l, m) = z;
+                }
+                float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+                if (mok) {
+                  const typename AF::C cc = AF::centre(z, beta);
+                  const float s1 = AF::d1(cc, beta);
+                  o0 = AF::value(cc, beta);
+                  o1 = s1 * t0;
+                  o2 = s1 * t1;
+                  o3 = s1 * t2;
+                }
+                skip_centre(l, m, c, valid, o0, o1, o2, o3);
+                if (last) {
+                  reduce4(blk, cl, wl, o0, o1, o2, o3);
+                } else {
+                  const float o4[4] = {o0, o1, o2, o3};
+                  if (need_free) {
+                    mbar_wait(bars.bfree, nd & 1u);
+                    need_free = false;
+                  }
+                  put_b4(cl * 4, m, o4);
+                }
+              } else {
+                const float* ci = cis + cl * NCINFO;
+                float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
+                if (l == 0) {
+                  if (mok) {
+                    const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
+                    const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
+                    const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
+                    const float hs = om * h;
+                    Av[0] = hs * du;
+                    Av[1] = hs * dv;
+                    Av[2] = hs * (du + dv);
+                    Av[3] = hs * (du - dv);
+                  }
+                } else {
+                  float v[8];
+                  tc_ld_sum8<C>(taddr, cl * 8, v);
+                  if (mok) {
+  #pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                      Av[p] = v[2 * p];
+                      Sv[p] = v[2 * p + 1];
+                    }
+                  }
+                }
+                if (step && valid) {
+                  float* zb = zt + cl * zcs;
+                  *zg4(zb, c, l, 1, m) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
+                  *zg4(zb, c, l, 2, m) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
+                }
+                float o[8];
+                {  // every lane (the pair maps vote on their fast form); rows past the width give 0
+                  const typename AF::C cc = AF::centre(z0, beta);
+                  AF::pairs_fwd4(cc, Av, Sv, beta, o);
+                  if (!mok) {
+  #pragma unroll
+                    for (int p = 0; p < 8; ++p) o[p] = 0.f;
+                  }
+                }
+                skip_pairs(l, m, ci, o);
+                if (last) {
+                  reduce4(blk, cl, wl, o[1], o[3], o[5], o[7]);
+                } else {
+                  if (need_free) {
+                    mbar_wait(bars.bfree, nd & 1u);
+                    need_free = false;
+                  }
+                  put_b8(cl * 8, m, o);
                 }
               }
-            }
-            if (step && valid) {
-              *zg4(c, l, 1) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
-              *zg4(c, l, 2) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
-            }
-            float o[8];
-            {  // every lane (the pair maps vote on their fast form); rows past the width give 0
-              const typename AF::C cc = AF::centre(z0, beta);
-              AF::pairs_fwd4(cc, Av, Sv, beta, o);
-              if (!mok) {
-#pragma unroll
-                for (int p = 0; p < 8; ++p) o[p] = 0.f;
+            };
+            {
+#pragma unroll kFwdUnroll
+              for (int i = 0; i < CPX; ++i) {
+                const int cl = egx + EGX * i;  // centre slot in the tile
+                const float z0 = z0n;
+                z0n = ldz(cl + EGX);
+                centre_body(cl, z0);
               }
             }
-            skip_pairs(l, ci, o);
-            if (last) {
-              reduce4(cl, o[1], o[3], o[5], o[7]);
-            } else {
-              put_b8(cl * 8, o);
+            if (l > 0) ptimer.end_b();
+            if (!last) {  // this M-block's rows of the next B operand (this warp's part): hand to the MMA
+              tc_epi_arrive(bars, HP ? blk : 0);
+            } else if (l > 0) {
+              tc::fence_before();
             }
-          }
+          }  // M-block
         }
-        if (l > 0) ptimer.end_b();
-        if (!last) {  // this split's B operand of layer l+1 (this warp's part): hand to the MMA thread
-          tc_epi_arrive(bars, sp);
-        } else if (l > 0) {
-          tc::fence_before();
-        }
-        }  // split
         if (l > 0) ++nd;
         if (l == 0 && pending) {  // the previous tile's per-centre work, overlapping the MMA phase
           if (ew == 0) finish(pend_c0, pend_red, pend_cis);

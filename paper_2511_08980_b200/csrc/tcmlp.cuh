@@ -66,7 +66,7 @@ __device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
 }
 
 template <int MPAD_, int N_, int NEPI_ = 8, int RANGES_ = 3, int STASH_ = 0, int NSPLIT_ = 1, int BMN_ = 0,
-          int NST_ = 6>
+          int NST_ = 6, int HP_ = 0>
 struct TcCfg {
   static constexpr int MPAD = MPAD_;
   static constexpr int N = N_;                  // GEMM columns per tile
@@ -97,6 +97,14 @@ struct TcCfg {
   static constexpr int BMN = BMN_;
   static constexpr int BSBO = 3 * (N / NSPLIT_) / 64 * 1024;
   static constexpr int NS = N / NSPLIT;
+  // M-half pipelining (two M-halves only): a layer's MMAs run as four groups (output half h,
+  // K half kh) in the order (0,0) (0,1) | (1,0) (1,1), with "D full" committed per output half,
+  // "B free" (B rows of K half 0 read by every MMA of the layer) after (1,0), and "B full" per
+  // K half.  The epilogue warps take the halves in turn: half 0's epilogue runs while the
+  // MMAs of output half 1 are in flight, and half 1's while the next layer's (0,0) group runs
+  // -- only the (0,1) group of each layer is left with no epilogue beside it.
+  static constexpr int HP = HP_;
+  static constexpr int NBF = HP ? 2 : NSPLIT;   // bfull / dfull barriers
   static constexpr int NEPI = NEPI_;            // epilogue warps (a multiple of 4 * MH)
   // warp-group aligned layout: warps 0..3 = control warp group (producer, MMA issuer, two idle
   // warps), warps EPI0.. = epilogue warp groups.  The control group gives registers back
@@ -127,30 +135,33 @@ struct TcCfg {
   static_assert(TUSE <= 512, "TMEM has 512 columns");
   static_assert(NEPI % (4 * MH) == 0, "every (lane quarter, M-half) needs the same number of epilogue warps");
   static_assert(!BMN || (NSPLIT == 1 && N % 64 == 0 && 8 * BSBO == BKC), "MN-major B: whole 64-column atoms");
+  static_assert(!HP || (MH == 2 && NSPLIT == 1 && MC == 1 && KC % 2 == 0), "M-half pipelining: two M-halves");
 };
 
 struct TcBars {
   uint64_t* wfull;
   uint64_t* wempty;
-  uint64_t* bfull;  // [NSPLIT]
-  uint64_t* dfull;  // [NSPLIT]
+  uint64_t* bfull;  // [NBF]
+  uint64_t* dfull;  // [NBF]
+  uint64_t* bfree;  // [1] (HP)
   uint32_t* tslot;
 };
 
-// barrier block: 2*NST + 2 mbarriers + the TMEM slot, at `p` (8-byte aligned)
+// barrier block: 2*NST + 2*NBF + 1 mbarriers + the TMEM slot, at `p` (8-byte aligned)
 template <class C>
 __device__ __forceinline__ TcBars tc_bars(unsigned char* p) {
   TcBars b;
   b.wfull = reinterpret_cast<uint64_t*>(p);
   b.wempty = b.wfull + C::NST;
   b.bfull = b.wempty + C::NST;
-  b.dfull = b.bfull + C::NSPLIT;
-  b.tslot = reinterpret_cast<uint32_t*>(b.dfull + C::NSPLIT);
+  b.dfull = b.bfull + C::NBF;
+  b.bfree = b.dfull + C::NBF;
+  b.tslot = reinterpret_cast<uint32_t*>(b.bfree + 1);
   return b;
 }
 template <class C>
 constexpr int tc_bars_bytes() {
-  return (2 * C::NST + 2 * C::NSPLIT) * 8 + 16;
+  return (2 * C::NST + 2 * C::NBF + 1) * 8 + 16;
 }
 
 // CTA prologue: barrier init (thread 0), TMEM allocation (warp 1); returns the TMEM base.
@@ -162,10 +173,11 @@ __device__ __forceinline__ uint32_t tc_setup(const TcBars& b) {
       mbar_init(&b.wfull[s], 1);
       mbar_init(&b.wempty[s], C::MC);  // freed by the MMA issuer of every CTA of the cluster
     }
-    for (int s = 0; s < C::NSPLIT; ++s) {
+    for (int s = 0; s < C::NBF; ++s) {
       mbar_init(&b.bfull[s], C::NEPI);
       mbar_init(&b.dfull[s], 1);
     }
+    mbar_init(b.bfree, 1);
     fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(b.tslot, C::TCOLS);
@@ -224,9 +236,10 @@ __device__ __forceinline__ void tc_producer(const unsigned char* img, int ngemm,
   for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x)
     for (int gi = 0; gi < ngemm * C::NSPLIT; ++gi) {  // each layer once per column split
       const int g = reverse ? ngemm - 1 - gi / C::NSPLIT : gi / C::NSPLIT;
-      for (int kc = 0; kc < C::KC; ++kc)
-        for (int h = 0; h < C::MH; ++h)
+      // block order of tc_mma: (kc, h) kc-major, or h-major under M-half pipelining
+      for (int blk = 0; blk < C::KC * C::MH; ++blk)
           for (int p = 0; p < tc::WP; p += C::WPS, ++it) {
+            const int kc = C::HP ? blk % C::KC : blk / C::MH, h = C::HP ? blk / C::KC : blk % C::MH;
             const int s = (int)(it % C::NST);
             const uint32_t ph = (it / C::NST) & 1u;
             mbar_wait_backoff(&b.wempty[s], ph ^ 1u);
@@ -265,74 +278,104 @@ __device__ __forceinline__ void tc_mma(int ngemm, int64_t ntiles, const unsigned
 #else
 #define TC_MMA_T(acc, stmt) stmt;
 #endif
+  // the (K chunk kc, M-half h) block of the current pass: the three weight pieces, piece-major
+  // (all K steps of a0, then of a1, then of a2; the first product into every range is a0's at
+  // kc = sub = 0, which overwrites)
+  auto issue_block = [&](int sp, int kc, int h) {
+    const uint32_t ba = smem_u32(Bs + kc * C::BKC + sp * 3 * C::NS * 128);
+    const uint32_t d = tbase + h * C::DH + sp * C::RANGES * C::NS;
+#pragma unroll
+    for (int p = 0; p < tc::WP; ++p) {
+      uint32_t wa;
+      int s = 0;
+      if (C::WPS == 1 || p == 0) {
+        s = (int)(it % C::NST);
+        const uint32_t ph = (it / C::NST) & 1u;
+        TC_MMA_T(tw, mbar_wait(&b.wfull[s], ph));
+        tc::fence_after();
+        ++it;
+      } else {
+        s = (int)((it - 1) % C::NST);
+      }
+      wa = smem_u32(Ws + s * C::STAGE) + (C::WPS == 1 ? 0 : p * 16384);
+      if constexpr (C::RANGES == 3) {
+        // a0 . [b0|b1|b2] (N = 3N: ranges 0, 1, 2), a1 . [b0|b1] (ranges 0, 1), a2 . b0 (range 0)
+        const uint32_t id = p == 0 ? id3 : (p == 1 ? id2 : id1);
+#pragma unroll
+        for (int sub = 0; sub < 4; ++sub) {
+          const uint64_t bd = C::BMN ? tc::sdesc_sw128_mn(ba + sub * 2 * C::BSBO, 1024, C::BSBO)
+                                     : tc::sdesc_sw128(ba + sub * 32);
+          tc::mma_bf16_w(d, tc::sdesc_sw128(wa + sub * 32), bd, id, (p | kc | sub) != 0 ? 1u : 0u);
+        }
+      } else {
+        // a0 . [b0|b1] (N = 2N: ranges 0, 1) and a0 . b2, a1 . [b0|b1], a2 . b0 (range 0): the
+        // six products, four A reads per K step instead of six
+        static_assert(!C::BMN, "two-range issue: K-major B only");
+#pragma unroll
+        for (int sub = 0; sub < 4; ++sub) {
+          const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);
+          const uint64_t a = tc::sdesc_sw128(wa + sub * 32);
+          if (p == 0) {
+            tc::mma_bf16_w(d, a, b01, id2, (kc | sub) != 0 ? 1u : 0u);
+            tc::mma_bf16_w(d, a, tc::sdesc_sw128(ba + 2 * C::NS * 128 + sub * 32), id1, 1u);
+          } else if (p == 1) {
+            tc::mma_bf16_w(d, a, b01, id2, 1u);
+          } else {
+            tc::mma_bf16_w(d, a, b01, id1, 1u);
+          }
+        }
+      }
+      if (C::WPS == 1 || p == tc::WP - 1) {
+        if (C::MC == 1)
+          tc::mma_commit_w(&b.wempty[s]);
+        else
+          mma_commit_mc_w(&b.wempty[s], (uint16_t)0x3);  // the stage is free in both CTAs
+      }
+    }
+  };
   const int64_t tend = tc_tile_end<C>(ntiles);
   for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x)
     for (int gs = 0; gs < ngemm * C::NSPLIT; ++gs, ++nb) {
-      const int sp = gs % C::NSPLIT;  // column split of this pass
-      TC_MMA_T(tb, mbar_wait_backoff(&b.bfull[sp], (nb / C::NSPLIT) & 1u));
+      if constexpr (C::HP) {
+        // groups (h, kh) in the order (0,0) (0,1) (1,0) (1,1); see TcCfg::HP
+        const uint32_t ph = nb & 1u;
 #ifdef FDSDF_PHASE_TIMING
-      const long long tstart = clock64();
+        long long tstart = 0;
 #endif
-      tc::fence_after();
-      for (int kc = 0; kc < C::KC; ++kc)
-        for (int h = 0; h < C::MH; ++h) {
-          const uint32_t ba = smem_u32(Bs + kc * C::BKC + sp * 3 * C::NS * 128);
-          const uint32_t d = tbase + h * C::DH + sp * C::RANGES * C::NS;
-          // piece-major within the (kc, h) block: all K steps of a0, then of a1, then of a2 (the
-          // first product into every range is a0's at kc = sub = 0, which overwrites)
-#pragma unroll
-          for (int p = 0; p < tc::WP; ++p) {
-            uint32_t wa;
-            int s = 0;
-            if (C::WPS == 1 || p == 0) {
-              s = (int)(it % C::NST);
-              const uint32_t ph = (it / C::NST) & 1u;
-              TC_MMA_T(tw, mbar_wait(&b.wfull[s], ph));
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+          for (int kh = 0; kh < 2; ++kh) {
+            if (h == 0) {
+              TC_MMA_T(tb, mbar_wait_backoff(&b.bfull[kh], ph));
               tc::fence_after();
-              ++it;
-            } else {
-              s = (int)((it - 1) % C::NST);
-            }
-            wa = smem_u32(Ws + s * C::STAGE) + (C::WPS == 1 ? 0 : p * 16384);
-            if constexpr (C::RANGES == 3) {
-              // a0 . [b0|b1|b2] (N = 3N: ranges 0, 1, 2), a1 . [b0|b1] (ranges 0, 1), a2 . b0 (range 0)
-              const uint32_t id = p == 0 ? id3 : (p == 1 ? id2 : id1);
-#pragma unroll
-              for (int sub = 0; sub < 4; ++sub) {
-                const uint64_t bd = C::BMN ? tc::sdesc_sw128_mn(ba + sub * 2 * C::BSBO, 1024, C::BSBO)
-                                           : tc::sdesc_sw128(ba + sub * 32);
-                tc::mma_bf16_w(d, tc::sdesc_sw128(wa + sub * 32), bd, id, (p | kc | sub) != 0 ? 1u : 0u);
-              }
-            } else {
-              // a0 . [b0|b1] (N = 2N: ranges 0, 1) and a0 . b2, a1 . [b0|b1], a2 . b0 (range 0): the
-              // six products, four A reads per K step instead of six
-              static_assert(!C::BMN, "two-range issue: K-major B only");
-#pragma unroll
-              for (int sub = 0; sub < 4; ++sub) {
-                const uint64_t b01 = tc::sdesc_sw128(ba + sub * 32);
-                const uint64_t a = tc::sdesc_sw128(wa + sub * 32);
-                if (p == 0) {
-                  tc::mma_bf16_w(d, a, b01, id2, (kc | sub) != 0 ? 1u : 0u);
-                  tc::mma_bf16_w(d, a, tc::sdesc_sw128(ba + 2 * C::NS * 128 + sub * 32), id1, 1u);
-                } else if (p == 1) {
-                  tc::mma_bf16_w(d, a, b01, id2, 1u);
-                } else {
-                  tc::mma_bf16_w(d, a, b01, id1, 1u);
-                }
-              }
-            }
-            if (C::WPS == 1 || p == tc::WP - 1) {
-              if (C::MC == 1)
-                tc::mma_commit_w(&b.wempty[s]);
-              else
-                mma_commit_mc_w(&b.wempty[s], (uint16_t)0x3);  // the stage is free in both CTAs
-            }
-          }
-        }
-      tc::mma_commit_w(&b.dfull[sp]);
 #ifdef FDSDF_PHASE_TIMING
-      tspan += clock64() - tstart;
+              if (kh == 0) tstart = clock64();
 #endif
+            }
+#pragma unroll 1
+            for (int kc = kh * (C::KC / 2); kc < (kh + 1) * (C::KC / 2); ++kc) issue_block(0, kc, h);
+            if (h == 1 && kh == 0) tc::mma_commit_w(b.bfree);
+          }
+          tc::mma_commit_w(&b.dfull[h]);
+        }
+#ifdef FDSDF_PHASE_TIMING
+        tspan += clock64() - tstart;
+#endif
+      } else {
+        const int sp = gs % C::NSPLIT;  // column split of this pass
+        TC_MMA_T(tb, mbar_wait_backoff(&b.bfull[sp], (nb / C::NSPLIT) & 1u));
+#ifdef FDSDF_PHASE_TIMING
+        const long long tstart = clock64();
+#endif
+        tc::fence_after();
+        for (int kc = 0; kc < C::KC; ++kc)
+          for (int h = 0; h < C::MH; ++h) issue_block(sp, kc, h);
+        tc::mma_commit_w(&b.dfull[sp]);
+#ifdef FDSDF_PHASE_TIMING
+        tspan += clock64() - tstart;
+#endif
+      }
     }
 #ifdef FDSDF_PHASE_TIMING
   if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
