@@ -138,6 +138,83 @@ struct Act<ACT_SINE> {
     *Dd = -p.sy * p.sA;
     *Z = fmaf(-4.0f * p.cy, p.s2A, 2.0f * p.dyc);
   }
+  // pre_fast on two pairs at once (packed fp32 x2: per lane exactly the scalar arithmetic)
+  struct P2x2 {
+    float2 sy, cy, sA, cA, s2A, dys, dyc;
+  };
+  __device__ __forceinline__ static P2x2 pre_fast2(const C& c, float2 A, float2 S) {
+    P2x2 p;
+    const float2 a2 = mul2(A, A);
+    float2 q = fma2(a2, f2s(2.7557319224e-6f), f2s(-1.9841269841e-4f));
+    q = fma2(a2, q, f2s(8.3333333333e-3f));
+    q = fma2(a2, q, f2s(-1.6666666667e-1f));
+    p.sA = fma2(mul2(A, a2), q, A);
+    float2 r = fma2(a2, f2s(1.3778659612e-7f), f2s(-1.2400793651e-5f));
+    r = fma2(a2, r, f2s(6.9444444444e-4f));
+    r = fma2(a2, r, f2s(-2.0833333333e-2f));
+    r = fma2(a2, r, f2s(0.25f));
+    p.s2A = mul2(a2, r);
+    p.cA = fma2(f2s(-2.0f), p.s2A, f2s(1.0f));
+    const float2 y = mul2(f2s(0.5f), S), y2 = mul2(y, y);
+    float2 t = fma2(y2, f2s(-1.9841269841e-4f), f2s(8.3333333333e-3f));
+    t = fma2(y2, t, f2s(-1.6666666667e-1f));
+    const float2 sS2 = fma2(mul2(y, y2), t, y);
+    float2 w = fma2(y2, f2s(6.9444444444e-4f), f2s(-2.0833333333e-2f));
+    w = fma2(y2, w, f2s(0.25f));
+    const float2 s2S = mul2(y2, w);
+    // (-2 s2S) sz = s2S (-2 sz) and (-sS2) sz = sS2 (-sz) exactly (power-of-two / sign scalings)
+    p.dys = fma2(sS2, f2s(c.cz), mul2(s2S, f2s(-2.0f * c.sz)));
+    p.dyc = fma2(sS2, f2s(-c.sz), mul2(s2S, f2s(-2.0f * c.cz)));
+    p.sy = add2(f2s(c.sz), p.dys);
+    p.cy = add2(f2s(c.cz), p.dyc);
+    return p;
+  }
+  __device__ __forceinline__ static bool fast_ok(const float2 (&A)[2], const float2 (&S)[2]) {
+    const float mA = fmaxf(fmaxf(fabsf(A[0].x), fabsf(A[0].y)), fmaxf(fabsf(A[1].x), fabsf(A[1].y)));
+    const float mS = fmaxf(fmaxf(fabsf(S[0].x), fabsf(S[0].y)), fmaxf(fabsf(S[1].x), fabsf(S[1].y)));
+    return FDSDF_PAIR_FAST && __all_sync(0xffffffffu, mA <= FAST_A && mS <= FAST_S);
+  }
+  // all 4 pairs of a centre, packed by two: A[k] = (A_{2k}, A_{2k+1}), S[k] likewise; out the same
+  // packing of A_a, S_a (warp-uniform choice of the fast form; every lane of the warp calls this)
+  __device__ __forceinline__ static void pairs_fwd4x2(const C& c, const float2 (&A)[2], const float2 (&S)[2],
+                                                      float beta, float2 (&Aa)[2], float2 (&Sa)[2]) {
+    if (fast_ok(A, S)) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const P2x2 p = pre_fast2(c, A[k], S[k]);
+        Aa[k] = mul2(p.cy, p.sA);
+        Sa[k] = fma2(mul2(f2s(-4.0f), p.sy), p.s2A, mul2(f2s(2.0f), p.dys));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        pair_fwd(c, A[k].x, S[k].x, beta, &Aa[k].x, &Sa[k].x);
+        pair_fwd(c, A[k].y, S[k].y, beta, &Aa[k].y, &Sa[k].y);
+      }
+    }
+  }
+  // + the derivative factors P, Dd, Z (same packing)
+  __device__ __forceinline__ static void pairs_bwd4x2(const C& c, const float2 (&A)[2], const float2 (&S)[2],
+                                                      float beta, float2 (&Aa)[2], float2 (&Sa)[2], float2 (&P)[2],
+                                                      float2 (&Dd)[2], float2 (&Z)[2]) {
+    if (fast_ok(A, S)) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const P2x2 p = pre_fast2(c, A[k], S[k]);
+        Aa[k] = mul2(p.cy, p.sA);
+        Sa[k] = fma2(mul2(f2s(-4.0f), p.sy), p.s2A, mul2(f2s(2.0f), p.dys));
+        P[k] = mul2(p.cy, p.cA);
+        Dd[k] = mul2(make_float2(-p.sy.x, -p.sy.y), p.sA);
+        Z[k] = fma2(mul2(f2s(-4.0f), p.cy), p.s2A, mul2(f2s(2.0f), p.dyc));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        pair_bwd(c, A[k].x, S[k].x, beta, &Aa[k].x, &Sa[k].x, &P[k].x, &Dd[k].x, &Z[k].x);
+        pair_bwd(c, A[k].y, S[k].y, beta, &Aa[k].y, &Sa[k].y, &P[k].y, &Dd[k].y, &Z[k].y);
+      }
+    }
+  }
   // all 4 pairs of a centre: t[5p .. 5p+4] = A_a, S_a, P, Dd, Z (warp-uniform fast form);
   // `all` = every lane of the warp calls this (else the general form, no vote)
   __device__ __forceinline__ static void pairs_bwd4(const C& c, const float (&A)[4], const float (&S)[4], float beta,
@@ -222,6 +299,24 @@ struct Act<ACT_SOFTPLUS> {
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       pair_bwd(c, A[q], S[q], beta, &t[5 * q], &t[5 * q + 1], &t[5 * q + 2], &t[5 * q + 3], &t[5 * q + 4]);
+  }
+  // the packed-by-two interface of the sine maps (scalar arithmetic here)
+  __device__ __forceinline__ static void pairs_fwd4x2(const C& c, const float2 (&A)[2], const float2 (&S)[2],
+                                                      float beta, float2 (&Aa)[2], float2 (&Sa)[2]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      pair_fwd(c, A[k].x, S[k].x, beta, &Aa[k].x, &Sa[k].x);
+      pair_fwd(c, A[k].y, S[k].y, beta, &Aa[k].y, &Sa[k].y);
+    }
+  }
+  __device__ __forceinline__ static void pairs_bwd4x2(const C& c, const float2 (&A)[2], const float2 (&S)[2],
+                                                      float beta, float2 (&Aa)[2], float2 (&Sa)[2], float2 (&P)[2],
+                                                      float2 (&Dd)[2], float2 (&Z)[2]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      pair_bwd(c, A[k].x, S[k].x, beta, &Aa[k].x, &Sa[k].x, &P[k].x, &Dd[k].x, &Z[k].x);
+      pair_bwd(c, A[k].y, S[k].y, beta, &Aa[k].y, &Sa[k].y, &P[k].y, &Dd[k].y, &Z[k].y);
+    }
   }
   __device__ __forceinline__ static void pair_bwd(const C& c, float A, float S, float beta, float* Aa,
                                                   float* Sa, float* P, float* Dd, float* Z) {

@@ -173,10 +173,10 @@ __global__ void __launch_bounds__(NTH, 2) bwd_kernel(const BwdArgs a) {
           float Av[4], Sv[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {  // (A_p, S_p): half (p & 1) of group 1 + p / 2
-            const float2 as = valid ? reinterpret_cast<const float2*>(zq + (1 + (p >> 1)) * MPAD + mb + j)[p & 1]
-                                    : make_float2(0.f, 0.f);
-            Av[j] = as.x;
-            Sv[j] = as.y;
+            // group 1 + p / 2 = (A_{2k}, A_{2k+1}, S_{2k}, S_{2k+1}), k = p / 2 (kernels.cuh)
+            const float4 g = valid ? zq[(1 + (p >> 1)) * MPAD + mb + j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            Av[j] = (p & 1) ? g.y : g.x;
+            Sv[j] = (p & 1) ? g.w : g.z;
           }
           // offset d_p (for the skip x-part and layer-0 weight gradient)
           const float dpx = p == 0 ? u0 : (p == 1 ? v0 : (p == 2 ? u0 + v0 : u0 - v0));

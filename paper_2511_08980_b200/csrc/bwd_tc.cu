@@ -37,10 +37,6 @@ namespace fdsdf {
 #define BWD_TC_UNROLL 1
 #endif
 constexpr int kBwdUnroll = BWD_TC_UNROLL;
-// 1: phase A's pair maps take act.cuh's warp-uniform fast series form (pairs_bwd4)
-#ifndef BWD_TC_FASTPAIR
-#define BWD_TC_FASTPAIR 0
-#endif
 // stores of delta / the layer activations (read once, by the weight-gradient kernel after the
 // whole backward): 1 = streaming (st.global.cs, evict-first), 0 = default caching
 #ifndef BWD_TC_STCS
@@ -201,6 +197,28 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
     const bool pipe_top = BWD_TC_PIPE_TOP && ngemm > 0;
     // this thread's last-layer weight (fan-out 1), loaded once instead of per top-layer centre
     const float wlast = m < net.width[ltop + 1] ? net.W[L - 1][m] : 0.f;
+    // the pair maps of a centre's 4 pairs, two pairs per packed fp32 x2 lane pair, into
+    // t[5 p .. 5 p + 4] = A_a, S_a, P, Dd, Z of pair p (zero on rows past the width); every lane
+    // of the warp calls this (the sine maps vote on their fast form)
+    auto pair_maps = [&](const typename AF::C& cc, bool mk, const float (&A)[4], const float (&S)[4], float (&t)[20]) {
+      const float2 A2[2] = {make_float2(A[0], A[1]), make_float2(A[2], A[3])};
+      const float2 S2[2] = {make_float2(S[0], S[1]), make_float2(S[2], S[3])};
+      float2 Aa[2], Sa[2], P[2], Dd[2], Z[2];
+      AF::pairs_bwd4x2(cc, A2, S2, beta, Aa, Sa, P, Dd, Z);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        t[10 * k + 0] = mk ? Aa[k].x : 0.f;
+        t[10 * k + 1] = mk ? Sa[k].x : 0.f;
+        t[10 * k + 2] = mk ? P[k].x : 0.f;
+        t[10 * k + 3] = mk ? Dd[k].x : 0.f;
+        t[10 * k + 4] = mk ? Z[k].x : 0.f;
+        t[10 * k + 5] = mk ? Aa[k].y : 0.f;
+        t[10 * k + 6] = mk ? Sa[k].y : 0.f;
+        t[10 * k + 7] = mk ? P[k].y : 0.f;
+        t[10 * k + 8] = mk ? Dd[k].y : 0.f;
+        t[10 * k + 9] = mk ? Z[k].y : 0.f;
+      }
+    };
     // this thread's stored pre-activations of top-layer centre i of tile tl (zero if none)
     auto top_load = [&](int64_t tl, int i, float4 (&zg)[ZG]) {
       const int64_t c = tl * CT + eg + EG * i;
@@ -214,7 +232,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
     auto top_centre = [&](int64_t tl, int i, const float* sdsT, const float4 (&zg)[ZG]) {
       const int cl = eg + EG * i;
       const int64_t c = tl * CT + cl;
-      if (tl >= a.ntiles || c >= a.n || m >= net.width[ltop + 1]) return;
+      if (tl >= a.ntiles || c >= a.n) return;  // warp-uniform: the pair maps below vote
+      const bool mk = m < net.width[ltop + 1];
       const float omt = net.omega[ltop];
       const float wlt = wlast;
       FDSDF_ASSERT(c >= 0 && c < a.n);
@@ -230,12 +249,17 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
       const float* sd = sdsT + cl * 20;
       const float dL[NCOLB] = {sd[0], 1.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
       const typename AF::C cc = AF::centre(zv[0], beta);
+      float t[20];
+      {
+        const float A[4] = {zv[4], zv[5], zv[8], zv[9]}, S[4] = {zv[6], zv[7], zv[10], zv[11]};  // kernels.cuh zf
+        pair_maps(cc, mk, A, S, t);
+      }
+      if (!mk) return;
       float dl[NCOLB], pv[NCOLB];
       float zbar = 0.f;
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
-        float Aa, Sa, P, Dd, Z;
-        AF::pair_bwd(cc, zv[4 + 2 * p], zv[5 + 2 * p], beta, &Aa, &Sa, &P, &Dd, &Z);
+        const float Aa = t[5 * p], Sa = t[5 * p + 1], P = t[5 * p + 2], Dd = t[5 * p + 3], Z = t[5 * p + 4];
         const float XA = wlt * dL[2 + 2 * p], XS = wlt * dL[3 + 2 * p];
         dl[2 + 2 * p] = omt * fmaf(XA, P, 2.0f * XS * Dd);
         dl[3 + 2 * p] = omt * fmaf(0.5f * XA, Dd, XS * P);
@@ -351,12 +375,12 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
             q.t1 = g0.z;
             q.t2 = g0.w;
             q.A[0] = g1.x;
-            q.S[0] = g1.y;
-            q.A[1] = g1.z;
+            q.A[1] = g1.y;
+            q.S[0] = g1.z;
             q.S[1] = g1.w;
             q.A[2] = g2.x;
-            q.S[2] = g2.y;
-            q.A[3] = g2.z;
+            q.A[3] = g2.y;
+            q.S[2] = g2.z;
             q.S[3] = g2.w;
           }
           return q;
@@ -377,27 +401,12 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
 #pragma unroll
             for (int j = 0; j < NCOLB; ++j) pv[j] = 0.f;
             float cs1 = 0.f, cs2tr = 0.f;
-#if BWD_TC_FASTPAIR
-            typename AF::C ccf{};
-            if (valid) {  // every lane of the warp: the pair maps vote on their fast series form
-              ccf = AF::centre(q.z, beta);
-              AF::pairs_bwd4(ccf, q.A, q.S, beta, t);
-              if (!mok) {
-#pragma unroll
-                for (int j = 0; j < 20; ++j) t[j] = 0.f;
-              }
+            typename AF::C cc{};
+            if (valid) {  // every lane of the warp: the sine maps vote on their fast series form
+              cc = AF::centre(q.z, beta);
+              pair_maps(cc, mok, q.A, q.S, t);
             }
-#endif
             if (mok && valid) {
-#if BWD_TC_FASTPAIR
-              const typename AF::C cc = ccf;
-#else
-              const typename AF::C cc = AF::centre(q.z, beta);
-#pragma unroll
-              for (int p = 0; p < 4; ++p)
-                AF::pair_bwd(cc, q.A[p], q.S[p], beta, &t[5 * p], &t[5 * p + 1], &t[5 * p + 2], &t[5 * p + 3],
-                             &t[5 * p + 4]);
-#endif
               {  // the layer's activations (wgrad operand) are X-independent: stored here
                 const float* sd = sds + cl * 20;
                 const float tr = fmaf(sd[5], q.t0, fmaf(sd[6], q.t1, sd[7] * q.t2));

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(BlCfg<MPAD, PAIR>::NTHR, 1)
 #pragma unroll
         for (int j = 0; j < NCOLB; ++j) dl[j] = pv[j] = 0.f;
         if (valid && mok) {
-          const float Av[4] = {g1.x, g1.z, g2.x, g2.z}, Sv[4] = {g1.y, g1.w, g2.y, g2.w};
+          const float Av[4] = {g1.x, g1.y, g2.x, g2.y}, Sv[4] = {g1.z, g1.w, g2.z, g2.w};
           const float tr = fmaf(r0, g0.y, fmaf(r1, g0.z, r2 * g0.w));
           const typename AF::C cc = AF::centre(g0.x, beta);
           float zbar = 0.f;

@@ -129,6 +129,15 @@ __device__ __forceinline__ void bar_compute(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+// ----------------------------------------------------------------------------- packed fp32 x2
+// sm_100 FFMA2 / FADD2 / FMUL2: two independent fp32 lanes per instruction, each rounded exactly
+// as the scalar instruction would (so a packed evaluation is bitwise the scalar one); half the
+// issue slots of the scalar form for the pair maps, which run two pairs per lane pair
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
 // ----------------------------------------------------------------------------- accurate fp32 math
 
 // sin and cos of x, |x| up to ~1e5, error ~1-2 ulp (relative for small |x|).

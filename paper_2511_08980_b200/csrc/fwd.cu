@@ -303,8 +303,8 @@ __global__ void __launch_bounds__(NTH, 2) fwd_kernel(const FwdArgs a) {
           if (step && valid) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              *zg4(c, l, 1, mb + j) = make_float4(Av[j][0], Sv[j][0], Av[j][1], Sv[j][1]);
-              *zg4(c, l, 2, mb + j) = make_float4(Av[j][2], Sv[j][2], Av[j][3], Sv[j][3]);
+              *zg4(c, l, 1, mb + j) = make_float4(Av[j][0], Av[j][1], Sv[j][0], Sv[j][1]);
+              *zg4(c, l, 2, mb + j) = make_float4(Av[j][2], Av[j][3], Sv[j][2], Sv[j][3]);
             }
           }
 #pragma unroll

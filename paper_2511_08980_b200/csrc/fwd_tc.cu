@@ -270,17 +270,33 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
     auto skip_pairs = [&](int l, int m, const float* ci, float (&o)[8]) {
       if (l + 1 != net.skip) return;
       const int M = net.width[l + 1];
-      if (m >= M && m < M + 3) {  // odd part of x0 +- h d_p = h d_p, even part 0
+      if (m >= M && m < M + 3) {  // odd part of x0 +- h d_p = h d_p, even part 0 (column order: see kPairCol)
         const int d = m - M;
         const float ud = ci[4 + d], vd = ci[7 + d];
         o[0] = h * ud;
-        o[2] = h * vd;
+        o[1] = h * vd;
         o[4] = h * (ud + vd);
-        o[6] = h * (ud - vd);
-        o[1] = o[3] = o[5] = o[7] = 0.f;
+        o[5] = h * (ud - vd);
+        o[2] = o[3] = o[6] = o[7] = 0.f;
       }
 #pragma unroll
       for (int p = 0; p < 8; ++p) o[p] *= RSQ2;
+    };
+    // the pair maps of all 4 pairs of a centre (packed by two: A2[k] = (A_{2k}, A_{2k+1})) -> the
+    // next layer's 8 B columns of the centre in the order A0 A1 S0 S1 A2 A3 S2 S3 (kPairCol: the
+    // accumulator columns come back in that order, i.e. already packed by two); every lane calls
+    // this (the sine maps vote on their fast form); rows past the width give 0
+    auto pair_outputs = [&](float z0, bool mok, const float2 (&A2)[2], const float2 (&S2)[2], float (&o)[8]) {
+      const typename AF::C cc = AF::centre(z0, beta);
+      float2 Aa[2], Sa[2];
+      AF::pairs_fwd4x2(cc, A2, S2, beta, Aa, Sa);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        o[4 * k] = mok ? Aa[k].x : 0.f;
+        o[4 * k + 1] = mok ? Aa[k].y : 0.f;
+        o[4 * k + 2] = mok ? Sa[k].x : 0.f;
+        o[4 * k + 3] = mok ? Sa[k].y : 0.f;
+      }
     };
     const bool pipe0 = FWD_PIPE0 && ngemm > 0;
     FDSDF_ASSERT(!FWD_PIPE0 || (MH * C::DH + MH * EGX * CPX * CPC) <= (int)C::TCOLS);
@@ -346,30 +362,21 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
         const float* ci = cis_t + cl * NCINFO;
         const float* zb = zrow(c);
         const float z0 = valid ? __ldg(zc(zb, c, 0, m)) : 0.f;
-        float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
+        float2 A2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, S2[2] = {A2[0], A2[0]};
         if (mok) {
           const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
           const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
           const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
           const float hs = om * h;
-          Av[0] = hs * du;
-          Av[1] = hs * dv;
-          Av[2] = hs * (du + dv);
-          Av[3] = hs * (du - dv);
+          A2[0] = make_float2(hs * du, hs * dv);
+          A2[1] = make_float2(hs * (du + dv), hs * (du - dv));
         }
         if (step && valid) {
-          *zg4(zb, c, 0, 1, m) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
-          *zg4(zb, c, 0, 2, m) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
+          *zg4(zb, c, 0, 1, m) = make_float4(A2[0].x, A2[0].y, S2[0].x, S2[0].y);
+          *zg4(zb, c, 0, 2, m) = make_float4(A2[1].x, A2[1].y, S2[1].x, S2[1].y);
         }
         float o[8];
-        {  // every lane (the pair maps vote on their fast form); rows past the width give 0
-          const typename AF::C cc = AF::centre(z0, beta);
-          AF::pairs_fwd4(cc, Av, Sv, beta, o);
-          if (!mok) {
-#pragma unroll
-            for (int p = 0; p < 8; ++p) o[p] = 0.f;
-          }
-        }
+        pair_outputs(z0, mok, A2, S2, o);
         skip_pairs(0, m, ci, o);
         float o4[4] = {o[0], o[1], o[2], o[3]};
         tc::tmem_st4(tstash + i * CPC, o4);
@@ -597,46 +604,36 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
                 }
               } else {
                 const float* ci = cis + cl * NCINFO;
-                float Av[4] = {0.f, 0.f, 0.f, 0.f}, Sv[4] = {0.f, 0.f, 0.f, 0.f};
+                float2 A2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, S2[2] = {A2[0], A2[0]};
                 if (l == 0) {
                   if (mok) {
                     const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
                     const float du = fmaf(w0, ci[4], fmaf(w1, ci[5], w2 * ci[6]));
                     const float dv = fmaf(w0, ci[7], fmaf(w1, ci[8], w2 * ci[9]));
                     const float hs = om * h;
-                    Av[0] = hs * du;
-                    Av[1] = hs * dv;
-                    Av[2] = hs * (du + dv);
-                    Av[3] = hs * (du - dv);
+                    A2[0] = make_float2(hs * du, hs * dv);
+                    A2[1] = make_float2(hs * (du + dv), hs * (du - dv));
                   }
                 } else {
                   float v[8];
-                  tc_ld_sum8<C>(taddr, cl * 8, v);
+                  tc_ld_sum8<C>(taddr, cl * 8, v);  // columns A0 A1 S0 S1 A2 A3 S2 S3 (kPairCol)
                   if (mok) {
-  #pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                      Av[p] = v[2 * p];
-                      Sv[p] = v[2 * p + 1];
-                    }
+                    A2[0] = make_float2(v[0], v[1]);
+                    S2[0] = make_float2(v[2], v[3]);
+                    A2[1] = make_float2(v[4], v[5]);
+                    S2[1] = make_float2(v[6], v[7]);
                   }
                 }
                 if (step && valid) {
                   float* zb = zt + cl * zcs;
-                  *zg4(zb, c, l, 1, m) = make_float4(Av[0], Sv[0], Av[1], Sv[1]);
-                  *zg4(zb, c, l, 2, m) = make_float4(Av[2], Sv[2], Av[3], Sv[3]);
+                  *zg4(zb, c, l, 1, m) = make_float4(A2[0].x, A2[0].y, S2[0].x, S2[0].y);
+                  *zg4(zb, c, l, 2, m) = make_float4(A2[1].x, A2[1].y, S2[1].x, S2[1].y);
                 }
                 float o[8];
-                {  // every lane (the pair maps vote on their fast form); rows past the width give 0
-                  const typename AF::C cc = AF::centre(z0, beta);
-                  AF::pairs_fwd4(cc, Av, Sv, beta, o);
-                  if (!mok) {
-  #pragma unroll
-                    for (int p = 0; p < 8; ++p) o[p] = 0.f;
-                  }
-                }
+                pair_outputs(z0, mok, A2, S2, o);
                 skip_pairs(l, m, ci, o);
                 if (last) {
-                  reduce4(blk, cl, wl, o[1], o[3], o[5], o[7]);
+                  reduce4(blk, cl, wl, o[2], o[3], o[6], o[7]);
                 } else {
                   if (need_free) {
                     mbar_wait(bars.bfree, nd & 1u);

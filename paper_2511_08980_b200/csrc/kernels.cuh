@@ -15,7 +15,7 @@ constexpr int NTH = NCT;           // thread 0 also issues the TMA weight slabs
 constexpr int NCOLF = 12;          // stored forward columns per centre: c, t0..2, (A,S) x 4
 // zf (the step's stored pre-activations) layout: [n][nh][NCOLF/4][mpad][4] -- per (centre,
 // hidden layer), the 12 columns in float4 groups per neuron m: g0 = (z, t0, t1, t2),
-// g1 = (A0, S0, A1, S1), g2 = (A2, S2, A3, S3) (one 16-byte access per group and neuron; a
+// g1 = (A0, A1, S0, S1), g2 = (A2, A3, S2, S3) (one 16-byte access per group and neuron; a
 // warp's 32 neurons are 512 contiguous bytes).  Eval stores z only, contiguous over m at the
 // start of each (centre, layer) block of zcols * mpad floats (zcols = 1 on eval-only contexts).
 constexpr int ZG = NCOLF / 4;      // float4 groups of zf per (centre, layer)

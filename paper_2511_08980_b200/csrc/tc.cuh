@@ -46,8 +46,10 @@ __device__ __forceinline__ void split3x2(float x, float y, uint32_t (&w)[3]) {
     const __nv_bfloat162 b = __floats2bfloat162_rn(x, y);
     const uint32_t u = *reinterpret_cast<const uint32_t*>(&b);
     w[p] = u;
-    x -= __uint_as_float(u << 16);
-    y -= __uint_as_float(u & 0xFFFF0000u);
+    // (x, y) -= the two pieces, one packed fp32 x2 subtraction (exact: each residual fits fp32)
+    const float2 r = add2(make_float2(x, y), make_float2(-__uint_as_float(u << 16), -__uint_as_float(u & 0xFFFF0000u)));
+    x = r.x;
+    y = r.y;
   }
 }
 
