@@ -34,7 +34,7 @@ namespace fdsdf {
 // arrays then live in local memory); CPE (4) unrolls them, so the carries stay in registers and
 // the loads of later centres can be hoisted
 #ifndef BWD_TC_UNROLL
-#define BWD_TC_UNROLL 1
+#define BWD_TC_UNROLL 4
 #endif
 constexpr int kBwdUnroll = BWD_TC_UNROLL;
 // stores of delta / the layer activations (read once, by the weight-gradient kernel after the

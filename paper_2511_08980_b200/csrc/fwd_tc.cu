@@ -39,7 +39,7 @@ namespace fdsdf {
 #endif
 // unroll of the per-centre epilogue loop (1 = rolled)
 #ifndef FWD_TC_UNROLL
-#define FWD_TC_UNROLL 1
+#define FWD_TC_UNROLL 2
 #endif
 constexpr int kFwdUnroll = FWD_TC_UNROLL;
 // GEMM columns per tile (mode 1: N/4 centres, mode 2: N/8 centres); with FWD_TC_NEPI the
