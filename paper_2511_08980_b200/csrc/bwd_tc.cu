@@ -62,7 +62,7 @@ __device__ __forceinline__ void bwd_st(float* p, float v) {
 // 1: one epilogue warp polls "D full", the others wait in a named barrier (no spinning warps
 // beside the ones still in phase A)
 #ifndef BWD_TC_POLL1
-#define BWD_TC_POLL1 1
+#define BWD_TC_POLL1 0
 #endif
 #ifndef BWD_TC_CARRY
 #define BWD_TC_CARRY 1
@@ -299,7 +299,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
       const size_t drow0 = (size_t)c0 * NCOLB * MPAD + m;    // its first delta / activation row, + m
       // this tile's first MMA pass reads layer L-3; the next tile's top layer (computed during
       // this tile's passes) reads layer L-2 of that tile
-      prefetch_layer(tile, L - 3);
+      if (tile == blockIdx.x) prefetch_layer(tile, L - 3);  // later tiles: during the previous tile
       prefetch_layer(tile + gridDim.x, L - 2);
       cp_async_wait_all();
       bar_named(1, C::NEPI * 32);  // this tile's seeds are in; every thread is done with the other buffer
@@ -355,7 +355,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
         const float db_l = r_db[l];  // local-memory read issued here, consumed after phase B
         constexpr bool CARRY = BWD_TC_CARRY;
         float c_s1[CPE], c_s2tr[CPE];  // CARRY: sigma'(z), sigma''(z) (r . t) per centre of this thread
-        if (!top) prefetch_layer(tile, l - 1);  // the next pass's phase A
+        // the next pass's phase A: layer l - 1 of this tile, or the next tile's first GEMM layer
+        if (!top) prefetch_layer(l > 0 ? tile : tile + gridDim.x, l > 0 ? l - 1 : L - 3);
         // ---- phase A (X-independent, overlaps this layer's MMA): the pair maps of every
         // centre of this thread -- A_a, S_a and the derivative factors P, Dd, Z -- from the
         // stored forward pre-activations, stashed in this thread's TMEM lane

@@ -30,6 +30,10 @@
 
 namespace fdsdf {
 
+// 1: every epilogue warp polls "D full" itself; 0: one warp polls, the others wait in a named barrier
+#ifndef FWD_TC_POLLALL
+#define FWD_TC_POLLALL 1
+#endif
 // M-half pipelining of the 256-wide layers (tcmlp.cuh TcCfg::HP): 1 = on
 #ifndef FWD_TC_HP
 #define FWD_TC_HP 1
@@ -538,8 +542,12 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
               ptimer.before_wait();
               // one warp polls the mbarrier, the others sleep in a hardware named barrier (no
               // spin instructions competing with the MMA warp for issue slots)
-              if (ew == 0) mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
-              bar_named(2, C::NEPI * 32);
+              if (FWD_TC_POLLALL) {  // every warp waits for itself (no wait for the slowest warp)
+                mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
+              } else {
+                if (ew == 0) mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
+                bar_named(2, C::NEPI * 32);
+              }
               ptimer.after_wait();
               tc::fence_after();
             }
