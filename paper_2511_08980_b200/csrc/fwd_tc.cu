@@ -174,12 +174,12 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tbase = tc_setup<C>(bars);
 
-  if (warp < C::EPI0) {
+  if (tc_is_ctl<C>(warp)) {
     // control warp group: producer (warp 0), MMA issuer (warp 1), two idle warps
     setmaxnreg_dec<C::REG_CTL>();
-    if (warp == 0) {
+    if (warp == C::CTL0) {
       if (lane == 0 && ngemm > 0) tc_producer<C>(a.wimg, ngemm, 0, a.ntiles, Ws, bars);
-    } else if (warp == 1) {
+    } else if (warp == C::CTL0 + 1) {
       if (ngemm > 0) tc_mma<C>(ngemm, a.ntiles, Ws, Bs, tbase, bars);
     }
   } else {
