@@ -64,6 +64,11 @@ __device__ __forceinline__ void bwd_st(float* p, float v) {
 #ifndef BWD_TC_POLL1
 #define BWD_TC_POLL1 0
 #endif
+// unroll of phase B's M-block loop (1: one copy of the phase-B code for both halves)
+#ifndef BWD_TC_BUNROLL
+#define BWD_TC_BUNROLL 1
+#endif
+constexpr int kBwdBUnroll = BWD_TC_BUNROLL;
 #ifndef BWD_TC_CARRY
 #define BWD_TC_CARRY 1
 #endif
@@ -72,9 +77,15 @@ __device__ __forceinline__ void bwd_st(float* p, float v) {
 constexpr int BWD_SV = 12;  // stashed values per centre: P, Dd, Z of the 4 pairs
 // TMEM stash: (MH x EG thread groups) x (centres per thread) x BWD_SV values
 #define BWD_TC_STASH(MPAD) ((BWD_TC_NEPI / 4) * (8 / (BWD_TC_NEPI / (4 * ((MPAD) / 128)))) * BWD_SV)
+// M-half pipelining of the 256-wide layers (tcmlp.cuh TcCfg::HP): phase B of M-half 0 runs
+// while the MMAs of output half 1 are in flight, and half 1's while the next layer's first group runs
+#ifndef BWD_TC_HP
+#define BWD_TC_HP 0
+#endif
+constexpr int bwd_tc_hp(int mpad) { return (BWD_TC_HP && mpad == 256) ? 1 : 0; }
 template <int MPAD>
-struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 2, BWD_TC_STASH(MPAD)> {
-  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 2, BWD_TC_STASH(MPAD)>;
+struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 2, BWD_TC_STASH(MPAD), 1, 0, 6, bwd_tc_hp(MPAD)> {
+  using B = TcCfg<MPAD, 80, BWD_TC_NEPI, 2, BWD_TC_STASH(MPAD), 1, 0, 6, bwd_tc_hp(MPAD)>;
   static constexpr int CT = 8;                                      // centres per tile
   static constexpr int OFF_SD = B::OFF_X;                           // float [2][CT][20]: seeds + x
   static constexpr int OFF_BAR = OFF_SD + 2 * CT * 20 * 4;
@@ -82,7 +93,8 @@ struct BtcCfg : TcCfg<MPAD, 80, BWD_TC_NEPI, 2, BWD_TC_STASH(MPAD)> {
 };
 
 int bwd_tc_tile_centres() { return 8; }
-int bwd_tc_acc_slots(int mpad) { return BWD_TC_NEPI / (4 * (mpad / 128)); }  // accumulator slots per CTA (EG)
+// accumulator slots per CTA: the centre groups (EG, or NEPI / 4 under M-half pipelining)
+int bwd_tc_acc_slots(int mpad) { return bwd_tc_hp(mpad) ? BWD_TC_NEPI / 4 : BWD_TC_NEPI / (4 * (mpad / 128)); }
 
 template <int ACT, int MPAD>
 __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc_kernel(const BwdArgs a) {
@@ -123,31 +135,55 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
     const int ew = warp - C::EPI0;
     const int et = tid - 32 * C::EPI0;
     const int q4 = warp & 3;
-    const int hh = (ew >> 2) % MH;
-    const int eg = ew / (4 * MH);
-    const int m = hh * 128 + 32 * q4 + lane;
-    const uint32_t taddr = tbase + ((uint32_t)(32 * q4) << 16) + hh * C::DH;
-    // this thread group's stash columns (after both halves' accumulators)
-    const uint32_t tstash = tbase + ((uint32_t)(32 * q4) << 16) + C::MH * C::DH + (hh * EG + eg) * CPE * SV;
+    // M-blocks (as in fwd_tc.cu): without M-half pipelining every warp owns one M-half and EG
+    // centre groups split the tile; with it (C::HP) every warp walks both M-halves in turn (phase
+    // B of half 0, then of half 1) and NEPI / 4 centre groups split the tile
+    constexpr bool HP = C::HP;
+    constexpr int NBLK = HP ? MH : 1;               // M-blocks per layer and thread
+    constexpr int EGX = HP ? C::NEPI / 4 : EG;      // centre groups = accumulator slots per CTA
+    constexpr int CPX = CT / EGX;                   // centres per thread and M-block
+    constexpr int NIT = NBLK * CPX;                 // (M-block, centre) items per thread and layer
+    static_assert(CT % EGX == 0 && NIT == CPE, "every thread handles CPE (neuron, centre) items per layer");
+    const int hh0 = HP ? 0 : (ew >> 2) % MH;
+    const int egx = HP ? (ew >> 2) : ew / (4 * MH);
+    auto half_of = [&](int blk) { return HP ? blk : hh0; };
+    auto m_of = [&](int blk) { return half_of(blk) * 128 + 32 * q4 + lane; };  // this thread's neuron
+    auto taddr_of = [&](int blk) -> uint32_t {
+      return tbase + ((uint32_t)(32 * q4) << 16) + half_of(blk) * C::DH;
+    };
+    // this thread's stash columns of M-block blk (after both halves' accumulators)
+    auto tstash_of = [&](int blk) -> uint32_t {
+      return tbase + ((uint32_t)(32 * q4) << 16) + C::MH * C::DH + (half_of(blk) * EGX + egx) * CPX * SV;
+    };
+    auto slot_of = [&](int i) { return egx + EGX * i; };  // centre slot of this thread's i-th centre
     const float beta = net.beta;
     const float h = a.h;
     const int64_t nrows = a.n * NCOLB;
     // this thread's accumulator slot (one per CTA and centre group): [L-1][MPAD] db |
     // dW_last [MPAD] | db_last [1] | dW_0 [MPAD][3]   (kernels.cuh bacc_size)
-    float* bacc = a.bacc + ((size_t)blockIdx.x * EG + eg) * a.nacc;
+    float* bacc = a.bacc + ((size_t)blockIdx.x * EGX + egx) * a.nacc;
     float* acc_db = bacc;
     float* acc_dWL = bacc + (size_t)(L - 1) * MPAD;
     float* acc_dbL = acc_dWL + MPAD;
     float* acc_dW0 = acc_dbL + 1;
-    // this thread's accumulators (its neuron m), summed over its tiles in tile order and
-    // written once at the end: db per hidden layer, dW_last[m], dW_0[m][:], db_last (m == 0)
-    float r_db[MAXL];
+    // this thread's accumulators (its neuron of each M-block), summed over its tiles in tile
+    // order and written once at the end: db per hidden layer, dW_last[m], dW_0[m][:], db_last (m == 0)
+    float r_db[NBLK][MAXL];
 #pragma unroll
-    for (int l = 0; l < MAXL; ++l) r_db[l] = 0.f;
-    float r_dWL = 0.f, r_dbL = 0.f, r_dW0[3] = {0.f, 0.f, 0.f};
-    // db of the top layer, accumulated by top_centre in a register (r_db, indexed by the
-    // runtime layer, lives in local memory); added to r_db[ltop] once at the end
-    float r_dbtop = 0.f;
+    for (int b = 0; b < NBLK; ++b)
+#pragma unroll
+      for (int l = 0; l < MAXL; ++l) r_db[b][l] = 0.f;
+    float r_dWL[NBLK], r_dW0[NBLK][3], r_dbtop[NBLK], r_dbL = 0.f;
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b) r_dWL[b] = r_dbtop[b] = r_dW0[b][0] = r_dW0[b][1] = r_dW0[b][2] = 0.f;
+    // += into element blk of a per-M-block register array (compile-time indices only: a runtime
+    // index would move the array to local memory)
+    auto addb = [&](float (&arr)[NBLK], int blk, float v) {
+      if (NBLK > 1 && blk)
+        arr[NBLK - 1] += v;
+      else
+        arr[0] += v;
+    };
     uint32_t nd = 0;
     PhaseTimer ptimer;
     ptimer.start();
@@ -162,7 +198,6 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
         }
       }
     };
-
 
     // per-tile seeds + coordinates, double-buffered: the next tile's are copied asynchronously
     // (cp.async) while this tile runs
@@ -180,23 +215,33 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
     load_seeds(blockIdx.x, sds0);
 
     // write delta (10 columns of centre slot cl, neuron m) as the next GEMM's B operand
-    auto put_b10 = [&](int cl, const float (&dl)[NCOLB]) {
+    auto put_b10 = [&](int m, int cl, const float (&dl)[NCOLB]) {
       FDSDF_ASSERT(cl >= 0 && cl < CT && m >= 0 && m < MPAD);
       // sw128_off(8 j + cl, m) = (m / 64) BKC + 1024 j + 128 cl + (((m % 64) / 8 ^ cl) << 4) + 2 (m % 8)
       unsigned char* bp = Bs + (m >> 6) * C::BKC + cl * 128 + ((((m & 63) >> 3) ^ cl) << 4) + ((m & 7) << 1);
+      // columns j, j+1 split together (packed bf16x2 conversions on the ALU pipe instead of
+      // scalar ones on the quarter-rate XU), each half stored at its own column
 #pragma unroll
-      for (int j = 0; j < NCOLB; ++j) {
-        const tc::Bf3 sp3 = tc::split3(dl[j]);
+      for (int j = 0; j < NCOLB; j += 2) {
+        uint32_t w[3];
+        tc::split3x2(dl[j], dl[j + 1], w);
 #pragma unroll
-        for (int p = 0; p < 3; ++p) *reinterpret_cast<__nv_bfloat16*>(bp + j * 1024 + p * C::NS * 128) = sp3.p[p];
+        for (int p = 0; p < 3; ++p) {
+          *reinterpret_cast<uint16_t*>(bp + j * 1024 + p * C::NS * 128) = (uint16_t)(w[p] & 0xFFFFu);
+          *reinterpret_cast<uint16_t*>(bp + (j + 1) * 1024 + p * C::NS * 128) = (uint16_t)(w[p] >> 16);
+        }
       }
     };
-    // the top layer l = L-2 for centre i of tile tl (seeds sdsT): X = W_{L-1}^T fbar-seeds, so
-    // delta_{L-2} needs no MMA.  Writes delta to a.del and accumulates db_{L-2} and dW_{L-1}.
+    // the top layer l = L-2 for centre i of M-block blk of tile tl (seeds sdsT): X = W_{L-1}^T
+    // fbar-seeds, so delta_{L-2} needs no MMA.  Writes delta to a.del and accumulates db_{L-2}
+    // and dW_{L-1}.
     const int ltop = L - 2;
     const bool pipe_top = BWD_TC_PIPE_TOP && ngemm > 0;
-    // this thread's last-layer weight (fan-out 1), loaded once instead of per top-layer centre
-    const float wlast = m < net.width[ltop + 1] ? net.W[L - 1][m] : 0.f;
+    // this thread's last-layer weights (fan-out 1), loaded once instead of per top-layer centre
+    float wlast[NBLK];
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b) wlast[b] = m_of(b) < net.width[ltop + 1] ? net.W[L - 1][m_of(b)] : 0.f;
+    auto wlast_of = [&](int blk) -> float { return (NBLK > 1 && blk) ? wlast[NBLK - 1] : wlast[0]; };
     // the pair maps of a centre's 4 pairs, two pairs per packed fp32 x2 lane pair, into
     // t[5 p .. 5 p + 4] = A_a, S_a, P, Dd, Z of pair p (zero on rows past the width); every lane
     // of the warp calls this (the sine maps vote on their fast form)
@@ -219,9 +264,10 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
         t[10 * k + 9] = mk ? Z[k].y : 0.f;
       }
     };
-    // this thread's stored pre-activations of top-layer centre i of tile tl (zero if none)
-    auto top_load = [&](int64_t tl, int i, float4 (&zg)[ZG]) {
-      const int64_t c = tl * CT + eg + EG * i;
+    // this thread's stored pre-activations of top-layer item (blk, i) of tile tl (zero if none)
+    auto top_load = [&](int64_t tl, int blk, int i, float4 (&zg)[ZG]) {
+      const int m = m_of(blk);
+      const int64_t c = tl * CT + slot_of(i);
 #pragma unroll
       for (int g = 0; g < ZG; ++g) zg[g] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (tl >= a.ntiles || c >= a.n || m >= net.width[ltop + 1]) return;
@@ -229,13 +275,14 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
 #pragma unroll
       for (int g = 0; g < ZG; ++g) zg[g] = __ldg(zq + g * MPAD);
     };
-    auto top_centre = [&](int64_t tl, int i, const float* sdsT, const float4 (&zg)[ZG]) {
-      const int cl = eg + EG * i;
+    auto top_centre = [&](int64_t tl, int blk, int i, const float* sdsT, const float4 (&zg)[ZG]) {
+      const int cl = slot_of(i);
       const int64_t c = tl * CT + cl;
       if (tl >= a.ntiles || c >= a.n) return;  // warp-uniform: the pair maps below vote
+      const int m = m_of(blk);
       const bool mk = m < net.width[ltop + 1];
       const float omt = net.omega[ltop];
-      const float wlt = wlast;
+      const float wlt = wlast_of(blk);
       FDSDF_ASSERT(c >= 0 && c < a.n);
       float zv[NCOLF];
 #pragma unroll
@@ -281,8 +328,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
       float v = 0.f;
 #pragma unroll
       for (int j = 0; j < NCOLB; ++j) v = fmaf(dL[j], pv[j], v);
-      r_dbtop += dl[0];
-      r_dWL += v;
+      addb(r_dbtop, blk, dl[0]);
+      addb(r_dWL, blk, v);
     };
     uint32_t spar = 0;
 #ifdef FDSDF_PHASE_TIMING
@@ -296,7 +343,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
     for (int64_t tile = blockIdx.x; tile < tend; tile += gridDim.x, spar ^= 1u) {
       const int64_t c0 = tile * CT;
       const float* const zt = a.zf + (size_t)c0 * zcs;       // zf block of the tile's first centre
-      const size_t drow0 = (size_t)c0 * NCOLB * MPAD + m;    // its first delta / activation row, + m
+      const size_t drow0 = (size_t)c0 * NCOLB * MPAD;        // its first delta / activation row
       // this tile's first MMA pass reads layer L-3; the next tile's top layer (computed during
       // this tile's passes) reads layer L-2 of that tile
       if (tile == blockIdx.x) prefetch_layer(tile, L - 3);  // later tiles: during the previous tile
@@ -312,32 +359,37 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
 #endif
       if (pipe_top) {
         // the first GEMM's B operand: delta_{L-2} of this tile, computed during the previous
-        // tile (here only for the CTA's first tile) and reloaded from a.del (this thread's writes)
+        // tile (here only for the CTA's first tile) and reloaded from a.del (this thread's
+        // writes), M-block by M-block
         if (tile == blockIdx.x)
-          for (int i = 0; i < CPE; ++i) {
+          for (int k = 0; k < NIT; ++k) {
             float4 zg[ZG];
-            top_load(tile, i, zg);
-            top_centre(tile, i, sds, zg);
+            top_load(tile, k / CPX, k % CPX, zg);
+            top_centre(tile, k / CPX, k % CPX, sds, zg);
           }
-        const bool mt = m < net.width[ltop + 1];
-        auto ldd = [&](int i, float (&d)[NCOLB]) {
-          const int64_t c = c0 + eg + EG * i;
-          const bool ok = i < CPE && c < a.n && mt;
-          const float* dp = a.del + ((size_t)ltop * nrows + (size_t)c * NCOLB) * MPAD + m;
 #pragma unroll
-          for (int j = 0; j < NCOLB; ++j) d[j] = ok ? dp[j * MPAD] : 0.f;
-        };
-        float dn[NCOLB];
-        ldd(0, dn);
+        for (int blk = 0; blk < NBLK; ++blk) {
+          const int m = m_of(blk);
+          const bool mt = m < net.width[ltop + 1];
+          auto ldd = [&](int i, float (&d)[NCOLB]) {
+            const int64_t c = c0 + slot_of(i);
+            const bool ok = i < CPX && c < a.n && mt;
+            const float* dp = a.del + ((size_t)ltop * nrows + (size_t)c * NCOLB) * MPAD + m;
+#pragma unroll
+            for (int j = 0; j < NCOLB; ++j) d[j] = ok ? dp[j * MPAD] : 0.f;
+          };
+          float dn[NCOLB];
+          ldd(0, dn);
 #pragma unroll 1
-        for (int i = 0; i < CPE; ++i) {
-          float dl[NCOLB];
+          for (int i = 0; i < CPX; ++i) {
+            float dl[NCOLB];
 #pragma unroll
-          for (int j = 0; j < NCOLB; ++j) dl[j] = dn[j];
-          ldd(i + 1, dn);
-          put_b10(eg + EG * i, dl);
+            for (int j = 0; j < NCOLB; ++j) dl[j] = dn[j];
+            ldd(i + 1, dn);
+            put_b10(m, slot_of(i), dl);
+          }
+          tc_epi_arrive(bars, HP ? blk : 0);
         }
-        tc_epi_arrive(bars);
       }
 #ifdef FDSDF_PHASE_TIMING
       t_tstart += clock64() - t_ts0;
@@ -347,28 +399,27 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
       for (int l = pipe_top ? L - 3 : L - 2; l >= 0; --l) {
         const bool top = (l == L - 2);
         const int M = net.width[l + 1];
-        const bool mok = m < M;
-        // omega_l: in the image of the GEMM that produced X (pack_tc_kernel), or (top layer without
-        // an MMA) in its last-layer weight
-        const float wl = (top && mok) ? wlast * net.omega[l] : 0.f;
-        float s_db = 0.f, s_vL = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
-        const float db_l = r_db[l];  // local-memory read issued here, consumed after phase B
+        float s_vL[NBLK];
+#pragma unroll
+        for (int b = 0; b < NBLK; ++b) s_vL[b] = 0.f;
         constexpr bool CARRY = BWD_TC_CARRY;
-        float c_s1[CPE], c_s2tr[CPE];  // CARRY: sigma'(z), sigma''(z) (r . t) per centre of this thread
+        float c_s1[NIT], c_s2tr[NIT];  // CARRY: sigma'(z), sigma''(z) (r . t) per item of this thread
         // the next pass's phase A: layer l - 1 of this tile, or the next tile's first GEMM layer
         if (!top) prefetch_layer(l > 0 ? tile : tile + gridDim.x, l > 0 ? l - 1 : L - 3);
         // ---- phase A (X-independent, overlaps this layer's MMA): the pair maps of every
-        // centre of this thread -- A_a, S_a and the derivative factors P, Dd, Z -- from the
+        // item of this thread -- A_a, S_a and the derivative factors P, Dd, Z -- from the
         // stored forward pre-activations, stashed in this thread's TMEM lane
         struct Zq {
           float z, t0, t1, t2, A[4], S[4];
         };
-        auto ldq = [&](int i) -> Zq {
+        auto ldq = [&](int k) -> Zq {
           Zq q{};
-          const int64_t c = c0 + eg + EG * i;
-          if (i < CPE && c < a.n && mok) {
+          const int blk = k / CPX, i = k % CPX;
+          const int m = m_of(blk);
+          const int64_t c = c0 + slot_of(i);
+          if (k < NIT && c < a.n && m < M) {
             FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
-            const float4* zq = reinterpret_cast<const float4*>(zt + (eg + EG * i) * zcs + l * ZCS_L) + m;
+            const float4* zq = reinterpret_cast<const float4*>(zt + slot_of(i) * zcs + l * ZCS_L) + m;
             FDSDF_ASSERT((const float*)zq == a.zf + ((size_t)c * nh + l) * NCOLF * MPAD + 4 * m);
             const float4 g0 = __ldg(zq), g1 = __ldg(zq + MPAD), g2 = __ldg(zq + 2 * MPAD);
             q.z = g0.x;
@@ -389,10 +440,13 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
         {
           Zq qn = ldq(0);
 #pragma unroll kBwdUnroll
-          for (int i = 0; i < CPE; ++i) {
+          for (int k = 0; k < NIT; ++k) {
             const Zq q = qn;
-            qn = ldq(i + 1);
-            const int cl = eg + EG * i;
+            qn = ldq(k + 1);
+            const int blk = k / CPX, i = k % CPX;
+            const int m = m_of(blk);
+            const bool mok = m < M;
+            const int cl = slot_of(i);
             const int64_t c = c0 + cl;
             const bool valid = c < a.n;
             float t[20];
@@ -425,13 +479,13 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
               }
             }
             if (CARRY) {
-              c_s1[i] = cs1;
-              c_s2tr[i] = cs2tr;
+              c_s1[k] = cs1;
+              c_s2tr[k] = cs2tr;
             }
             {
               if (valid && l <= L - 3) {
                 FDSDF_ASSERT(c >= 0 && c < a.n && l >= 0 && l < nh);
-                float* ap = a.actv + (size_t)l * nrows * MPAD + drow0 + cl * (NCOLB * MPAD);
+                float* ap = a.actv + (size_t)l * nrows * MPAD + drow0 + cl * (NCOLB * MPAD) + m;
                 FDSDF_ASSERT(ap == a.actv + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m);
 #pragma unroll
                 for (int j = 0; j < NCOLB; ++j) bwd_st(ap + j * MPAD, pv[j]);
@@ -442,18 +496,18 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
                 float v = 0.f;
 #pragma unroll
                 for (int j = 0; j < NCOLB; ++j) v = fmaf(dL[j], pv[j], v);
-                s_vL += v;
+                addb(s_vL, blk, v);
               }
               // stash P, Dd, Z of the four pairs
               float v4[4];
 #pragma unroll
-              for (int k = 0; k < 3; ++k) {
+              for (int kk = 0; kk < 3; ++kk) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  const int e = 4 * k + j;  // (pair e / 3, factor e % 3)
+                  const int e = 4 * kk + j;  // (pair e / 3, factor e % 3)
                   v4[j] = t[5 * (e / 3) + 2 + e % 3];
                 }
-                tc::tmem_st4(tstash + i * SV + 4 * k, v4);
+                tc::tmem_st4(tstash_of(blk) + i * SV + 4 * kk, v4);
               }
             }
           }
@@ -462,178 +516,199 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
 #ifdef FDSDF_PHASE_TIMING
         const long long t_pa1 = clock64();
 #endif
-        if (pipe_top) {  // the next tile's top layer, its centres spread over this tile's MMA phases
+        if (pipe_top) {  // the next tile's top layer, its items spread over this tile's MMA phases
           const int g = L - 3 - l;
           if (g == 0) {
             cp_async_wait_all();
             bar_named(1, C::NEPI * 32);  // the next tile's seeds are in
           }
 #pragma unroll 1
-          for (int i = g; i < CPE; i += ngemm) {
+          for (int k = g; k < NIT; k += ngemm) {
             float4 zg[ZG];
-            top_load(tile + gridDim.x, i, zg);
-            top_centre(tile + gridDim.x, i, sds_next, zg);
+            top_load(tile + gridDim.x, k / CPX, k % CPX, zg);
+            top_centre(tile + gridDim.x, k / CPX, k % CPX, sds_next, zg);
           }
         }
 #ifdef FDSDF_PHASE_TIMING
         t_top += clock64() - t_pa1;
 #endif
-        // ---- phase B (after the MMA): combine with the adjoint X
-        auto ldz = [&](int i, float (&z4)[4]) {
-          const int64_t c = c0 + eg + EG * i;
-          z4[0] = z4[1] = z4[2] = z4[3] = 0.f;
-          if (!CARRY && i < CPE && c < a.n && mok) {
-            const float4 g0 = __ldg(reinterpret_cast<const float4*>(zt + (eg + EG * i) * zcs + l * ZCS_L) + m);
-            z4[0] = g0.x;
-            z4[1] = g0.y;
-            z4[2] = g0.z;
-            z4[3] = g0.w;
-          }
-        };
-        float zn[4];
-        ldz(0, zn);
-        // CARRY values of the next centre, read one centre ahead (local memory)
-        float cs1n = CARRY ? c_s1[0] : 0.f, cs2n = CARRY ? c_s2tr[0] : 0.f;
-        if (!top) {
-          ptimer.before_wait();
-          if (BWD_TC_POLL1) {  // one warp polls, the others sleep in a hardware named barrier
-            if (et < 32) mbar_wait(bars.dfull, nd & 1u);
-            bar_named(2, C::NEPI * 32);
-          } else {
-            mbar_wait(bars.dfull, nd & 1u);
-          }
-          ptimer.after_wait();
-          ++nd;
-          tc::fence_after();
-        }
-#pragma unroll kBwdUnroll
-        for (int i = 0; i < CPE; ++i) {
-          const int cl = eg + EG * i;
-          const int64_t c = c0 + cl;
-          const bool valid = c < a.n;
-          const float zc[4] = {zn[0], zn[1], zn[2], zn[3]};
-          ldz(i + 1, zn);
-          const float cs1 = cs1n, cs2 = cs2n;
-          if (CARRY && i + 1 < CPE) {
-            cs1n = c_s1[i + 1];
-            cs2n = c_s2tr[i + 1];
-          }
-          const float* sd = sds + cl * 20;
-          float X[NCOLB];
-          if (top) {
-            const float dL[NCOLB] = {sd[0], valid ? 1.f : 0.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
-#pragma unroll
-            for (int j = 0; j < NCOLB; ++j) X[j] = wl * dL[j];
-          } else {  // the two accumulator ranges, columns cl + 8 j
-            tc::tmem_ld10x2_stride8(taddr + cl, taddr + C::NS + cl, X);
-          }
-          float t[20];  // per pair: A_a, S_a, P, Dd, Z (only P, Dd, Z are stashed / used here)
-          {
-            float v4[4];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              tc::tmem_ld4(tstash + i * SV + 4 * k, v4);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int e = 4 * k + j;
-                t[5 * (e / 3) + 2 + e % 3] = v4[j];
-              }
+        // ---- phase B (after the MMA), M-block by M-block: combine with the adjoint X
+#pragma unroll kBwdBUnroll
+        for (int blk = 0; blk < NBLK; ++blk) {
+          const int m = m_of(blk);
+          const bool mok = m < M;
+          // omega_l: in the image of the GEMM that produced X (pack_tc_kernel), or (top layer
+          // without an MMA) in its last-layer weight
+          const float wl = (top && mok) ? wlast_of(blk) * net.omega[l] : 0.f;
+          const uint32_t taddr = taddr_of(blk);
+          const uint32_t tstash = tstash_of(blk);
+          float s_db = 0.f, s_w0[3] = {0.f, 0.f, 0.f};
+          const float db_l = r_db[blk][l];  // local-memory read issued here, consumed after phase B
+          auto ldz = [&](int i, float (&z4)[4]) {
+            const int64_t c = c0 + slot_of(i);
+            z4[0] = z4[1] = z4[2] = z4[3] = 0.f;
+            if (!CARRY && i < CPX && c < a.n && mok) {
+              const float4 g0 = __ldg(reinterpret_cast<const float4*>(zt + slot_of(i) * zcs + l * ZCS_L) + m);
+              z4[0] = g0.x;
+              z4[1] = g0.y;
+              z4[2] = g0.z;
+              z4[3] = g0.w;
             }
-#pragma unroll
-            for (int p = 0; p < 4; ++p) t[5 * p] = t[5 * p + 1] = 0.f;
-          }
-          const float r0 = sd[5], r1 = sd[6], r2 = sd[7];
-          const float u0 = sd[8], u1 = sd[9], u2 = sd[10], v0 = sd[11], v1 = sd[12], v2_ = sd[13];
-          float dl[NCOLB];
-#pragma unroll
-          for (int j = 0; j < NCOLB; ++j) dl[j] = 0.f;
-          float w0p[3] = {0.f, 0.f, 0.f};
-          if (mok && valid) {
-            float tr = 0.f, s1, s2tr;
-            typename AF::C cc{};
-            if (CARRY) {
-              s1 = cs1;
-              s2tr = cs2;
+          };
+          float zn[4];
+          ldz(0, zn);
+          if (!top) {
+            ptimer.before_wait();
+            if (BWD_TC_POLL1) {  // one warp polls, the others sleep in a hardware named barrier
+              if (et < 32) mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
+              bar_named(2, C::NEPI * 32);
             } else {
-              tr = fmaf(r0, zc[1], fmaf(r1, zc[2], r2 * zc[3]));
-              cc = AF::centre(zc[0], beta);
-              s1 = AF::d1(cc, beta);
-              s2tr = AF::d2(cc, beta) * tr;
+              mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
             }
-            float zbar = 0.f;
+            ptimer.after_wait();
+            tc::fence_after();
+          }
+          // HP: the B rows of K half 0 may still be read by the layer's (1, 0) MMA group --
+          // wait for "B free" before this M-block's first B store
+          if (HP && blk == 0 && l >= 1) mbar_wait(bars.bfree, nd & 1u);
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              const float P = t[5 * p + 2], Dd = t[5 * p + 3], Z = t[5 * p + 4];
-              const float XA = X[2 + 2 * p], XS = X[3 + 2 * p];
-              const float dA = fmaf(XA, P, 2.0f * XS * Dd);
-              const float dS = fmaf(0.5f * XA, Dd, XS * P);
-              zbar = fmaf(XA, Dd, fmaf(XS, Z, zbar));
-              dl[2 + 2 * p] = dA;
-              dl[3 + 2 * p] = dS;
-              if (l == 0) {  // a^{-1} of pair columns: A -> h d_p, S -> 0
-                const float dpx = p == 0 ? u0 : (p == 1 ? v0 : (p == 2 ? u0 + v0 : u0 - v0));
-                const float dpy = p == 0 ? u1 : (p == 1 ? v1 : (p == 2 ? u1 + v1 : u1 - v1));
-                const float dpz = p == 0 ? u2 : (p == 1 ? v2_ : (p == 2 ? u2 + v2_ : u2 - v2_));
-                w0p[0] = fmaf(dA, h * dpx, w0p[0]);
-                w0p[1] = fmaf(dA, h * dpy, w0p[1]);
-                w0p[2] = fmaf(dA, h * dpz, w0p[2]);
+          for (int i = 0; i < CPX; ++i) {
+            const int k = blk * CPX + i;
+            const int cl = slot_of(i);
+            const int64_t c = c0 + cl;
+            const bool valid = c < a.n;
+            const float zc[4] = {zn[0], zn[1], zn[2], zn[3]};
+            ldz(i + 1, zn);
+            const float cs1 = CARRY ? c_s1[k] : 0.f, cs2 = CARRY ? c_s2tr[k] : 0.f;
+            const float* sd = sds + cl * 20;
+            float X[NCOLB];
+            if (top) {
+              const float dL[NCOLB] = {sd[0], valid ? 1.f : 0.f, 0.f, sd[1], 0.f, sd[2], 0.f, sd[3], 0.f, sd[4]};
+#pragma unroll
+              for (int j = 0; j < NCOLB; ++j) X[j] = wl * dL[j];
+            } else {  // the two accumulator ranges, columns cl + 8 j
+              tc::tmem_ld10x2_stride8(taddr + cl, taddr + C::NS + cl, X);
+            }
+            float t[20];  // per pair: A_a, S_a, P, Dd, Z (only P, Dd, Z are stashed / used here)
+            {
+              float v4[4];
+#pragma unroll
+              for (int kk = 0; kk < 3; ++kk) {
+                tc::tmem_ld4(tstash + i * SV + 4 * kk, v4);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const int e = 4 * kk + j;
+                  t[5 * (e / 3) + 2 + e % 3] = v4[j];
+                }
+              }
+#pragma unroll
+              for (int p = 0; p < 4; ++p) t[5 * p] = t[5 * p + 1] = 0.f;
+            }
+            const float r0 = sd[5], r1 = sd[6], r2 = sd[7];
+            const float u0 = sd[8], u1 = sd[9], u2 = sd[10], v0 = sd[11], v1 = sd[12], v2_ = sd[13];
+            float dl[NCOLB];
+#pragma unroll
+            for (int j = 0; j < NCOLB; ++j) dl[j] = 0.f;
+            float w0p[3] = {0.f, 0.f, 0.f};
+            if (mok && valid) {
+              float tr = 0.f, s1, s2tr;
+              typename AF::C cc{};
+              if (CARRY) {
+                s1 = cs1;
+                s2tr = cs2;
+              } else {
+                tr = fmaf(r0, zc[1], fmaf(r1, zc[2], r2 * zc[3]));
+                cc = AF::centre(zc[0], beta);
+                s1 = AF::d1(cc, beta);
+                s2tr = AF::d2(cc, beta) * tr;
+              }
+              float zbar = 0.f;
+#pragma unroll
+              for (int p = 0; p < 4; ++p) {
+                const float P = t[5 * p + 2], Dd = t[5 * p + 3], Z = t[5 * p + 4];
+                const float XA = X[2 + 2 * p], XS = X[3 + 2 * p];
+                const float dA = fmaf(XA, P, 2.0f * XS * Dd);
+                const float dS = fmaf(0.5f * XA, Dd, XS * P);
+                zbar = fmaf(XA, Dd, fmaf(XS, Z, zbar));
+                dl[2 + 2 * p] = dA;
+                dl[3 + 2 * p] = dS;
+                if (l == 0) {  // a^{-1} of pair columns: A -> h d_p, S -> 0
+                  const float dpx = p == 0 ? u0 : (p == 1 ? v0 : (p == 2 ? u0 + v0 : u0 - v0));
+                  const float dpy = p == 0 ? u1 : (p == 1 ? v1 : (p == 2 ? u1 + v1 : u1 - v1));
+                  const float dpz = p == 0 ? u2 : (p == 1 ? v2_ : (p == 2 ? u2 + v2_ : u2 - v2_));
+                  w0p[0] = fmaf(dA, h * dpx, w0p[0]);
+                  w0p[1] = fmaf(dA, h * dpy, w0p[1]);
+                  w0p[2] = fmaf(dA, h * dpz, w0p[2]);
+                }
+              }
+              const float Xc = X[0], Xt = X[1];
+              const float zb = fmaf(Xc, s1, fmaf(s2tr, Xt, zbar));
+              dl[0] = zb;
+              dl[1] = s1 * Xt;
+              if (l == 0) {  // a^{-1}: centre -> x0, tangent -> r
+                w0p[0] = fmaf(dl[0], sd[16], fmaf(dl[1], r0, w0p[0]));
+                w0p[1] = fmaf(dl[0], sd[17], fmaf(dl[1], r1, w0p[1]));
+                w0p[2] = fmaf(dl[0], sd[18], fmaf(dl[1], r2, w0p[2]));
               }
             }
-            const float Xc = X[0], Xt = X[1];
-            const float zb = fmaf(Xc, s1, fmaf(s2tr, Xt, zbar));
-            dl[0] = zb;
-            dl[1] = s1 * Xt;
-            if (l == 0) {  // a^{-1}: centre -> x0, tangent -> r
-              w0p[0] = fmaf(dl[0], sd[16], fmaf(dl[1], r0, w0p[0]));
-              w0p[1] = fmaf(dl[0], sd[17], fmaf(dl[1], r1, w0p[1]));
-              w0p[2] = fmaf(dl[0], sd[18], fmaf(dl[1], r2, w0p[2]));
-            }
-          }
-          if (valid) {
-            if (l >= 1) {
-              FDSDF_ASSERT(c >= 0 && c < a.n && l >= 1 && l < nh);
-              float* dp = a.del + (size_t)l * nrows * MPAD + drow0 + cl * (NCOLB * MPAD);
-              FDSDF_ASSERT(dp == a.del + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m);
+            if (valid) {
+              if (l >= 1) {
+                FDSDF_ASSERT(c >= 0 && c < a.n && l >= 1 && l < nh);
+                float* dp = a.del + (size_t)l * nrows * MPAD + drow0 + cl * (NCOLB * MPAD) + m;
+                FDSDF_ASSERT(dp == a.del + ((size_t)l * nrows + (size_t)c * NCOLB) * MPAD + m);
 #pragma unroll
-              for (int j = 0; j < NCOLB; ++j) bwd_st(dp + j * MPAD, dl[j]);
+                for (int j = 0; j < NCOLB; ++j) bwd_st(dp + j * MPAD, dl[j]);
+              }
+            }
+            if (l >= 1) put_b10(m, cl, dl);
+            s_db += dl[0];
+            if (l == 0) {
+              s_w0[0] += w0p[0];
+              s_w0[1] += w0p[1];
+              s_w0[2] += w0p[2];
             }
           }
-          if (l >= 1) put_b10(cl, dl);
-          s_db += dl[0];
-          if (l == 0) {
-            s_w0[0] += w0p[0];
-            s_w0[1] += w0p[1];
-            s_w0[2] += w0p[2];
+          if (!top) ptimer.end_b();
+          if (l >= 1) {
+            tc_epi_arrive(bars, HP ? blk : 0);
+          } else if (!top) {
+            tc::fence_before();
           }
-        }
-        if (!top) ptimer.end_b();
-        if (l >= 1) {
-          tc_epi_arrive(bars);
-        } else if (!top) {
-          tc::fence_before();
-        }
-        r_db[l] = db_l + s_db;
-        if (top) r_dWL += s_vL;
-        if (l == 0) {
-          r_dW0[0] += s_w0[0];
-          r_dW0[1] += s_w0[1];
-          r_dW0[2] += s_w0[2];
+          r_db[blk][l] = db_l + s_db;
+          if (l == 0) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              if (NBLK > 1 && blk)
+                r_dW0[NBLK - 1][d] += s_w0[d];
+              else
+                r_dW0[0][d] += s_w0[d];
+            }
+          }
+        }  // M-block
+        if (!top) ++nd;
+        if (top) {
+#pragma unroll
+          for (int b = 0; b < NBLK; ++b) r_dWL[b] += s_vL[b];
         }
       }
-      if (m == 0) {  // bias of the last layer: sum of the centre seeds (fbar) of this group
+      if (m_of(0) == 0) {  // bias of the last layer: sum of the centre seeds (fbar) of this group
         float v = 0.f;
-        for (int i = 0; i < CPE; ++i) v += sds[(eg + EG * i) * 20 + 0];
+        for (int i = 0; i < CPX; ++i) v += sds[slot_of(i) * 20 + 0];
         r_dbL += v;
       }
     }
-    r_db[ltop] += r_dbtop;
     // write this thread's slots (every element of the slot is owned by exactly one thread)
-    for (int l = 0; l <= L - 2; ++l) acc_db[(size_t)l * MPAD + m] = r_db[l];
-    acc_dWL[m] = r_dWL;
-    acc_dW0[m * 3 + 0] = r_dW0[0];
-    acc_dW0[m * 3 + 1] = r_dW0[1];
-    acc_dW0[m * 3 + 2] = r_dW0[2];
-    if (m == 0) acc_dbL[0] = r_dbL;
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b) {
+      const int m = m_of(b);
+      r_db[b][ltop] += r_dbtop[b];
+      for (int l = 0; l <= L - 2; ++l) acc_db[(size_t)l * MPAD + m] = r_db[b][l];
+      acc_dWL[m] = r_dWL[b];
+      acc_dW0[m * 3 + 0] = r_dW0[b][0];
+      acc_dW0[m * 3 + 1] = r_dW0[b][1];
+      acc_dW0[m * 3 + 2] = r_dW0[b][2];
+    }
+    if (m_of(0) == 0) acc_dbL[0] = r_dbL;
 #ifdef FDSDF_PHASE_TIMING
     if (blockIdx.x == 0 && (et == 0 || et == C::NEPI * 32 - 32))
       printf("[phase] bwd_tc (thread %d): tile-start phase %.0f cyc/tile, next-tile top work %.0f cyc/tile\n", (int)threadIdx.x,
@@ -641,6 +716,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
 #endif
     ptimer.report("bwd_tc", et == 0 || et == C::NEPI * 32 - 32);
   }
+
   tc_teardown<C>(tbase);
 }
 

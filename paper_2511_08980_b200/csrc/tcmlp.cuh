@@ -88,7 +88,7 @@ struct TcCfg {
   static constexpr int STAGE = WPS * 128 * 128;        // weight stage in shared memory
   static constexpr int NST = WPS == 1 ? NST_ : 2;  // ring depth in stages
   static_assert(WPS == 1 || WPS == 3, "whole blocks or single pieces");
-  static constexpr int MC = FDSDF_WMC ? 2 : 1;  // CTAs sharing the weight stream (cluster size)
+  static constexpr int MC = (FDSDF_WMC && !HP_) ? 2 : 1;  // CTAs sharing the weight stream (cluster size)
   static constexpr int BPIECE = N * MPAD * 2;   // one bf16 piece of the B operand
   static constexpr int BKC = 3 * N * 128;       // one K chunk of B
   // column splits: the tile's N columns are NSPLIT independent MMA passes of NS columns each,
