@@ -64,6 +64,10 @@ __device__ __forceinline__ void bwd_st(float* p, float v) {
 #ifndef BWD_TC_POLL1
 #define BWD_TC_POLL1 0
 #endif
+// back-off between the per-warp polls (ns; 0 = try_wait with a suspend-time hint only)
+#ifndef BWD_TC_POLL_NS
+#define BWD_TC_POLL_NS 0
+#endif
 // unroll of phase B's M-block loop (1: one copy of the phase-B code for both halves)
 #ifndef BWD_TC_BUNROLL
 #define BWD_TC_BUNROLL 1
@@ -563,7 +567,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(BtcCfg<MPAD>::NTHR, 1) bwd_tc
               if (et < 32) mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
               bar_named(2, C::NEPI * 32);
             } else {
-              mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
+              mbar_wait_sleep<BWD_TC_POLL_NS>(&bars.dfull[HP ? blk : 0], nd & 1u);
             }
             ptimer.after_wait();
             tc::fence_after();

@@ -86,6 +86,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// poll with a fixed __nanosleep between polls (ns > 0): for many warps waiting on the same
+// phase, so their polls do not take the issue slots of the warps still working
+template <int NS>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  if (NS <= 0) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  while (!mbar_try_wait(bar, parity)) __nanosleep(NS);
+}
+
 // the same with a __nanosleep back-off between polls: for the long waits of the single-thread
 // roles (producer, MMA issuer), whose polling shares a scheduler with epilogue warps
 #ifndef FDSDF_WAIT_BACKOFF_NS

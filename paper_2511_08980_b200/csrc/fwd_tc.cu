@@ -34,6 +34,10 @@ namespace fdsdf {
 #ifndef FWD_TC_POLLALL
 #define FWD_TC_POLLALL 1
 #endif
+// back-off between those polls (ns; 0 = try_wait with a suspend-time hint only)
+#ifndef FWD_TC_POLL_NS
+#define FWD_TC_POLL_NS 0
+#endif
 // M-half pipelining of the 256-wide layers (tcmlp.cuh TcCfg::HP): 1 = on
 #ifndef FWD_TC_HP
 #define FWD_TC_HP 1
@@ -543,7 +547,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
               // one warp polls the mbarrier, the others sleep in a hardware named barrier (no
               // spin instructions competing with the MMA warp for issue slots)
               if (FWD_TC_POLLALL) {  // every warp waits for itself (no wait for the slowest warp)
-                mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
+                mbar_wait_sleep<FWD_TC_POLL_NS>(&bars.dfull[HP ? blk : 0], nd & 1u);
               } else {
                 if (ew == 0) mbar_wait(&bars.dfull[HP ? blk : 0], nd & 1u);
                 bar_named(2, C::NEPI * 32);
