@@ -385,10 +385,14 @@ def measure_c5(args, spec, local, rank, world, dev, stream, flush, barrier):
 
 def measure_recon(args, model, cfg, stream):
     """The paper's experiment in kind (§4) on the synthetic CSG shape: train the
-    SIREN (Trainer: 20k of a 30k surface pool + 20k box points per iteration, FD-NCR + eikonal +
-    Dirichlet, Adam 5e-5) for --recon-iters iterations, then extract the zero level set on a 128^3
-    grid (fdsdf_eval_field + marching tetrahedra) and score it against 30k held-out ground-truth
-    samples with normals: CD x10^3, F1 x10^2 (tau = 0.005), NC x10^2 -- at init and after training."""
+    SIREN (Trainer: 20k of a 30k surface pool + 20k box points per iteration, Adam 5e-5) for
+    --recon-iters iterations with and without the FD curvature term, then extract the zero level
+    set on a 128^3 grid (fdsdf_eval_field + marching tetrahedra) and score it against 30k held-out
+    ground-truth samples with normals: CD x10^3, F1 x10^2 (tau = 0.005), NC x10^2.
+    Loss (DESIGN.md §2 item 22): the SIREN originals' weights ("hyperparameters follow the
+    originals": Dirichlet 3e3, DNM 1e2 with alpha 1e2, eikonal 5e1), lambda_fd = 10 (inside the
+    paper's stable range, Table tab:ablation_weights) and ||grad f|| -> 1 in every
+    curvature denominator (the P:L131 replacement applied to all centres)."""
     import torch
     from harness import csg_surface, csg_surface_normals
     from paper_2511_08980_b200.fdsdf import Trainer, fdsdf_mesh_metrics
@@ -397,34 +401,41 @@ def measure_recon(args, model, cfg, stream):
     pool = csg_surface(int(ns * 1.5), 3, 100).astype(np.float32)
     G, Gn = csg_surface_normals(30_000, 3, 77)
     G, Gn = torch.from_numpy(G).to(dev), torch.from_numpy(Gn).to(dev)
-    # the full Eq. (1) with SPEC's defaults: the non-manifold term keeps the untrained SIREN
-    # from leaving zero crossings in free space (the headline C2 step uses BASELINE's loss list)
-    lc = dict(cfg["loss"], lambda_dnm=100.0)
-    tr = Trainer(model, cfg["params"], pool, ns, len(cfg["x"]) - ns, 1.1, cfg["h"], lc, seed=4)
     res = 128
 
-    def score():
+    def score(params):
         t0 = time.perf_counter()
-        tris, _ = model.extract_mesh(tr.params, res, stream=stream)
+        tris, _ = model.extract_mesh(params, res, stream=stream)
         mm = fdsdf_mesh_metrics(tris, G, Gn, nsample=100_000, seed=1, tau=0.005, stream=stream)
         torch.cuda.synchronize()
         return {"cd_x1e3": mm["cd"] * 1e3, "f1_x1e2": mm["f1"] * 1e2, "nc_x1e2": mm["nc"] * 1e2,
                 "hausdorff": mm["hausdorff"], "triangles": int(tris.shape[0]),
                 "extract_and_score_s": time.perf_counter() - t0}
 
-    init = score()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.recon_iters):
-        tr.iterate(stream)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    final = score()
+    def train(lambda_fd):
+        lc = dict(cfg["loss"], w_dm=3000.0, lambda_dnm=100.0, alpha_dnm=100.0, lambda_eik=50.0,
+                  lambda_fd=float(lambda_fd), denom="one")
+        tr = Trainer(model, cfg["params"], pool, ns, len(cfg["x"]) - ns, 1.1, cfg["h"], lc, seed=4, lr=5e-5)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.recon_iters):
+            tr.iterate(stream)
+        torch.cuda.synchronize()
+        return tr.params, time.perf_counter() - t0
+
+    init = score(cfg["params"])
+    p_fd, dt = train(10.0)
+    final = score(p_fd)
+    p_base, _ = train(0.0)
+    base = score(p_base)
     return {"iterations": args.recon_iters, "wall_s": dt, "ms_per_iteration_wall": dt * 1e3 / args.recon_iters,
-            "grid": f"{res}^3 over [-1,1]^3", "metrics_at_init": init, "metrics_after": final,
+            "grid": f"{res}^3 over [-1,1]^3",
+            "loss": "w_dm 3e3, lambda_dnm 1e2 (alpha 1e2), lambda_eik 5e1, lambda_fd 10 (FD-NCR), ||grad f|| -> 1 "
+                    "in the denominators, Adam 5e-5",
+            "metrics_at_init": init, "metrics_after": final, "metrics_after_without_fd_term": base,
             "ground_truth": "30k held-out CSG surface samples with normals (harness.csg_surface_normals)",
-            "note": "synthetic CSG stand-in for the ABC meshes (DESIGN.md §3); the paper trains ~5-9k iterations "
-                    "with CD-based early stopping (P:L153)"}
+            "note": "synthetic CSG stand-in for the ABC meshes (DESIGN.md §3); the paper trains to CD-based early "
+                    "stopping (P:L153); the without-fd run is the same training with lambda_fd = 0"}
 
 
 def setup_comm(model, world, rank, dev):
