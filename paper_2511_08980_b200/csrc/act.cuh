@@ -44,6 +44,15 @@ struct Act<ACT_SINE> {
     sincos_acc(z, &c.sz, &c.cz);
     return c;
   }
+  // the centre terms of two centres at once (packed sincos: bitwise centre() of each)
+  __device__ __forceinline__ static void centre2(float za, float zb, float /*beta*/, C& ca, C& cb) {
+    float2 sv, cv;
+    sincos_acc2(make_float2(za, zb), &sv, &cv);
+    ca.sz = sv.x;
+    ca.cz = cv.x;
+    cb.sz = sv.y;
+    cb.cz = cv.y;
+  }
   __device__ __forceinline__ static float value(const C& c, float) { return c.sz; }
   __device__ __forceinline__ static float d1(const C& c, float) { return c.cz; }
   __device__ __forceinline__ static float d2(const C& c, float) { return -c.sz; }
@@ -254,6 +263,10 @@ struct Act<ACT_SOFTPLUS> {
     c.t = beta * z;
     logistic2(c.t, &c.s0, &c.s0m);
     return c;
+  }
+  __device__ __forceinline__ static void centre2(float za, float zb, float beta, C& ca, C& cb) {
+    ca = centre(za, beta);
+    cb = centre(zb, beta);
   }
   __device__ __forceinline__ static float value(const C& c, float beta) { return softplus_acc(c.t) / beta; }
   __device__ __forceinline__ static float d1(const C& c, float) { return c.s0; }

@@ -172,6 +172,31 @@ __device__ __forceinline__ void sincos_acc(float x, float* s, float* c) {
   *c = cv;
 }
 
+// sincos_acc of two arguments at once (packed fp32 x2 for the reduction and the polynomials:
+// per lane exactly the scalar arithmetic, so bitwise sincos_acc of each)
+__device__ __forceinline__ void sincos_acc2(float2 x, float2* s, float2* c) {
+  const float2 kx = mul2(x, f2s(0.636619772367581343f));
+  const float2 k = make_float2(rintf(kx.x), rintf(kx.y));
+  const float2 nk = make_float2(-k.x, -k.y);
+  float2 r = fma2(nk, f2s(1.5707963705062866f), x);
+  r = fma2(nk, f2s(-4.371138828673793e-08f), r);
+  r = fma2(nk, f2s(-1.7763568394002505e-15f), r);
+  const float2 z = mul2(r, r);
+  float2 ps = fma2(fma2(f2s(-1.9515295891e-4f), z, f2s(8.3321608736e-3f)), z, f2s(-1.6666654611e-1f));
+  ps = fma2(mul2(ps, z), r, r);
+  float2 pc = fma2(fma2(f2s(2.443315711809948e-5f), z, f2s(-1.388731625493765e-3f)), z, f2s(4.166664568298827e-2f));
+  pc = fma2(mul2(pc, z), z, fma2(f2s(-0.5f), z, f2s(1.0f)));
+  const int qa = static_cast<int>(k.x), qb = static_cast<int>(k.y);
+  float sa = (qa & 1) ? pc.x : ps.x, ca = (qa & 1) ? ps.x : pc.x;
+  float sb = (qb & 1) ? pc.y : ps.y, cb = (qb & 1) ? ps.y : pc.y;
+  if (qa & 2) sa = -sa;
+  if ((qa + 1) & 2) ca = -ca;
+  if (qb & 2) sb = -sb;
+  if ((qb + 1) & 2) cb = -cb;
+  *s = make_float2(sa, sb);
+  *c = make_float2(ca, cb);
+}
+
 // sincos for the small arguments of the pair maps (A/2, S/4): most are below 2^-4, where a
 // short Taylor polynomial is exact to fp32 rounding; |x| <= pi/4 needs no range reduction
 // (k = 0, r = x: the sincos_acc polynomial alone); larger |x| (rare) take the full path.

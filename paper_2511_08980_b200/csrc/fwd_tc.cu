@@ -294,8 +294,8 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
     // next layer's 8 B columns of the centre in the order A0 A1 S0 S1 A2 A3 S2 S3 (kPairCol: the
     // accumulator columns come back in that order, i.e. already packed by two); every lane calls
     // this (the sine maps vote on their fast form); rows past the width give 0
-    auto pair_outputs = [&](float z0, bool mok, const float2 (&A2)[2], const float2 (&S2)[2], float (&o)[8]) {
-      const typename AF::C cc = AF::centre(z0, beta);
+    auto pair_outputs = [&](const typename AF::C& cc, bool mok, const float2 (&A2)[2], const float2 (&S2)[2],
+                            float (&o)[8]) {
       float2 Aa[2], Sa[2];
       AF::pairs_fwd4x2(cc, A2, S2, beta, Aa, Sa);
 #pragma unroll
@@ -384,7 +384,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
           *zg4(zb, c, 0, 2, m) = make_float4(A2[1].x, A2[1].y, S2[1].x, S2[1].y);
         }
         float o[8];
-        pair_outputs(z0, mok, A2, S2, o);
+        pair_outputs(AF::centre(z0, beta), mok, A2, S2, o);
         skip_pairs(0, m, ci, o);
         float o4[4] = {o[0], o[1], o[2], o[3]};
         tc::tmem_st4(tstash + i * CPC, o4);
@@ -541,7 +541,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
               const int64_t c = c0 + cl;
               return (MODE == 2 && cl < CT && c < a.n) ? __ldg(zc(zt + cl * zcs, c, l, m)) : 0.f;
             };
-            float z0n = ldz(egx);
+            float z0n = ldz(egx);  // mode 2: prefetched one centre ahead (the first before the MMA wait)
             if (l > 0) {
               ptimer.before_wait();
               // one warp polls the mbarrier, the others sleep in a hardware named barrier (no
@@ -558,63 +558,78 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
             // HP: the B rows of K half 0 may still be read by the layer's (1, 0) MMA group --
             // wait for "B free" before this M-block's first B store
             bool need_free = HP && blk == 0 && l > 0 && !last;
-            auto centre_body = [&](const int cl, const float z0) {
+            // cc0: mode 2, the centre terms sigma(z0), sigma'(z0) of the centre (two centres' sincos
+            // evaluated together, packed)
+            // mode 1, per centre: the accumulator -> z, tangents (-> zf), then (with the centre
+            // terms of two centres evaluated together, packed) the outputs -> next B / last layer
+            struct M1 {
+              float z, t0, t1, t2;
+            };
+            auto m1_pre = [&](const int cl) -> M1 {
               const int64_t c = c0 + cl;
               const bool valid = c < a.n;
-                if constexpr (MODE == 1) {
-                float z = 0.f, t0 = 0.f, t1 = 0.f, t2 = 0.f;
-                if (l == 0) {
-                  float x0 = 0.f, x1 = 0.f, x2 = 0.f;
-                  if (valid) {
-                    x0 = a.x[c * 3 + 0];
-                    x1 = a.x[c * 3 + 1];
-                    x2 = a.x[c * 3 + 2];
-                    if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
-                  }
-                  if (mok) {
-                    const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
-                    z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0of(blk));
-                    t0 = om * w0;
-                    t1 = om * w1;
-                    t2 = om * w2;
-                  }
-                } else {
-                  float v[4];
-                  tc_ld_sum4<C>(taddr, cl * 4, v);  // centre cl's 4 columns
-                  if (mok) {
-                    z = v[0] + bias_l;
-                    t0 = v[1];
-                    t1 = v[2];
-                    t2 = v[3];
-                  }
-                }
+              M1 q{0.f, 0.f, 0.f, 0.f};
+              if (l == 0) {
+                float x0 = 0.f, x1 = 0.f, x2 = 0.f;
                 if (valid) {
-                  if (step)
-                    *zg4(zt + cl * zcs, c, l, 0, m) = make_float4(z, t0, t1, t2);
-                  else
-                    *zc(zt + cl * zcs, c, l, m) = z;
+                  x0 = a.x[c * 3 + 0];
+                  x1 = a.x[c * 3 + 1];
+                  x2 = a.x[c * 3 + 2];
+                  if (m == 0 && !(isfinite(x0) && isfinite(x1) && isfinite(x2))) atomicOr(a.dflags, 1u);
                 }
-                float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
                 if (mok) {
-                  const typename AF::C cc = AF::centre(z, beta);
-                  const float s1 = AF::d1(cc, beta);
-                  o0 = AF::value(cc, beta);
-                  o1 = s1 * t0;
-                  o2 = s1 * t1;
-                  o3 = s1 * t2;
-                }
-                skip_centre(l, m, c, valid, o0, o1, o2, o3);
-                if (last) {
-                  reduce4(blk, cl, wl, o0, o1, o2, o3);
-                } else {
-                  const float o4[4] = {o0, o1, o2, o3};
-                  if (need_free) {
-                    mbar_wait(bars.bfree, nd & 1u);
-                    need_free = false;
-                  }
-                  put_b4(cl * 4, m, o4);
+                  const float w0 = w0of(blk, 0), w1 = w0of(blk, 1), w2 = w0of(blk, 2);
+                  q.z = om * (fmaf(w0, x0, fmaf(w1, x1, w2 * x2)) + b0of(blk));
+                  q.t0 = om * w0;
+                  q.t1 = om * w1;
+                  q.t2 = om * w2;
                 }
               } else {
+                float v[4];
+                tc_ld_sum4<C>(taddr, cl * 4, v);  // centre cl's 4 columns
+                if (mok) {
+                  q.z = v[0] + bias_l;
+                  q.t0 = v[1];
+                  q.t1 = v[2];
+                  q.t2 = v[3];
+                }
+              }
+              if (valid) {
+                if (step)
+                  *zg4(zt + cl * zcs, c, l, 0, m) = make_float4(q.z, q.t0, q.t1, q.t2);
+                else
+                  *zc(zt + cl * zcs, c, l, m) = q.z;
+              }
+              return q;
+            };
+            auto m1_post = [&](const int cl, const typename AF::C& cc, const M1& q) {
+              const int64_t c = c0 + cl;
+              const bool valid = c < a.n;
+              float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+              if (mok) {
+                const float s1 = AF::d1(cc, beta);
+                o0 = AF::value(cc, beta);
+                o1 = s1 * q.t0;
+                o2 = s1 * q.t1;
+                o3 = s1 * q.t2;
+              }
+              skip_centre(l, m, c, valid, o0, o1, o2, o3);
+              if (last) {
+                reduce4(blk, cl, wl, o0, o1, o2, o3);
+              } else {
+                const float o4[4] = {o0, o1, o2, o3};
+                if (need_free) {
+                  mbar_wait(bars.bfree, nd & 1u);
+                  need_free = false;
+                }
+                put_b4(cl * 4, m, o4);
+              }
+            };
+            // mode 2, per centre; cc0 = the centre terms sigma(z0), sigma'(z0) of the centre
+            auto centre_body = [&](const int cl, const typename AF::C& cc0) {
+              const int64_t c = c0 + cl;
+              const bool valid = c < a.n;
+              if constexpr (MODE == 2) {
                 const float* ci = cis + cl * NCINFO;
                 float2 A2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, S2[2] = {A2[0], A2[0]};
                 if (l == 0) {
@@ -642,7 +657,7 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
                   *zg4(zb, c, l, 2, m) = make_float4(A2[1].x, A2[1].y, S2[1].x, S2[1].y);
                 }
                 float o[8];
-                pair_outputs(z0, mok, A2, S2, o);
+                pair_outputs(cc0, mok, A2, S2, o);
                 skip_pairs(l, m, ci, o);
                 if (last) {
                   reduce4(blk, cl, wl, o[2], o[3], o[6], o[7]);
@@ -656,12 +671,25 @@ __global__ void FDSDF_TC_CLUSTER __launch_bounds__(FtcCfg<MPAD, MODE>::NTHR, 1) 
               }
             };
             {
+              if constexpr (MODE == 1) {
 #pragma unroll kFwdUnroll
-              for (int i = 0; i < CPX; ++i) {
-                const int cl = egx + EGX * i;  // centre slot in the tile
-                const float z0 = z0n;
-                z0n = ldz(cl + EGX);
-                centre_body(cl, z0);
+                for (int i = 0; i < CPX; i += 2) {
+                  static_assert(CPX % 2 == 0, "centres of a thread and M-block come in pairs");
+                  const int cla = egx + EGX * i, clb = egx + EGX * (i + 1);  // centre slots in the tile
+                  const M1 qa = m1_pre(cla), qb = m1_pre(clb);
+                  typename AF::C cc[2];
+                  AF::centre2(qa.z, qb.z, beta, cc[0], cc[1]);
+                  m1_post(cla, cc[0], qa);
+                  m1_post(clb, cc[1], qb);
+                }
+              } else {  // (packing two centres' sincos here measured 1-2% slower)
+#pragma unroll kFwdUnroll
+                for (int i = 0; i < CPX; ++i) {
+                  const int cl = egx + EGX * i;  // centre slot in the tile
+                  const float z0 = z0n;
+                  z0n = ldz(cl + EGX);
+                  centre_body(cl, AF::centre(z0, beta));
+                }
               }
             }
             if (l > 0) ptimer.end_b();
