@@ -524,7 +524,12 @@ __device__ __forceinline__ void tc_ld_sum4(uint32_t taddr, int col, float (&v)[4
   const uint32_t t0 = taddr + sp * 3 * C::NS + nl;
   tc::tmem_ld4x3(t0, t0 + C::NS, t0 + 2 * C::NS, v, r1, r2);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) v[j] += r1[j] + r2[j];
+  for (int j = 0; j < 4; j += 2) {  // v + (r1 + r2), two columns per packed add
+    const float2 q = add2(make_float2(r1[j], r1[j + 1]), make_float2(r2[j], r2[j + 1]));
+    const float2 o = add2(make_float2(v[j], v[j + 1]), q);
+    v[j] = o.x;
+    v[j + 1] = o.y;
+  }
 }
 
 template <class C>

@@ -21,6 +21,13 @@
 
 namespace fdsdf {
 
+// stage depth along j and ring depth (the ring holds NST * JC / 16 K steps: 2 x 32 or 4 x 16)
+#ifndef WGRAD_TC_JC
+#define WGRAD_TC_JC 32
+#endif
+#ifndef WGRAD_TC_NST
+#define WGRAD_TC_NST 2
+#endif
 // NPROD: bf16 piece products per MAC -- 6 = bf16x6 (fp32-accurate, the default);
 // 3 = a0 b0 + a0 b1 + a1 b0 (FDSDF_CREATE_WGRAD_BF16X3: each product to ~3 * 2^-16 relative; the
 // third pieces are neither split nor stored)
@@ -28,12 +35,12 @@ template <int MPAD>
 struct WtcCfg {
   static constexpr int BW = MPAD > 256 ? 256 : MPAD;  // output block edge
   static constexpr int NB = MPAD / BW;              // blocks per edge
-  static constexpr int JC = 32;                     // j per stage (4 swizzle atoms along K)
+  static constexpr int JC = WGRAD_TC_JC;            // j per stage (JC / 8 swizzle atoms along K)
   static constexpr int MH = BW / 128;
   static constexpr int PIECE = BW * JC * 2;         // one bf16 piece of one operand chunk
   static constexpr int OPER = 3 * PIECE;            // one operand chunk (3 pieces)
   static constexpr int STAGE = 2 * OPER;            // delta chunk + a chunk
-  static constexpr int NST = 2;
+  static constexpr int NST = WGRAD_TC_NST;
   static constexpr int KSTRIDE = (BW / 64) * 1024;  // byte stride between swizzle atoms along K
   static constexpr int NSTG = 16;                   // stager warps
   static constexpr int NTHR = (1 + NSTG) * 32;
