@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NTH, 2) bwd_kernel(const BwdArgs a) {
 template <int ACT, int MPAD>
 static cudaError_t launch_bwd_t(const BwdArgs& a, int grid, cudaStream_t st) {
   const size_t smem = BwdSmem<MPAD>::BYTES;
-  cudaError_t e = cudaFuncSetAttribute(bwd_kernel<ACT, MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr_once<bwd_kernel<ACT, MPAD>>((int)smem);
   if (e != cudaSuccess) return e;
   bwd_kernel<ACT, MPAD><<<grid, NTH, smem, st>>>(a);
   return cudaGetLastError();

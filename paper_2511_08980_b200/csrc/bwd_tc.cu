@@ -728,7 +728,7 @@ template <int ACT, int MPAD>
 static cudaError_t launch_bwd_tc_t(const BwdArgs& a, int grid, cudaStream_t st) {
   using C = BtcCfg<MPAD>;
   auto k = bwd_tc_kernel<ACT, MPAD>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  cudaError_t e = smem_attr_once<bwd_tc_kernel<ACT, MPAD>>(C::BYTES);
   if (e != cudaSuccess) return e;
   k<<<grid, C::NTHR, C::BYTES, st>>>(a);
   return cudaGetLastError();

@@ -548,7 +548,7 @@ static cudaError_t launch_bwdl_tc_t(const BwdArgs& a, int l, int grid, cudaStrea
   using C = BlCfg<MPAD, PAIR>;
   auto k = bwdl_tc_kernel<ACT, MPAD, PAIR>;
   if (PAIR && (grid & 1)) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  cudaError_t e = smem_attr_once<bwdl_tc_kernel<ACT, MPAD, PAIR>>(C::BYTES);
   if (e != cudaSuccess) return e;
   CUtensorMap tm{};
   if (l < a.net.L - 2) {

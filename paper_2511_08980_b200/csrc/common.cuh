@@ -140,6 +140,22 @@ __device__ __forceinline__ void bar_compute(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+// ----------------------------------------------------------------------------- launch helpers
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel K, device): the attribute
+// persists on the device, and setting it before every launch cost a driver call per launch on the
+// step's host-side enqueue path
+template <auto K>
+inline cudaError_t smem_attr_once(int bytes) {
+  static unsigned long long done = 0;  // bit d: set on device d
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done |= bit;
+  return e;
+}
+
 // ----------------------------------------------------------------------------- packed fp32 x2
 // sm_100 FFMA2 / FADD2 / FMUL2: two independent fp32 lanes per instruction, each rounded exactly
 // as the scalar instruction would (so a packed evaluation is bitwise the scalar one); half the

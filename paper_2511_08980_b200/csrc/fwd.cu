@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(NTH, 2) fwd_kernel(const FwdArgs a) {
 template <int ACT, int MPAD>
 static cudaError_t launch_fwd_t(const FwdArgs& a, int grid, cudaStream_t st) {
   const size_t smem = FwdSmem<MPAD>::BYTES;
-  cudaError_t e = cudaFuncSetAttribute(fwd_kernel<ACT, MPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_attr_once<fwd_kernel<ACT, MPAD>>((int)smem);
   if (e != cudaSuccess) return e;
   fwd_kernel<ACT, MPAD><<<grid, NTH, smem, st>>>(a);
   return cudaGetLastError();

@@ -731,7 +731,7 @@ template <int ACT, int MPAD, int MODE>
 static cudaError_t launch_fwd_tc_t(const FwdArgs& a, int grid, cudaStream_t st) {
   using C = FtcCfg<MPAD, MODE>;
   auto k = fwd_tc_kernel<ACT, MPAD, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  cudaError_t e = smem_attr_once<fwd_tc_kernel<ACT, MPAD, MODE>>(C::BYTES);
   if (e != cudaSuccess) return e;
   k<<<grid, C::NTHR, C::BYTES, st>>>(a);
   return cudaGetLastError();

@@ -213,8 +213,7 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
 template <int MPAD, int NPROD>
 static cudaError_t launch_wgrad_tc_t(const WgradArgs& a, int nglayers, cudaStream_t st) {
   using C = WtcCfg<MPAD>;
-  cudaError_t e =
-      cudaFuncSetAttribute(wgrad_tc_kernel<MPAD, NPROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+  cudaError_t e = smem_attr_once<wgrad_tc_kernel<MPAD, NPROD>>(C::BYTES);
   if (e != cudaSuccess) return e;
   wgrad_tc_kernel<MPAD, NPROD><<<dim3(a.nsplit * C::NB * C::NB, nglayers), C::NTHR, C::BYTES, st>>>(a);
   return cudaGetLastError();
