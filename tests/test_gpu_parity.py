@@ -64,20 +64,22 @@ def test_eval_parity_given_frames(name, ns, nu, h, path):
     assert err["mask"] == 0
 
 
-@pytest.mark.parametrize("name,ns,nu", [("c1", 1024, 1024), ("c2", 200, 200)])
-def test_eval_parity_self_framed(name, ns, nu, path):
+@pytest.mark.parametrize("name,ns,nu,h", [("c1", 1024, 1024, 1e-2), ("c2", 200, 200, 1e-2), ("c2", 200, 200, None)])
+def test_eval_parity_self_framed(name, ns, nu, h, path):
     """End-to-end: the GPU draws its own frame from its fp32 gradient; the oracle from its
-    fp64 gradient with the same counter-based SplitMix64 angle."""
-    c = make_config(name, ns, nu, h=1e-2)
+    fp64 gradient with the same counter-based SplitMix64 angle (h = None: the config's own h,
+    5e-3 for C2).  Every output, D and K included."""
+    c = make_config(name, ns, nu, h=h)
     m = _model(c["spec"], len(c["x"]), eval_only=True, path=path)
     g = gpu_eval(m, c)
     o = ref_eval(c["spec"], c["params"], c["x"], c["n_surface"], c["h"], frame_seed=c["frame_seed"])
     fr = np.concatenate([o["u"], o["v"]], 1)
     assert np.max(np.abs(g["frames"] - fr)) < 1e-3
     err = compare_eval(g, o)
-    print(name, {k: float(v) for k, v in err.items()})
-    for k in ("f", "g", "fuu", "fuv", "fvv"):
+    print(name, h, {k: float(v) for k, v in err.items()})
+    for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K"):
         assert err[k] <= 1.0, (k, err)
+    assert err["mask"] == 0
 
 
 STEP_CASES = [
