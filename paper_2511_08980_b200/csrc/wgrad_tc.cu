@@ -137,15 +137,11 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
       const int layer = a.first_layer + li;
       const float* D = a.del + (size_t)layer * a.stride_layer + bm * BW;
       const float* A = a.actv + (size_t)(layer - 1) * a.stride_layer + bn * BW;
-      for (int ch = 0; ch < nchunk; ++ch, ++it) {
-        const int s = (int)(it % NST);
-        mbar_wait(&sempty[s], ((it / NST) & 1u) ^ 1u);
-        unsigned char* dst = sm + s * C::STAGE;
+      // the chunk's float4 loads of delta and a, issued one chunk ahead of their split (the
+      // global-load latency of chunk ch+1 overlaps the split and stores of chunk ch)
+      constexpr int NIT = JC * QUADS / (C::NSTG * 32);
+      auto load_chunk = [&](int ch, float4 (&dv)[NIT], float4 (&av)[NIT]) {
         const int64_t jb = j0 + (int64_t)ch * JC;
-        // all loads of this thread's items first (8 float4 of delta + 8 of a in flight), then
-        // split and store
-        constexpr int NIT = JC * QUADS / (C::NSTG * 32);
-        float4 dv[NIT], av[NIT];
 #pragma unroll
         for (int q = 0; q < NIT; ++q) {
           const int item = st + q * C::NSTG * 32;
@@ -153,12 +149,21 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
           const int64_t j = jb + jj;
           dv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           av[q] = dv[q];
-          if (j < j1) {
+          if (ch < nchunk && j < j1) {
             FDSDF_ASSERT(j >= 0 && j < a.rows && r + 4 <= BW && layer >= 1);
             dv[q] = __ldg(reinterpret_cast<const float4*>(D + j * MPAD + r));
             av[q] = __ldg(reinterpret_cast<const float4*>(A + j * MPAD + r));
           }
         }
+      };
+      float4 dv[NIT], av[NIT];
+      load_chunk(0, dv, av);
+      for (int ch = 0; ch < nchunk; ++ch, ++it) {
+        const int s = (int)(it % NST);
+        float4 dn[NIT], an[NIT];
+        load_chunk(ch + 1, dn, an);
+        mbar_wait(&sempty[s], ((it / NST) & 1u) ^ 1u);
+        unsigned char* dst = sm + s * C::STAGE;
 #pragma unroll
         for (int q = 0; q < NIT; ++q) {
           const int item = st + q * C::NSTG * 32;
@@ -179,6 +184,11 @@ __global__ void __launch_bounds__(WtcCfg<MPAD>::NTHR, 1) wgrad_tc_kernel(const W
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sfull[s]);
+#pragma unroll
+        for (int q = 0; q < NIT; ++q) {
+          dv[q] = dn[q];
+          av[q] = an[q];
+        }
       }
       // readback of this layer's partial: warp sw -> lane quarter (warp % 4), halves (sw / 4) + 4i
       mbar_wait(dfull, 0u);
