@@ -88,6 +88,29 @@ def p_mm(spec):
     return sum(o * i for o, i in sh), sum(o * i for o, i in sh[1:-1])
 
 
+def pipe_peak(path, dev_index=0, sm_max_mhz=1965.0):
+    """The contraction pipe's ceiling in TFLOP/s of fp32-accurate arithmetic:
+    tensor / hybrid path = measured dense bf16 / 6 (bf16x6), FFMA path = SMs x 128 lanes x 2 x clock."""
+    if path == "ffma":
+        import torch
+        nsm = torch.cuda.get_device_properties(dev_index).multi_processor_count
+        return nsm * FP32_LANES_PER_SM * 2 * sm_max_mhz * 1e6 / 1e12, "alu"
+    return measured_bf16_peak()[0] / 6.0, "tensor"
+
+
+def roofline_of(alg_flops, ms, path, dev_index, clocks):
+    """algorithmic TFLOP/s of a timed region against the pipe ceiling, with the
+    fraction at the SM clock sampled during the region beside it"""
+    sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak, bound = pipe_peak(path, dev_index, sm_max)
+    ach = alg_flops / (ms * 1e-3) / 1e12
+    out = {"bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
+    if clocks is not None:
+        out["clocks"] = clocks
+        out["frac_at_run_clock"] = ach / (peak * clocks["sm_mhz"] / sm_max) if clocks.get("sm_mhz") else None
+    return out
+
+
 # ----------------------------------------------------------------------------- clocks
 
 
@@ -329,10 +352,20 @@ def measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank
             o = em.eval(pdev, xi, nn // 2, cfg["h"], frame_seed=0, stream=stream)
             for i in range(2):
                 em.eval(pdev, xi, nn // 2, cfg["h"], frame_seed=i, stream=stream, outputs=o)
-            reps = 5 if nn <= 1_000_000 else 2
+            # >= 1e6 centres (SURVEY §8d's eval target): enough repetitions to sample the SM clock
+            reps = 5 if nn < 1_000_000 else (12 if nn == 1_000_000 else (4 if nn == 3_000_000 else 2))
+            clk = None
+            if nn >= 1_000_000:
+                clk = ClockSampler(dev.index)
+                clk.start()
+                time.sleep(0.15)
             ms_s = _event_ms(stream, lambda i: em.eval(pdev, xi, nn // 2, cfg["h"], frame_seed=i, stream=stream,
                                                       outputs=o), reps, flush)
-            sweep.append({"centres": nn, "ms": ms_s, "stencil_points_per_s": 9.0 * nn / (ms_s * 1e-3)})
+            P_mm_e = p_mm(cfg["spec"])[0]
+            # eval: 20 P_mm algorithmic flops per centre (9 forward values + 1 reverse sweep)
+            sweep.append({"centres": nn, "ms": ms_s, "stencil_points_per_s": 9.0 * nn / (ms_s * 1e-3),
+                          "roofline": roofline_of(20.0 * P_mm_e * nn, ms_s, em.path, dev.index,
+                                                  clk.stop() if clk else None)})
         em.close()
         out["eval_sweep"] = sweep
     return out
@@ -371,16 +404,23 @@ def measure_c5(args, spec, local, rank, world, dev, stream, flush, barrier):
         step(i)
     barrier()
     k = max(3, min(args.steps, 10))
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.2)
     ms = _event_ms(stream, lambda i: step(args.warmup + i), k, flush)
+    clocks = clk.stop()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ok = bool(np.isfinite(lo.cpu().numpy()[4]))
+    P_mm, P_gemm = p_mm(spec)
+    # whole-step algorithmic flops per GPU: (16 + 4 + 20) P_mm + 20 P_gemm per centre
+    roof = roofline_of((40.0 * P_mm + 20.0 * P_gemm) * n, ms, m.path, local, clocks)
     m.close()
     return {"workload": c["config_json"]["workload"], "centres_per_gpu": n, "global_centres": n * world,
             "steps": k, "ms_per_step": ms, "steps_per_s": 1e3 / ms, "value": 9.0 * n * world / (ms * 1e-3),
-            "unit": UNIT, "finite_loss": ok, "collective": coll}
+            "unit": UNIT, "finite_loss": ok, "collective": coll, "roofline_step": roof}
 
 
 def measure_recon(args, model, cfg, stream):
