@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfdsdf.so")
 BUILD = os.path.join(ROOT, "build")
 SOURCES = ["api.cu", "fwd.cu", "bwd.cu", "wgrad.cu", "tcprobe.cu", "fwd_tc.cu", "bwd_tc.cu", "wgrad_tc.cu", "train.cu", "bwdl_tc.cu", "mesh.cu"]
-HEADERS = ["common.cuh", "act.cuh", "tile.cuh", "kernels.cuh", "tc.cuh", "fdepi.cuh", "tcmlp.cuh"]
+HEADERS = ["common.cuh", "act.cuh", "tile.cuh", "kernels.cuh", "tc.cuh", "fdepi.cuh", "tcmlp.cuh", "tcpair.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("FDSDF_NVCC_EXTRA", "").split()  # debug builds only (e.g. -DFDSDF_PHASE_TIMING)
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
