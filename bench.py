@@ -115,7 +115,9 @@ def roofline_of(alg_flops, ms, path, dev_index, clocks):
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clock and throttle reasons DURING the timed region."""
+    """nvidia-smi sampling (every 20 ms) of SM clock, board power and throttle reasons DURING the
+    timed region: start() launches the sampler, mark() (called right before the region, after the
+    sampler's start-up) discards what came before, stop() summarises the samples since mark()."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -126,12 +128,13 @@ class ClockSampler:
         self.proc = None
         self.lines = []
         self.thread = None
+        self.first = 0
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
@@ -141,6 +144,9 @@ class ClockSampler:
     def _read(self):
         for ln in self.proc.stdout:
             self.lines.append(ln.strip())
+
+    def mark(self):
+        self.first = len(self.lines)
 
     def stop(self):
         if self.proc is None:
@@ -153,7 +159,7 @@ class ClockSampler:
         self.thread.join(timeout=2)
         sm, pw, smax, reasons = [], [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for ln in self.lines[self.first:]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -364,6 +370,7 @@ def measure_extras(args, model, cfg, params, stream, flush, barrier, world, rank
                 clk = ClockSampler(dev.index)
                 clk.start()
                 time.sleep(0.15)
+                clk.mark()
             ms_s = _event_ms(stream, lambda i: em.eval(pdev, xi, nn // 2, cfg["h"], frame_seed=i, stream=stream,
                                                       outputs=o), reps, flush)
             P_mm_e = p_mm(cfg["spec"])[0]
@@ -412,6 +419,7 @@ def measure_c5(args, spec, local, rank, world, dev, stream, flush, barrier):
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.2)
+    clk.mark()
     ms = _event_ms(stream, lambda i: step(args.warmup + i), k, flush)
     clocks = clk.stop()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -594,6 +602,7 @@ def main():
     clk.start()
     time.sleep(0.3)
     barrier()
+    clk.mark()
     wall0 = time.perf_counter()
     for i in range(args.steps):
         flush.zero_()
@@ -730,6 +739,7 @@ def main():
         clk2 = ClockSampler(local)
         clk2.start()
         time.sleep(0.2)
+        clk2.mark()
         ms_sus = _event_ms(stream, lambda i: one_step(args.warmup + i), ks, flush)
         cl2 = clk2.stop()
         ts = torch.tensor([ms_sus], dtype=torch.float64, device=dev)
