@@ -134,7 +134,8 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("FDSDF_BENCH_SMI_MS", "20")], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
