@@ -613,7 +613,10 @@ def main():
     barrier()
     wall = time.perf_counter() - wall0
     clocks = clk.stop()
-    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    t_ms = sum(per_step)
+    k3 = max(1, args.steps // 3)  # the region's first and last third (this rank): the power limiter's drift
+    drift = {"first_third_ms": sum(per_step[:k3]) / k3, "last_third_ms": sum(per_step[-k3:]) / k3}
     tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -828,7 +831,7 @@ def main():
             "precision": ("bf16x6: fp32 operands split exactly into 3 bf16 pieces, 6 tcgen05 products, fp32 "
                           "accumulation" if path == "tensor" else "fp32 FFMA"), "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps), "clocks": clocks, **extras,
-            "collective": collective, "c5": c5, "sustained": sustained,
+            "collective": collective, "c5": c5, "sustained": sustained, "ms_per_step_drift": drift,
             "wall_s_timed_region": wall,
         }
         print(json.dumps(line), flush=True)
