@@ -7,6 +7,7 @@ tensor-core path, one CTA per SM over all tiles).
  * C5 (data-parallel shard, 200k centres): eval entries on 3000 sampled rows; the step's loss and
    gradient against the oracle accumulated over 20k-row chunks with the global counts (the
    loss and gradient are sums of per-centre terms).
+ * C5e (the eval sweep's 10^6-centre size, eval-only context): 512 sampled rows against the C oracle.
  * C4 h sweep (2e-2 .. 2.5e-3): BJ fixes the 1e-4 gate at h = 1e-2; the difference form
     keeps every entry inside that same gate at every h of the sweep (measured
    worst: 0.29 of the gate at h = 2.5e-3), so the test applies it unscaled.
@@ -184,4 +185,40 @@ def test_c3_step_parity_first_rows():
         assert np.all(gerr <= GRAD_RTOL), gerr
         if path is not None:
             mm.close()
+    m.close()
+
+
+def test_c5e_eval_sweep_size_sampled():
+    """C5e (SURVEY §8d's eval target, the bench's `eval_sweep`): fdsdf_eval over 10^6 centres on an
+    eval-only context, as bench.py runs it (C2's network, half CSG surface / half uniform rows,
+    h = 5e-3) -- 512 sampled rows (the first and the last tile included) against the C oracle with
+    the GPU's exported frames; the frames themselves must be orthonormal, right-handed and
+    tangent to the oracle's gradient on every sampled row, and every output finite on all rows."""
+    from harness import csg_surface, uniform_box
+    c = make_config("c2", 64, 64)  # network, parameters, h of the sweep; the points are replaced below
+    n = 1_000_000
+    x = np.concatenate([csg_surface(n // 2, 3, 7), uniform_box(n - n // 2, 1.1, 8)]).astype(np.float32)
+    ns = n // 2
+    m = _model(c["spec"], n, eval_only=True)
+    o = m.eval(c["params"], x, ns, c["h"], frame_seed=0)
+    ev = {k: v.cpu().numpy() for k, v in o.items()}
+    for k in ("f", "g", "hess", "D", "K", "frames"):
+        assert np.isfinite(ev[k]).all(), k
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([np.arange(8), np.arange(n - 8, n), [ns - 1, ns], rng.choice(n, 494, replace=False)]))
+    sub = {k: v[idx] for k, v in ev.items()}
+    fr = sub["frames"]
+    surf = idx < ns
+    ref = ref_eval(c["spec"], c["params"], x[idx], int(surf.sum()), c["h"], frames=(fr[:, :3], fr[:, 3:]))
+    err = compare_eval(sub, ref)
+    print("c5e 1e6-centre sampled eval errors", {k: float(v) for k, v in err.items()})
+    assert all(err[k] <= 1.0 for k in ("f", "g", "fuu", "fuv", "fvv", "D", "K")), err
+    assert err["mask"] == 0
+    # the exported frames: orthonormal, right-handed, tangent to the oracle's normal
+    u, v = fr[:, :3].astype(np.float64), fr[:, 3:].astype(np.float64)
+    nrm = ref["g"] / np.linalg.norm(ref["g"], axis=1, keepdims=True)
+    assert np.abs(np.linalg.norm(u, axis=1) - 1).max() < 1e-5 and np.abs(np.linalg.norm(v, axis=1) - 1).max() < 1e-5
+    assert np.abs((u * v).sum(1)).max() < 1e-5
+    assert np.abs((u * nrm).sum(1)).max() < 1e-4 and np.abs((v * nrm).sum(1)).max() < 1e-4
+    assert ((np.cross(u, v) * nrm).sum(1) > 0.999).all()
     m.close()
