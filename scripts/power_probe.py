@@ -1,6 +1,6 @@
 """Debug: SM clock, power draw and throttle reasons (nvidia-smi, 20 ms sampling) while the C2 step
 runs back to back for a few seconds, with and without the bench's L2 flush between steps.
-usage (under gpurun): python scripts/power_probe.py [seconds]"""
+usage (under gpurun): python scripts/power_probe.py [seconds] [wgrad3]   (wgrad3: the opt-in 3-product weight gradient)"""
 import subprocess
 import sys
 import threading
@@ -14,7 +14,7 @@ from paper_2511_08980_b200 import FDSDF  # noqa: E402
 
 secs = float(sys.argv[1]) if len(sys.argv) > 1 else 3.0
 c = make_config("c2")
-m = FDSDF(c["spec"], 0, max_centers=len(c["x"]))
+m = FDSDF(c["spec"], 0, max_centers=len(c["x"]), wgrad_bf16x3="wgrad3" in sys.argv[2:])
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 F = "clocks.sm,power.draw,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_thermal_slowdown"
 
